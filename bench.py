@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""bench.py -- effective TFLOPS of the vector-wise N:M SpMM hot path on B200.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W` prints ONE
+JSON line on rank 0.  A "step" is one pass of the hot path over one batch:
+  N = 1 : nm_spmm(A, B', D) -> C  (one launch of our kernel);
+  N > 1 : column-sharded: each rank runs nm_spmm on its slice of
+          the column groups, C is assembled with an NCCL all-gather and our
+          unshard kernel (strong scaling: the problem size is fixed).
+Metric (BASELINE.json): effective TFLOPS = 2*m*n*w / t, w = k*N/M (kept MACs
+only), plus speedup over cuBLAS dense GEMM of the same shape and dtype
+on the same GPU.  Inputs are resident in HBM when the timed region starts;
+L2 is flushed (256 MiB write) between timed steps, outside the CUDA events.
+
+`--impl reference` times the CPU oracle (oracle/, the only other place this
+file executes it) on a bounded row sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (m, n, k, N, M, L)   -- BASELINE.json configs
+    "cfg1": (256, 256, 256, 2, 4, 4),
+    "cfg2": (4096, 4096, 4096, 16, 32, 32),
+    "cfg3_62": (2048, 11008, 4096, 12, 32, 32),
+    "cfg3_75": (2048, 11008, 4096, 8, 32, 32),
+    "cfg4_13b": (2048, 13824, 5120, 4, 32, 32),
+    "cfg4_65b": (2048, 22016, 8192, 4, 32, 32),
+}
+HEADLINE = "cfg2"
+VARIANTS = ["cfg3_62", "cfg3_75", "cfg4_65b"]
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def fp32_alu_peak_tflops(sm_mhz: float, sms: int = 148) -> float:
+    # FP32 FFMA: 128 lanes/SM x 2 FLOP x SMs x clock
+    return sms * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+# ----------------------------------------------------------------------- clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap", 0x1: "gpu_idle", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                try:
+                    r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except AttributeError:
+                    r = self.nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------- inputs
+def make_inputs(cfg, dtype, device, seed=0):
+    import torch
+    from paper_2503_01253_b200 import nmspmm, synth
+    m, n, k, N, M, L = cfg
+    gen = synth.uniform if dtype == torch.float32 else synth.bf16grid
+    A = torch.from_numpy(gen((m, k), seed + 1, synth.TID_A)).to(device=device, dtype=dtype)
+    Bd = torch.from_numpy(gen((k, n), seed + 2, synth.TID_B)).to(device=device, dtype=dtype)
+    W = nmspmm.nm_compress(Bd, N, M, L)  # magnitude pruning on the device (offline, untimed)
+    return A, Bd, W
+
+
+def time_steps(fn, steps, warmup, stream, flush=None):
+    """W untimed warm-ups, then `steps` steps each bracketed by CUDA events on
+    `stream` (L2 flush between steps, outside the events).  Returns per-step ms."""
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for s, e in ev:
+            if flush is not None:
+                flush()
+            s.record(stream)
+            fn()
+            e.record(stream)
+    torch.cuda.synchronize()
+    return [s.elapsed_time(e) for s, e in ev]
+
+
+def flop_count(cfg):
+    m, n, k, N, M, L = cfg
+    return 2.0 * m * n * (k // M * N)
+
+
+def alg_bytes(cfg, e):
+    m, n, k, N, M, L = cfg
+    w, q = k // M * N, n // L
+    return e * m * k + e * w * n + w * q + e * m * n
+
+
+def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True):
+    import torch
+    from paper_2503_01253_b200 import nmspmm
+    stream = torch.cuda.current_stream()
+    A, Bd, W = make_inputs(cfg, dtype, "cuda")
+    C = torch.empty(cfg[0], cfg[1], dtype=dtype, device="cuda")
+    math = "f32_simt" if dtype == torch.float32 else "auto"
+    ms = time_steps(lambda: nmspmm.nm_spmm(A, W, out=C, math=math), steps, warmup, stream, flush)
+    t = statistics.median(ms)
+    res = {"ms": t, "ms_mean": statistics.fmean(ms), "tflops": flop_count(cfg) / (t * 1e-3) / 1e12,
+           "plan": nmspmm.nm_plan_query(*cfg, dtype=dtype, math=math)}
+    if with_cublas:
+        torch.backends.cuda.matmul.allow_tf32 = False
+        Cd = torch.empty_like(C)
+        msd = time_steps(lambda: torch.mm(A, Bd, out=Cd), steps, warmup, stream, flush)
+        td = statistics.median(msd)
+        m, n, k = cfg[:3]
+        res.update({"cublas_ms": td, "cublas_dense_tflops": 2.0 * m * n * k / (td * 1e-3) / 1e12,
+                    "speedup_vs_cublas": td / t, "target_speedup": 0.7 * cfg[4] / cfg[3]})
+    del A, Bd, W, C
+    return res, ms
+
+
+def e2e_measure(cfg, dtype, steps, warmup):
+    """Same metric through nm_spmm_host (host pinned buffers; H2D + kernel + D2H timed)."""
+    import torch
+    from paper_2503_01253_b200 import nmspmm
+    m, n, k, N, M, L = cfg
+    A, Bd, W = make_inputs(cfg, dtype, "cuda")
+    Ah = A.cpu().pin_memory()
+    Vh = W.values.cpu().pin_memory()
+    Dh = W.idx.cpu().pin_memory()
+    Ch = torch.empty(m, n, dtype=dtype).pin_memory()
+    run = nmspmm.HostSpmm(m, n, k, N, M, L, ab_dtype=dtype, math="f32_simt" if dtype == torch.float32 else "auto")
+    stream = torch.cuda.current_stream()
+    ms = time_steps(lambda: run(Ah, Vh, Dh, Ch, stream=stream), steps, warmup, stream)
+    t = statistics.median(ms)
+    e = Ah.element_size()
+    return {"value": round(flop_count(cfg) / (t * 1e-3) / 1e12, 4), "unit": "TFLOP/s (effective, kept MACs)",
+            "ms_per_step": round(t, 4), "h2d_bytes_per_step": int(Ah.numel() * e + Vh.numel() * e + Dh.numel()),
+            "d2h_bytes_per_step": int(Ch.numel() * Ch.element_size()),
+            "path": "nm_spmm_host (C ABI, host pinned A/B'/D in, C out, synchronous)"}
+
+
+def cpu_baseline(cfg, target_s=10.0):
+    """The oracle as it stands (O2, fp64, OpenMP over rows) on a bounded row sample."""
+    from oracle import oracle
+    from paper_2503_01253_b200 import synth
+    m, n, k, N, M, L = cfg
+    A = synth.uniform((m, k), 1, synth.TID_A)
+    B = synth.uniform((k, n), 2, synth.TID_B)
+    vals, D = oracle.compress(B, N, M, L)
+    threads = oracle.num_threads()
+    probe = list(range(min(m, max(4, threads))))
+    t0 = time.perf_counter()
+    oracle.spmm_sparse_f64(A, vals, D, k, N, M, L, rows=probe)
+    tp = time.perf_counter() - t0
+    rows = int(min(m, max(len(probe), len(probe) * target_s / max(tp, 1e-6))))
+    sample = np.linspace(0, m - 1, rows).astype(np.int64)
+    t0 = time.perf_counter()
+    oracle.spmm_sparse_f64(A, vals, D, k, N, M, L, rows=sample)
+    t = time.perf_counter() - t0
+    w = k // M * N
+    return {"value": round(2.0 * rows * n * w / t / 1e12, 6), "unit": "TFLOP/s (effective, kept MACs)",
+            "cores": threads, "kind": "oracle",
+            "sample": f"{rows} of {m} rows (all {n} columns) of {cfg_name(cfg)}, O2 fp64 sparse loop, {t:.1f} s",
+            "seconds": round(t, 3)}
+
+
+def cfg_name(cfg):
+    for k, v in CONFIGS.items():
+        if v == cfg:
+            return k
+    return str(cfg)
+
+
+def config_dict(cfg, dtype_name, extra=None):
+    m, n, k, N, M, L = cfg
+    d = {"workload": f"{cfg_name(cfg)}: C[m,n] = A[m,k] . B~ (vector-wise {N}:{M}, L={L})", "m": m, "n": n,
+         "k": k, "N": N, "M": M, "L": L, "sparsity": 1 - N / M, "operands": dtype_name,
+         "l2": "flushed between timed steps (256 MiB write, outside the CUDA events)",
+         "inputs": "synthetic U[-1,1) (splitmix64 counter PRNG), magnitude-pruned by nm_compress"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def traffic_for(kernel_key):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(kernel_key)
+    return None
+
+
+# ----------------------------------------------------------------------- arms
+def run_reference(args):
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    runs = []
+    for _ in range(args.warmup + args.steps):
+        runs.append(cpu_baseline(cfg, target_s=max(1.0, args.ref_seconds / max(1, args.steps))))
+    timed = runs[args.warmup:]
+    v = statistics.median(r["value"] for r in timed)
+    w = cfg[2] // cfg[4] * cfg[3]
+    line = {"impl": "reference", "metric": "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M",
+            "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config_dict(cfg, "f32 in, fp64 accumulate"),
+            "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample")} | {"value": v},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "CPU oracle (plain C, OpenMP over rows) on a bounded row sample per step; "
+                    f"full step would be {2.0 * cfg[0] * cfg[1] * w / (v * 1e12):.1f} s"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_01253_b200 import nmspmm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks, peaks_src = load_peaks()
+    cfg = CONFIGS[args.config]
+    dtype = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    flush = (lambda: flush_buf.fill_(1.0)) if not args.no_flush else None
+    m, n, k, N, M, L = cfg
+
+    if world == 1:
+        stream = torch.cuda.current_stream()
+        A, Bd, W = make_inputs(cfg, dtype, "cuda")
+        C = torch.empty(m, n, dtype=dtype, device="cuda")
+        math = "f32_simt" if dtype == torch.float32 else "auto"
+        step = lambda: nmspmm.nm_spmm(A, W, out=C, math=math)  # noqa: E731
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        sampler = ClockSampler(local)
+        with sampler:
+            t0 = time.perf_counter()
+            ms = time_steps(step, args.steps, 0, stream, flush)
+            wall = time.perf_counter() - t0
+        t_step = statistics.fmean(ms)
+        value = flop_count(cfg) / (t_step * 1e-3) / 1e12
+        launches = args.steps
+        kernel_ms = t_step
+        del Bd
+        if args.profile:
+            print(json.dumps({"profile_run": True, "ms": t_step}), flush=True)
+            return 0
+        res = {}
+        if not args.quick:
+            torch.backends.cuda.matmul.allow_tf32 = False
+            Ad = A
+            Bdense = nmspmm.nm_decompress(W)  # same shape as the dense weight
+            Cd = torch.empty_like(C)
+            msd = time_steps(lambda: torch.mm(Ad, Bdense, out=Cd), args.steps, args.warmup, stream, flush)
+            td = statistics.fmean(msd)
+            res = {"cublas_ms": td, "cublas_dense_tflops": 2.0 * m * n * k / (td * 1e-3) / 1e12,
+                   "speedup_vs_cublas": td / t_step, "target_speedup_0.7xM/N": 0.7 * M / N}
+            del Bdense, Cd
+        del A, W, C
+        torch.cuda.empty_cache()
+    else:
+        raise SystemExit("multi-GPU path: see run_sharded")
+
+    sm_mhz = peaks.get("sm_max_mhz", 1965.0)
+    if dtype == torch.float32:
+        peak = fp32_alu_peak_tflops(sm_mhz)
+        roof = {"bound": "alu", "achieved": round(flop_count(cfg) / (kernel_ms * 1e-3) / 1e12, 3),
+                "peak": round(peak, 2), "unit": "TFLOP/s", "frac": None,
+                "peak_source": f"derived: 148 SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz (sm_max_mhz, {peaks_src})",
+                "kernel": "nm::simt::spmm_simt_f32_kernel",
+                "algorithmic_flops_per_launch": flop_count(cfg),
+                "algorithmic_bytes_per_launch": alg_bytes(cfg, 4)}
+    else:
+        peak = peaks.get("bf16_tflops", 1590.0)
+        roof = {"bound": "tensor", "achieved": round(flop_count(cfg) / (kernel_ms * 1e-3) / 1e12, 3),
+                "peak": peak, "unit": "TFLOP/s", "frac": None, "peak_source": f"bf16_tflops ({peaks_src})",
+                "kernel": "nm_spmm bf16", "algorithmic_flops_per_launch": flop_count(cfg),
+                "algorithmic_bytes_per_launch": alg_bytes(cfg, 2)}
+    roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
+    roof["traffic"] = traffic_for(f"{args.config}_{args.dtype}")
+
+    line = {"metric": "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M; speedup vs cuBLAS dense",
+            "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": config_dict(cfg, args.dtype, {"parallelism": "single GPU"}),
+            "gpu_launches": launches, "roofline": roof, "clocks": sampler.summary(),
+            "wall_s_timed_region": round(wall, 4)}
+    line.update({k2: (round(v2, 4) if isinstance(v2, float) else v2) for k2, v2 in res.items()})
+    if not args.quick:
+        line["e2e"] = e2e_measure(cfg, dtype, max(3, args.steps // 4), args.warmup)
+        line["cpu_baseline"] = cpu_baseline(cfg, target_s=args.ref_seconds)
+        variants = []
+        for name in args.variants.split(",") if args.variants else []:
+            vcfg = CONFIGS[name]
+            r, _ = measure_config(vcfg, dtype, max(5, args.steps // 2), args.warmup, flush)
+            variants.append({"config": name, "m_n_k": vcfg[:3], "N:M": f"{vcfg[3]}:{vcfg[4]}", "L": vcfg[5],
+                             "tflops": round(r["tflops"], 3), "ms": round(r["ms"], 4),
+                             "cublas_dense_tflops": round(r["cublas_dense_tflops"], 3),
+                             "speedup_vs_cublas": round(r["speedup_vs_cublas"], 3),
+                             "target_speedup": r["target_speedup"]})
+            torch.cuda.empty_cache()
+        line["variants"] = variants
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_sharded(args):
+    """N > 1: column groups sharded over ranks, NCCL all-gather + unshard kernel."""
+    import torch
+    import torch.distributed as dist
+    from paper_2503_01253_b200 import sharded
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+    dtype = torch.float32 if args.dtype == "f32" else torch.bfloat16
+    m, n, k, N, M, L = cfg
+    A, Bd, _ = make_inputs(cfg, dtype, "cuda")  # A replicated (column-parallel input), B generated identically
+    layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD)
+    del Bd
+    flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    step = lambda: layer(A)  # noqa: E731
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(local)
+    with sampler:
+        ms = time_steps(step, args.steps, 0, stream, (lambda: flush_buf.fill_(1.0)))
+    dist.barrier()
+    t = torch.tensor([statistics.fmean(ms)], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    # kernel-only time (local nm_spmm), also max over ranks
+    msk = time_steps(lambda: layer.local(A), args.steps, 0, stream, (lambda: flush_buf.fill_(1.0)))
+    tk = torch.tensor([statistics.fmean(msk)], device="cuda")
+    dist.all_reduce(tk, op=dist.ReduceOp.MAX)
+    t_step, t_kernel = t.item(), tk.item()
+    if rank == 0:
+        value = flop_count(cfg) / (t_step * 1e-3) / 1e12
+        line = {"metric": "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M; speedup vs cuBLAS dense",
+                "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+                "config": config_dict(cfg, args.dtype, {"parallelism": f"col{world} (column groups sharded, "
+                                                                        "NCCL all-gather of C)"}),
+                "gpu_launches": args.steps * 2, "clocks": sampler.summary(),
+                "kernel_only_tflops": round(flop_count(cfg) / (t_kernel * 1e-3) / 1e12, 4),
+                "kernel_only_ms": round(t_kernel, 4),
+                "allgather_floor_ms": round((world - 1) / world * m * n * A.element_size() / 770e9 * 1e3, 4)}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=HEADLINE, choices=sorted(CONFIGS))
+    ap.add_argument("--dtype", default="f32", choices=["f32", "bf16"])
+    ap.add_argument("--variants", default=",".join(VARIANTS))
+    ap.add_argument("--quick", action="store_true", help="headline kernel only (no cuBLAS / e2e / oracle)")
+    ap.add_argument("--profile", action="store_true", help="minimal run for ncu")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.profile:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_sharded(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,173 @@
+/*
+ * nmspmm.h -- C ABI of libnmspmm.so: B200-native (sm_100a) vector-wise N:M
+ * sparse matrix multiplication, after NM-SpMM (arXiv 2503.01253).
+ *
+ * Citations: "P:<line>" = PAPER.md line (+ section / equation), "S:<line>" =
+ * SPEC.md line; readings Rn are listed in DESIGN.md "Readings of the paper".
+ *
+ * Notation (Sec. II-A): C (m x n) = A (m x k) . B~ (k x n), where B~
+ * is B pruned vector-wise N:M along k: in every window of M consecutive
+ * length-L row vectors of one column group, N are kept.  Storage:
+ *   B' ("values") : w x n, w = k*N/M, row u = the (u mod N)-th kept vector of
+ *                   window floor(u/N), ascending offset (R7);
+ *   D  ("idx")    : w x q uint8, q = n/L, offset of that vector in its window.
+ * The product is Eq. 1 with readings R1-R4 (window base
+ * floor(u/N)*M, sum u = 0..w-1, floor(j/L), no M/N prefactor):
+ *   C[i][j] = sum_{u=0}^{w-1} A[i][floor(u/N)*M + D[u][floor(j/L)]] * B'[u][j].
+ *
+ * Conventions for every entry point:
+ *  - all matrices are row-major and contiguous; every data pointer is a
+ *    DEVICE pointer owned by the caller (the library keeps no pointer after
+ *    return and allocates no persistent memory);
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream); calls are stream-ordered and asynchronous unless stated;
+ *  - argument errors are returned synchronously, before any launch; device
+ *    faults surface at the next synchronisation (CUDA semantics);
+ *  - no exceptions or aborts cross the ABI; nm_last_error() gives a
+ *    thread-local message for the last non-OK status of the calling thread;
+ *  - there is no CPU fallback: without a CUDA device every compute entry
+ *    point returns NM_ERR_CUDA.
+ */
+#ifndef NMSPMM_H_
+#define NMSPMM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NM_OK = 0,
+    NM_ERR_INVALID_CONFIG = 1,  /* !(1 <= N <= M <= 256) or L < 1 (uint8 D, R8)        */
+    NM_ERR_SHAPE = 2,           /* k % M, n % L, negative dims (caller pads, R9)            */
+    NM_ERR_ALIGNMENT = 3,       /* a pointer the chosen kernel needs 16-B aligned is not         */
+    NM_ERR_NONFINITE = 4,       /* NaN in B during compress (score undefined, R6)                 */
+    NM_ERR_UNSUPPORTED = 5,     /* dtype / math / shape combination without a kernel              */
+    NM_ERR_INVALID_INDICES = 6, /* nm_validate found an entry >= M or not strictly increasing      */
+    NM_ERR_CUDA = 7,            /* CUDA runtime error (message in nm_last_error)                  */
+    NM_ERR_NULL = 8             /* a required pointer is NULL                                      */
+} nm_status;
+
+typedef enum { NM_F32 = 0, NM_BF16 = 1 } nm_dtype;
+
+typedef enum {
+    NM_MATH_AUTO = 0,     /* selector decides (nm_plan_query)                                 */
+    NM_MATH_F32_SIMT = 1, /* fp32 FFMA on CUDA cores: the paper's fp32 semantics     */
+    NM_MATH_TF32_TC = 2,  /* tcgen05 kind::tf32, fp32 accumulate in TMEM (R11)                */
+    NM_MATH_BF16_TC = 3   /* tcgen05 kind::f16 (bf16 operands), fp32 accumulate in TMEM      */
+} nm_math;
+
+/* Selector output (P:150 blocking parameters re-cut for B200). */
+typedef struct {
+    int32_t math;         /* nm_math actually used                                             */
+    int32_t kernel;       /* kernel id; 0 = generic                             */
+    int32_t bm, bn, bk;   /* CTA tile: rows of A, columns of C, dense k per panel (mult. of M)  */
+    int32_t bkw;          /* compressed rows per panel = bk*N/M                                 */
+    int32_t stages;       /* smem pipeline depth                                               */
+    int32_t grid;         /* CTAs launched                                                     */
+    int32_t threads;      /* threads per CTA                                                   */
+    int32_t smem_bytes;   /* dynamic shared memory per CTA                                     */
+    double flops;         /* 2*m*n*w (kept MACs only)                                   */
+    double bytes;         /* algorithmic HBM bytes: A + B' + D + C                             */
+    double t_compute_us;  /* roofline estimates from the peaks passed in (or built-in nominal)   */
+    double t_memory_us;
+    int32_t bound;        /* 0 = compute (FMA or tensor), 1 = HBM                               */
+} nm_plan;
+
+/* Library version string, e.g. "nmspmm 0.1 sm_100a". */
+const char* nm_version(void);
+
+/* Thread-local message for the last non-OK status returned on this thread. */
+const char* nm_last_error(void);
+
+/* Checks 1 <= N <= M <= 256 and L >= 1.  Host only. */
+nm_status nm_check_config(int N, int M, int L);
+
+/*
+ * nm_compress -- magnitude pruning + compression (readings R6, R7, R10, R11).
+ *   B      : k x n, dtype b_dt (NM_F32 or NM_BF16), device.
+ *   values : w x n, dtype v_dt, device, written.  v_dt == b_dt is a bit copy;
+ *            NM_F32 -> NM_BF16 rounds to nearest even; NM_BF16 -> NM_F32 widens.
+ *   idx    : w x q uint8, device, written.
+ * For every window t and group g: score_r = sum_{c<L} x^2 (x = B[t*M+r][g*L+c]),
+ * formed in fp64 with products and sums rounded in ascending c, no FMA; the N
+ * largest scores are kept, ties to the smaller offset; offsets written
+ * ascending.  Bit-exact with the CPU oracle.
+ * SYNCHRONOUS: returns after the work on `stream` has finished, because a NaN
+ * in B is reported as NM_ERR_NONFINITE (outputs are then unspecified).
+ */
+nm_status nm_compress(const void* B, nm_dtype b_dt, int64_t k, int64_t n, int N, int M, int L,
+                      void* values, nm_dtype v_dt, uint8_t* idx, void* stream);
+
+/*
+ * nm_decompress -- B~ (k x n, dtype v_dt): +0.0 everywhere except
+ * B~[t*M + idx[t*N+s][g]][g*L+c] = values[t*N+s][g*L+c].
+ * Entries of idx >= M are skipped (use nm_validate first).  Asynchronous.
+ */
+nm_status nm_decompress(const void* values, nm_dtype v_dt, const uint8_t* idx, int64_t k, int64_t n,
+                        int N, int M, int L, void* B_out, void* stream);
+
+/*
+ * nm_validate -- S:93-101.  *first_bad_host (host pointer) receives -1 if every
+ * entry is < M and strictly increasing inside its window, else the smallest
+ * row-major flat index u*q+g of a violating entry; the return value is then
+ * NM_ERR_INVALID_INDICES.  SYNCHRONOUS on `stream`.
+ */
+nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, int L,
+                      int64_t* first_bad_host, void* stream);
+
+/*
+ * nm_spmm -- C = A . decompress(values, idx) (Eq. 1 with R1-R4).
+ *   A      : m x k, dtype ab_dt, device;   values : w x n, dtype ab_dt;
+ *   idx    : w x q uint8 (must be valid; not re-checked on the hot path);
+ *   C      : m x n, dtype c_dt, device, overwritten.
+ *   ab_dt / c_dt / math:  NM_F32 + NM_MATH_F32_SIMT   -> fp32 FFMA, c_dt NM_F32
+ *                         NM_F32 + NM_MATH_TF32_TC    -> tcgen05 tf32, c_dt NM_F32
+ *                         NM_BF16 + NM_MATH_BF16_TC   -> tcgen05 bf16, c_dt NM_BF16 (RNE) or NM_F32
+ *                         NM_MATH_AUTO                -> selector (nm_plan_query)
+ * Each C element is accumulated inside one CTA in a fixed order (no split-K,
+ * no atomics): results are bit-reproducible run to run (R13).
+ * m == 0 or n == 0 is a no-op returning NM_OK.  Asynchronous.
+ */
+nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
+                  int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math,
+                  void* stream);
+
+/*
+ * nm_spmm_host -- the same product with HOST operands (end-to-end path):
+ * copies A, values, idx from host memory (pinned for async copies) into the
+ * caller's device workspace, runs nm_spmm, copies C back to C_host.
+ * Workspace `dev_ws` must hold nm_spmm_host_ws_bytes(...) bytes (device).
+ * SYNCHRONOUS (returns after C_host is written).
+ */
+int64_t nm_spmm_host_ws_bytes(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab_dt,
+                              nm_dtype c_dt);
+nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_t* idx_host,
+                       void* C_host, int64_t m, int64_t n, int64_t k, int N, int M, int L,
+                       nm_dtype ab_dt, nm_dtype c_dt, nm_math math, void* dev_ws, void* stream);
+
+/*
+ * nm_plan_query -- the selector's decision for a problem (S9 of SURVEY 8(a)),
+ * without launching.  peak_flops / peak_hbm_bytes_per_s: the roofline
+ * denominators (<= 0 selects built-in nominal B200 numbers).  Host only;
+ * needs a device only to read the SM count (148 assumed if none).
+ */
+nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab_dt,
+                        nm_math math, double peak_flops, double peak_hbm_bytes_per_s, nm_plan* out);
+
+/*
+ * nm_unshard_columns -- multi-GPU assembly.  The q = n/L column
+ * groups are split over G ranks, rank r owning groups [floor(r*q/G),
+ * floor((r+1)*q/G)); every rank's slice is padded to nr >= L*ceil(q/G)
+ * columns.  src is the all-gathered [G][m][nr] buffer (device), dst the
+ * m x n row-major result (device); padding columns are dropped.
+ * elem_bytes is 2 (bf16) or 4 (fp32).  Asynchronous.
+ */
+nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, int64_t nr, int64_t n, int L,
+                             int elem_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NMSPMM_H_ */

@@ -1,0 +1,364 @@
+// abi.cu -- the extern "C" boundary of libnmspmm.so (declared in include/nmspmm.h):
+// argument validation, the selector, dispatch to the sm_100a kernels, status /
+// thread-local error reporting.  No CPU fallback: every compute entry point
+// needs a CUDA device and returns NM_ERR_CUDA without one.
+#include <cuda_bf16.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace nm {
+
+// ------------------------------------------------------------ error plumbing
+static thread_local std::string g_last_error;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+
+nm_status fail(nm_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+nm_status cuda_fail(cudaError_t e, const char* what) {
+    g_last_error = std::string("CUDA error in ") + what + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return NM_ERR_CUDA;
+}
+
+static std::once_flag g_props_once;
+static int g_num_sms = 0;
+static int g_cc = 0;
+
+static void read_props() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return;
+    }
+    int sms = 0, major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) g_num_sms = sms;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess)
+        g_cc = major * 10 + minor;
+    cudaGetLastError();
+}
+
+int num_sms() {
+    std::call_once(g_props_once, read_props);
+    return g_num_sms > 0 ? g_num_sms : 148;
+}
+
+static nm_status require_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return fail(NM_ERR_CUDA, "no CUDA device: libnmspmm has no CPU fallback");
+    }
+    std::call_once(g_props_once, read_props);
+    if (g_cc != 100)
+        return fail(NM_ERR_UNSUPPORTED, "libnmspmm is built for sm_100a (B200); device compute capability is " +
+                                            std::to_string(g_cc));
+    return NM_OK;
+}
+
+// ------------------------------------------------------------------ TMA
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+        cudaGetLastError();
+    });
+    return fn;
+}
+
+nm_status make_tma_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t rows,
+                      int64_t cols, int box_rows, int box_cols, int swizzle) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(NM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t gstride[1] = {static_cast<cuuint64_t>(cols) * elem_bytes};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUtensorMapSwizzle sw = swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                            : swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = enc(map, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[256];
+        snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld box=%dx%d swizzle=%d",
+                 static_cast<int>(r), static_cast<long long>(rows), static_cast<long long>(cols), box_rows, box_cols,
+                 swizzle);
+        return fail(NM_ERR_ALIGNMENT, buf);
+    }
+    return NM_OK;
+}
+
+// ---------------------------------------------------------- kernels (extern)
+nm_status compress_launch(const void* B, nm_dtype b_dt, int64_t k, int64_t n, int N, int M, int L, void* values,
+                          nm_dtype v_dt, uint8_t* idx, cudaStream_t s);
+nm_status decompress_launch(const void* values, nm_dtype v_dt, const uint8_t* idx, int64_t k, int64_t n, int N,
+                            int M, int L, void* out, cudaStream_t s);
+nm_status validate_launch(const uint8_t* idx, int64_t k, int64_t n, int N, int M, int L, int64_t* first_bad_host,
+                          cudaStream_t s);
+nm_status unshard_launch(const void* src, void* dst, int64_t G, int64_t m, int64_t nr, int64_t q, int L,
+                         int elem_bytes, cudaStream_t s);
+bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
+                         int L);
+void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
+nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
+                          int N, int M, int L, cudaStream_t s);
+
+// ---------------------------------------------------------- generic kernel
+// One thread per C element; correct for every valid (N, M, L) and alignment.
+// Used when no tiled kernel applies (L % 4 != 0, M > 64, N > 32, misaligned).
+template <typename T>
+__device__ __forceinline__ float ld_f(const T* p, int64_t i);
+template <>
+__device__ __forceinline__ float ld_f<float>(const float* p, int64_t i) { return p[i]; }
+template <>
+__device__ __forceinline__ float ld_f<__nv_bfloat16>(const __nv_bfloat16* p, int64_t i) {
+    return __bfloat162float(p[i]);
+}
+template <typename T>
+__device__ __forceinline__ void st_f(T* p, int64_t i, float v);
+template <>
+__device__ __forceinline__ void st_f<float>(float* p, int64_t i, float v) { p[i] = v; }
+template <>
+__device__ __forceinline__ void st_f<__nv_bfloat16>(__nv_bfloat16* p, int64_t i, float v) {
+    p[i] = __float2bfloat16_rn(v);
+}
+
+template <typename TA, typename TC>
+__global__ void spmm_generic_kernel(const TA* __restrict__ A, const TA* __restrict__ Bv, const uint8_t* __restrict__ D,
+                                    TC* __restrict__ C, int64_t m, int64_t n, int64_t k, int N, int M, int L) {
+    const int64_t j = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int64_t i = static_cast<int64_t>(blockIdx.y) * blockDim.y + threadIdx.y;
+    if (i >= m || j >= n) return;
+    const int64_t q = n / L, w = k / M * N, g = j / L;
+    const TA* arow = A + i * k;
+    float acc = 0.f;
+    for (int64_t u = 0; u < w; ++u) {
+        const int64_t kabs = (u / N) * M + D[u * q + g];  // Eq. 1 with R1-R3
+        acc = fmaf(ld_f<TA>(arow, kabs), ld_f<TA>(Bv, u * n + j), acc);
+    }
+    st_f<TC>(C, i * n + j, acc);
+}
+
+template <typename TA, typename TC>
+static nm_status generic_launch(const void* A, const void* Bv, const uint8_t* D, void* C, int64_t m, int64_t n,
+                                int64_t k, int N, int M, int L, cudaStream_t s) {
+    const dim3 block(32, 8);
+    const int64_t gy = ceil_div(m, 8);
+    if (gy > 65535) return fail(NM_ERR_UNSUPPORTED, "generic kernel: m too large");
+    const dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(gy));
+    spmm_generic_kernel<TA, TC><<<grid, block, 0, s>>>(static_cast<const TA*>(A), static_cast<const TA*>(Bv), D,
+                                                       static_cast<TC*>(C), m, n, k, N, M, L);
+    NM_LAUNCH_CHECK("spmm_generic_kernel");
+    return NM_OK;
+}
+
+// ------------------------------------------------------------------ selector
+enum KernelId { K_GENERIC = 0, K_SIMT_F32 = 1, K_TC_BF16 = 2, K_TC_TF32 = 3 };
+
+static nm_status select(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
+                        int L, nm_dtype ab, nm_dtype cd, nm_math math, int* kernel, nm_math* used) {
+    if (ab == NM_F32) {
+        if (cd != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
+        if (math == NM_MATH_AUTO || math == NM_MATH_F32_SIMT) {
+            *used = NM_MATH_F32_SIMT;
+            *kernel = simt_f32_applicable(A, Bv, C, m, n, k, N, M, L) ? K_SIMT_F32 : K_GENERIC;
+            return NM_OK;
+        }
+        if (math == NM_MATH_TF32_TC) return fail(NM_ERR_UNSUPPORTED, "tf32 tensor-core path not built yet");
+        return fail(NM_ERR_UNSUPPORTED, "bf16 math requested on fp32 operands");
+    }
+    if (math == NM_MATH_AUTO || math == NM_MATH_BF16_TC) {
+        *used = NM_MATH_BF16_TC;
+        *kernel = K_GENERIC;
+        return NM_OK;
+    }
+    return fail(NM_ERR_UNSUPPORTED, "math mode not available for bf16 operands");
+}
+
+static nm_status check_common(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
+    if (N < 1 || M < N || M > 256 || L < 1)
+        return fail(NM_ERR_INVALID_CONFIG, "invalid N:M/L: need 1 <= N <= M <= 256 and L >= 1");
+    if (m < 0 || n < 0 || k < 0) return fail(NM_ERR_SHAPE, "negative dimension");
+    if (k % M != 0) return fail(NM_ERR_SHAPE, "k must be a multiple of M (caller pads, P:94)");
+    if (n % L != 0) return fail(NM_ERR_SHAPE, "n must be a multiple of L (caller pads, P:94)");
+    return NM_OK;
+}
+
+}  // namespace nm
+
+using namespace nm;
+
+extern "C" {
+
+const char* nm_version(void) { return "nmspmm 0.1 sm_100a"; }
+
+const char* nm_last_error(void) { return g_last_error.c_str(); }
+
+nm_status nm_check_config(int N, int M, int L) {
+    if (N < 1 || M < N || M > 256 || L < 1)
+        return fail(NM_ERR_INVALID_CONFIG, "invalid N:M/L: need 1 <= N <= M <= 256 and L >= 1");
+    return NM_OK;
+}
+
+nm_status nm_compress(const void* B, nm_dtype b_dt, int64_t k, int64_t n, int N, int M, int L, void* values,
+                      nm_dtype v_dt, uint8_t* idx, void* stream) {
+    nm_status st = check_common(0, n, k, N, M, L);
+    if (st) return st;
+    if (b_dt > NM_BF16 || v_dt > NM_BF16) return fail(NM_ERR_UNSUPPORTED, "dtype");
+    if (k * n > 0 && (!B || !values || !idx)) return fail(NM_ERR_NULL, "nm_compress: NULL pointer");
+    if ((st = require_device())) return st;
+    return compress_launch(B, b_dt, k, n, N, M, L, values, v_dt, idx, static_cast<cudaStream_t>(stream));
+}
+
+nm_status nm_decompress(const void* values, nm_dtype v_dt, const uint8_t* idx, int64_t k, int64_t n, int N, int M,
+                        int L, void* B_out, void* stream) {
+    nm_status st = check_common(0, n, k, N, M, L);
+    if (st) return st;
+    if (v_dt > NM_BF16) return fail(NM_ERR_UNSUPPORTED, "dtype");
+    if (k * n > 0 && (!values || !idx || !B_out)) return fail(NM_ERR_NULL, "nm_decompress: NULL pointer");
+    if ((st = require_device())) return st;
+    return decompress_launch(values, v_dt, idx, k, n, N, M, L, B_out, static_cast<cudaStream_t>(stream));
+}
+
+nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, int L, int64_t* first_bad_host,
+                      void* stream) {
+    nm_status st = check_common(0, n, k, N, M, L);
+    if (st) return st;
+    if (!first_bad_host || (k * n > 0 && !idx)) return fail(NM_ERR_NULL, "nm_validate: NULL pointer");
+    if ((st = require_device())) return st;
+    return validate_launch(idx, k, n, N, M, L, first_bad_host, static_cast<cudaStream_t>(stream));
+}
+
+nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n, int64_t k,
+                  int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math, void* stream) {
+    nm_status st = check_common(m, n, k, N, M, L);
+    if (st) return st;
+    if (ab_dt > NM_BF16 || c_dt > NM_BF16 || math > NM_MATH_BF16_TC) return fail(NM_ERR_UNSUPPORTED, "dtype/math");
+    if (m == 0 || n == 0) return NM_OK;
+    if (!A || !C || (k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_spmm: NULL pointer");
+    if ((st = require_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (k == 0) {
+        NM_CUDA_TRY(cudaMemsetAsync(C, 0, static_cast<size_t>(m * n) * (c_dt == NM_BF16 ? 2 : 4), s));
+        return NM_OK;
+    }
+    int kernel = K_GENERIC;
+    nm_math used = NM_MATH_AUTO;
+    if ((st = select(A, values, C, m, n, k, N, M, L, ab_dt, c_dt, math, &kernel, &used))) return st;
+    if (kernel == K_SIMT_F32)
+        return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
+                               static_cast<float*>(C), m, n, k, N, M, L, s);
+    if (ab_dt == NM_F32) return generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
+    if (c_dt == NM_BF16) return generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);
+    return generic_launch<__nv_bfloat16, float>(A, values, idx, C, m, n, k, N, M, L, s);
+}
+
+int64_t nm_spmm_host_ws_bytes(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt) {
+    if (N < 1 || M < N || L < 1 || k % M || n % L) return -1;
+    const int64_t e = ab_dt == NM_BF16 ? 2 : 4, ec = c_dt == NM_BF16 ? 2 : 4;
+    const int64_t w = k / M * N, q = n / L;
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+    return al(m * k * e) + al(w * n * e) + al(w * q) + al(m * n * ec);
+}
+
+nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_t* idx_host, void* C_host, int64_t m,
+                       int64_t n, int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math,
+                       void* dev_ws, void* stream) {
+    nm_status st = check_common(m, n, k, N, M, L);
+    if (st) return st;
+    if (m == 0 || n == 0) return NM_OK;
+    if (!A_host || !C_host || !dev_ws || (k > 0 && (!values_host || !idx_host)))
+        return fail(NM_ERR_NULL, "nm_spmm_host: NULL pointer");
+    if ((st = require_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int64_t e = ab_dt == NM_BF16 ? 2 : 4, ec = c_dt == NM_BF16 ? 2 : 4;
+    const int64_t w = k / M * N, q = n / L;
+    auto al = [](int64_t b) { return (b + 255) / 256 * 256; };
+    uint8_t* base = static_cast<uint8_t*>(dev_ws);
+    uint8_t* dA = base;
+    uint8_t* dV = dA + al(m * k * e);
+    uint8_t* dD = dV + al(w * n * e);
+    uint8_t* dC = dD + al(w * q);
+    NM_CUDA_TRY(cudaMemcpyAsync(dA, A_host, static_cast<size_t>(m * k * e), cudaMemcpyHostToDevice, s));
+    NM_CUDA_TRY(cudaMemcpyAsync(dV, values_host, static_cast<size_t>(w * n * e), cudaMemcpyHostToDevice, s));
+    NM_CUDA_TRY(cudaMemcpyAsync(dD, idx_host, static_cast<size_t>(w * q), cudaMemcpyHostToDevice, s));
+    if ((st = nm_spmm(dA, dV, dD, dC, m, n, k, N, M, L, ab_dt, c_dt, math, stream))) return st;
+    NM_CUDA_TRY(cudaMemcpyAsync(C_host, dC, static_cast<size_t>(m * n * ec), cudaMemcpyDeviceToHost, s));
+    NM_CUDA_TRY(cudaStreamSynchronize(s));
+    return NM_OK;
+}
+
+nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_math math,
+                        double peak_flops, double peak_hbm, nm_plan* out) {
+    nm_status st = check_common(m, n, k, N, M, L);
+    if (st) return st;
+    if (!out) return fail(NM_ERR_NULL, "nm_plan_query: NULL out");
+    *out = nm_plan{};
+    const int64_t w = k / M * N, q = n / L;
+    const double e = ab_dt == NM_BF16 ? 2.0 : 4.0;
+    out->flops = 2.0 * double(m) * double(n) * double(w);
+    out->bytes = e * double(m) * double(k) + e * double(w) * double(n) + double(w) * double(q) + e * double(m) * double(n);
+    int kernel = K_GENERIC;
+    nm_math used = NM_MATH_AUTO;
+    static const float dummy[4] = {0, 0, 0, 0};  // 16-B aligned stand-in pointers for the alignment test
+    if ((st = select(dummy, dummy, dummy, m, n, k, N, M, L, ab_dt, ab_dt, math, &kernel, &used))) return st;
+    out->math = used;
+    out->kernel = kernel;
+    const int sms = num_sms();
+    if (kernel == K_SIMT_F32) {
+        int wp, bk, bkw;
+        simt_f32_geometry(N, M, &wp, &bk, &bkw);
+        out->bm = 128;
+        out->bn = 128;
+        out->bk = bk;
+        out->bkw = bkw;
+        out->stages = 2;
+        out->threads = 256;
+        out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
+        out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
+    } else {
+        out->bm = 8;
+        out->bn = 32;
+        out->threads = 256;
+        out->grid = static_cast<int32_t>(ceil_div(m, 8) * ceil_div(n, 32));
+    }
+    // nominal peaks when none are given: FP32 FFMA = SMs * 128 lanes * 2 * 1.965 GHz; bf16 TC 2.25 PF; HBM 7.7 TB/s
+    if (peak_flops <= 0) peak_flops = used == NM_MATH_F32_SIMT ? double(sms) * 128 * 2 * 1.965e9 : 2.25e15;
+    if (peak_hbm <= 0) peak_hbm = 7.7e12;
+    out->t_compute_us = out->flops / peak_flops * 1e6;
+    out->t_memory_us = out->bytes / peak_hbm * 1e6;
+    out->bound = out->t_memory_us > out->t_compute_us ? 1 : 0;
+    return NM_OK;
+}
+
+nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, int64_t nr, int64_t n, int L,
+                             int elem_bytes, void* stream) {
+    if (G < 1 || m < 0 || nr < 0 || n < 0 || L < 1 || n % L) return fail(NM_ERR_SHAPE, "nm_unshard_columns: shape");
+    if (elem_bytes != 2 && elem_bytes != 4) return fail(NM_ERR_UNSUPPORTED, "elem_bytes must be 2 or 4");
+    const int64_t q = n / L;
+    if (L * ceil_div(q, G) > nr) return fail(NM_ERR_SHAPE, "nm_unshard_columns: nr < L*ceil(q/G)");
+    if (m * n > 0 && (!src || !dst)) return fail(NM_ERR_NULL, "nm_unshard_columns: NULL pointer");
+    nm_status st = require_device();
+    if (st) return st;
+    return unshard_launch(src, dst, G, m, nr, q, L, elem_bytes, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

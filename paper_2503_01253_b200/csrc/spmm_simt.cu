@@ -1,0 +1,260 @@
+// spmm_simt.cu -- fp32 CUDA-core N:M SpMM (the paper's fp32 semantics),
+// re-designed for sm_100a.
+//
+// What is kept from the paper: the hierarchical blocking of Listing 1 (CTA
+// tile over C, k-loop inside the CTA, no split-K), the register
+// outer-product micro-kernel of Listing 2 / Eq. 6 (8x8 thread tiles,
+// P:349-400), index prefetch ahead of the fragment loads (Listing 4)
+// and double buffering.
+// What is B200-specific: operand panels arrive by TMA (one thread issues,
+// mbarrier completion, OOB zero-fill for ragged m / n / k tails); the dense A
+// panel lands in the 128-byte-swizzled layout so the index-driven column
+// gather (A_s[row][kabs]) is bank-conflict free across the 8 rows a warp
+// touches; the per-panel index table D_s is converted once into swizzled byte
+// offsets so the inner loop spends one LDS + one XOR per (step, group).
+//
+// Tile: BM=128 rows x BN=128 columns, 256 threads (8 warps of 64x32), thread
+// tile 8 rows x 8 columns (two 4-column chunks 16 apart).  A panel: WP whole
+// windows (BK = WP*M <= 64 dense k, never straddling a window), i.e.
+// BKW = WP*N <= 32 compressed rows.
+#include "common.cuh"
+
+namespace nm {
+namespace simt {
+
+constexpr int BM = 128, BN = 128, BK = 64, BKW = 32, THREADS = 256, STAGES = 2;
+constexpr int A_BOX_COLS = 32;                      // 128 B of fp32: the swizzle-128B atom width
+constexpr int A_BOX_BYTES = BM * A_BOX_COLS * 4;    // 16 KB
+constexpr int A_STAGE_BYTES = BM * BK * 4;          // 32 KB
+constexpr int B_STAGE_BYTES = BKW * BN * 4;         // 16 KB
+constexpr int MAX_SLOTS = 33;                       // column groups touched by a 128-wide tile, L >= 4
+constexpr int KOFF_BYTES = 2 * BKW * MAX_SLOTS * 4;
+constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + KOFF_BYTES + 64 + 1024;
+constexpr int D_PER_THREAD = (BKW * MAX_SLOTS + THREADS - 1) / THREADS;  // 5
+
+struct Params {
+    const uint8_t* D;
+    float* C;
+    int m, n, k, N, M, L;
+    int q, wp, bk, bkw, npanels, nboxA;
+};
+
+// Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
+// box kk/32, 16-byte chunk (kk%32)/4, word kk%4.
+__device__ __forceinline__ int a_col_offset(int kk) {
+    return ((kk >> 5) * A_BOX_BYTES) + (((kk & 31) >> 2) << 4) + ((kk & 3) << 2);
+}
+
+// TWO: the thread's two 4-column chunks may belong to different column groups (L < 32).
+template <bool TWO>
+__global__ void __launch_bounds__(THREADS, 2)
+    spmm_simt_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                         const Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-B alignment for the swizzle-128B TMA destination; offset arithmetic on the
+    // __shared__ array keeps the shared address space visible to the compiler (LDS, not LD)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sA = smem;                                        // STAGES x 32 KB
+    uint8_t* sB = smem + STAGES * A_STAGE_BYTES;               // STAGES x 16 KB
+    int* koff = reinterpret_cast<int*>(sB + STAGES * B_STAGE_BYTES);  // [2][BKW][MAX_SLOTS]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(koff) + KOFF_BYTES);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp & 1, wn = warp >> 1;
+    const int t_m = lane & 7, t_n = lane >> 3;
+    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    const int g_first = n0 / p.L;
+    const int nslots = min((n0 + BN - 1) / p.L, p.q - 1) - g_first + 1;
+
+    if (tid == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint32_t stage_tx = static_cast<uint32_t>(p.nboxA * A_BOX_BYTES + p.bkw * BN * 4);
+    auto issue = [&](int panel) {
+        const int s = panel % STAGES;
+        mbar_arrive_expect_tx(&bars[s], stage_tx);
+        const int k0 = panel * p.bk, u0 = panel * p.bkw;
+        for (int b = 0; b < p.nboxA; ++b)
+            tma_load_2d(sA + s * A_STAGE_BYTES + b * A_BOX_BYTES, &tmA, &bars[s], k0 + b * A_BOX_COLS, m0);
+        tma_load_2d(sB + s * B_STAGE_BYTES, &tmB, &bars[s], n0, u0);
+    };
+
+    // D_s -> swizzled byte offsets koff[buf][u][slot] (index prefetch).
+    int dreg[D_PER_THREAD];
+    auto load_d = [&](int panel) {
+        const int u0 = panel * p.bkw;
+        const int bkw = min(p.bkw, (p.k / p.M) * p.N - u0);
+#pragma unroll
+        for (int r = 0; r < D_PER_THREAD; ++r) {
+            const int e = tid + r * THREADS;
+            const int u = e / nslots, s = e - u * nslots;
+            int v = 0;
+            if (u < bkw && s < nslots) v = p.D[static_cast<int64_t>(u0 + u) * p.q + g_first + s];
+            dreg[r] = v;
+        }
+    };
+    auto store_d = [&](int panel) {
+        const int u0 = panel * p.bkw, t0 = panel * p.wp;
+        int* kb = koff + (panel & 1) * (BKW * MAX_SLOTS);
+#pragma unroll
+        for (int r = 0; r < D_PER_THREAD; ++r) {
+            const int e = tid + r * THREADS;
+            const int u = e / nslots, s = e - u * nslots;
+            if (u < BKW && s < nslots) {
+                const int kk = ((u0 + u) / p.N - t0) * p.M + dreg[r];  // dense column inside the panel
+                kb[u * MAX_SLOTS + s] = a_col_offset(kk);
+            }
+        }
+    };
+
+    if (tid == 0) issue(0);
+    load_d(0);
+    store_d(0);
+    __syncthreads();
+
+    // thread geometry
+    const int col0 = wn * 32 + 4 * t_n;  // chunk 0 (chunk 1 at col0 + 16), tile-relative
+    // columns past n (ragged tile) read a valid slot; their results are never stored
+    const int slot0 = min((n0 + col0) / p.L - g_first, nslots - 1);
+    const int slot1 = min((n0 + col0 + 16) / p.L - g_first, nslots - 1);
+    const int tmx = t_m << 4;
+    const int a_row = (wm * 64 + t_m) * 128;
+
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+    for (int panel = 0; panel < p.npanels; ++panel) {
+        const int s = panel % STAGES;
+        if (tid == 0 && panel + 1 < p.npanels) issue(panel + 1);  // stage (panel+1)%2 freed by last sync
+        if (panel + 1 < p.npanels) load_d(panel + 1);
+        mbar_wait(&bars[s], (panel / STAGES) & 1);
+
+        const int u0 = panel * p.bkw;
+        const int bkw = min(p.bkw, (p.k / p.M) * p.N - u0);
+        const uint8_t* aS = sA + s * A_STAGE_BYTES + a_row;
+        const float* bS = reinterpret_cast<const float*>(sB + s * B_STAGE_BYTES) + col0;
+        const int* kS = koff + (panel & 1) * (BKW * MAX_SLOTS);
+
+        float a0[8], a1[8];
+        float4 b0, b1;
+#pragma unroll 2
+        for (int u = 0; u < bkw; ++u) {
+            const int* krow = kS + u * MAX_SLOTS;
+            const uint8_t* ap0 = aS + (krow[slot0] ^ tmx);
+            b0 = *reinterpret_cast<const float4*>(bS + u * BN);
+            b1 = *reinterpret_cast<const float4*>(bS + u * BN + 16);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a0[i] = *reinterpret_cast<const float*>(ap0 + i * 1024);
+            if (TWO) {
+                const uint8_t* ap1 = aS + (krow[slot1] ^ tmx);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a1[i] = *reinterpret_cast<const float*>(ap1 + i * 1024);
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a1[i] = a0[i];
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                acc[i][0] = fmaf(a0[i], b0.x, acc[i][0]);
+                acc[i][1] = fmaf(a0[i], b0.y, acc[i][1]);
+                acc[i][2] = fmaf(a0[i], b0.z, acc[i][2]);
+                acc[i][3] = fmaf(a0[i], b0.w, acc[i][3]);
+                acc[i][4] = fmaf(a1[i], b1.x, acc[i][4]);
+                acc[i][5] = fmaf(a1[i], b1.y, acc[i][5]);
+                acc[i][6] = fmaf(a1[i], b1.z, acc[i][6]);
+                acc[i][7] = fmaf(a1[i], b1.w, acc[i][7]);
+            }
+        }
+        if (panel + 1 < p.npanels) store_d(panel + 1);
+        __syncthreads();
+    }
+
+    // epilogue: registers -> global (float4 stores, guarded for ragged m / n)
+    const int gc0 = n0 + col0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int row = m0 + wm * 64 + 8 * i + t_m;
+        if (row >= p.m) continue;
+        float* crow = p.C + static_cast<int64_t>(row) * p.n;
+        if (gc0 < p.n) *reinterpret_cast<float4*>(crow + gc0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+        if (gc0 + 16 < p.n)
+            *reinterpret_cast<float4*>(crow + gc0 + 16) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    }
+}
+
+}  // namespace simt
+
+// Applicability of the tiled SIMT kernel (else the generic kernel runs).
+bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
+                         int L) {
+    if (L % 4 != 0 || M > simt::BK || N > simt::BKW) return false;
+    if (k % 4 != 0 || n % 4 != 0) return false;
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(Bv) | reinterpret_cast<uintptr_t>(C)) & 15)
+        return false;
+    if (m > (1ll << 31) - simt::BM || n > (1ll << 31) - simt::BN || k >= (1ll << 31)) return false;
+    return true;
+}
+
+void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw) {
+    int w = simt::BK / M;
+    w = w < simt::BKW / N ? w : simt::BKW / N;
+    if (w < 1) w = 1;
+    *wp = w;
+    *bk = w * M;
+    *bkw = w * N;
+}
+
+nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
+                          int N, int M, int L, cudaStream_t s) {
+    using namespace simt;
+    Params p{};
+    p.D = D;
+    p.C = C;
+    p.m = static_cast<int>(m);
+    p.n = static_cast<int>(n);
+    p.k = static_cast<int>(k);
+    p.N = N;
+    p.M = M;
+    p.L = L;
+    p.q = static_cast<int>(n / L);
+    simt_f32_geometry(N, M, &p.wp, &p.bk, &p.bkw);
+    const int windows = static_cast<int>(k / M);
+    p.npanels = (windows + p.wp - 1) / p.wp;
+    p.nboxA = (p.bk + A_BOX_COLS - 1) / A_BOX_COLS;
+    const int64_t w = k / M * N;
+
+    CUtensorMap tmA, tmB;
+    nm_status st = make_tma_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, m, k, BM, A_BOX_COLS, 128);
+    if (st) return st;
+    st = make_tma_2d(&tmB, Bv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, w, n, p.bkw, BN, 0);
+    if (st) return st;
+
+    const dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(m, BM)));
+    const bool two = L < 32;
+    static bool attr_done[2] = {false, false};
+    if (!attr_done[two]) {
+        if (two)
+            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             SMEM_BYTES));
+        else
+            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<false>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+        attr_done[two] = true;
+    }
+    if (two)
+        spmm_simt_f32_kernel<true><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p);
+    else
+        spmm_simt_f32_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p);
+    NM_LAUNCH_CHECK("spmm_simt_f32_kernel");
+    return NM_OK;
+}
+
+}  // namespace nm

@@ -1,0 +1,217 @@
+"""Thin Python binding of libnmspmm.so (include/nmspmm.h): argument
+marshalling only -- every step of the path runs in the library's sm_100a
+kernels.  torch supplies device memory and streams.  There is no CPU
+fallback: if the library or a CUDA device is missing, calls raise.
+
+Names follow the C ABI: nm_compress, nm_decompress, nm_validate, nm_spmm,
+nm_spmm_host, nm_plan_query, nm_unshard_columns.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libnmspmm.so")
+
+NM_OK = 0
+STATUS = {0: "NM_OK", 1: "NM_ERR_INVALID_CONFIG", 2: "NM_ERR_SHAPE", 3: "NM_ERR_ALIGNMENT",
+          4: "NM_ERR_NONFINITE", 5: "NM_ERR_UNSUPPORTED", 6: "NM_ERR_INVALID_INDICES", 7: "NM_ERR_CUDA",
+          8: "NM_ERR_NULL"}
+NM_F32, NM_BF16 = 0, 1
+MATH = {"auto": 0, "f32_simt": 1, "tf32_tc": 2, "bf16_tc": 3}
+
+EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_decompress", "nm_validate",
+           "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns"]
+
+
+class NmError(RuntimeError):
+    def __init__(self, status: int, fn: str, msg: str):
+        super().__init__(f"{fn}: {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("math", ctypes.c_int32), ("kernel", ctypes.c_int32), ("bm", ctypes.c_int32),
+                ("bn", ctypes.c_int32), ("bk", ctypes.c_int32), ("bkw", ctypes.c_int32),
+                ("stages", ctypes.c_int32), ("grid", ctypes.c_int32), ("threads", ctypes.c_int32),
+                ("smem_bytes", ctypes.c_int32), ("flops", ctypes.c_double), ("bytes", ctypes.c_double),
+                ("t_compute_us", ctypes.c_double), ("t_memory_us", ctypes.c_double), ("bound", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+
+
+def lib():
+    """Load libnmspmm.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I64, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.nm_version.restype = ctypes.c_char_p
+        L.nm_last_error.restype = ctypes.c_char_p
+        L.nm_check_config.argtypes = [I, I, I]
+        L.nm_compress.argtypes = [P, I, I64, I64, I, I, I, P, I, P, P]
+        L.nm_decompress.argtypes = [P, I, P, I64, I64, I, I, I, P, P]
+        L.nm_validate.argtypes = [P, I64, I64, I, I, I, ctypes.POINTER(ctypes.c_int64), P]
+        L.nm_spmm.argtypes = [P, P, P, P, I64, I64, I64, I, I, I, I, I, I, P]
+        L.nm_spmm_host_ws_bytes.argtypes = [I64, I64, I64, I, I, I, I, I]
+        L.nm_spmm_host_ws_bytes.restype = I64
+        L.nm_spmm_host.argtypes = [P, P, P, P, I64, I64, I64, I, I, I, I, I, I, P, P]
+        L.nm_plan_query.argtypes = [I64, I64, I64, I, I, I, I, I, ctypes.c_double, ctypes.c_double,
+                                    ctypes.POINTER(Plan)]
+        L.nm_unshard_columns.argtypes = [P, P, I64, I64, I64, I64, I, I, P]
+        for name in EXPORTS[2:]:
+            if name != "nm_spmm_host_ws_bytes":
+                getattr(L, name).restype = I
+        _lib = L
+    return _lib
+
+
+def _check(status: int, fn: str):
+    if status != NM_OK:
+        raise NmError(status, fn, lib().nm_last_error().decode())
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return NM_F32
+    if t.dtype == torch.bfloat16:
+        return NM_BF16
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream(t: torch.Tensor, stream=None):
+    if stream is not None:
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(torch.cuda.current_stream(t.device).cuda_stream)
+
+
+def _dev(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (row-major)")
+
+
+def version() -> str:
+    return lib().nm_version().decode()
+
+
+@dataclass
+class NmWeight:
+    """Compressed weight: values B' (w x n) + index matrix D (w x q, uint8)."""
+    values: torch.Tensor
+    idx: torch.Tensor
+    k: int
+    N: int
+    M: int
+    L: int
+
+    @property
+    def n(self) -> int:
+        return self.values.shape[1]
+
+    @property
+    def w(self) -> int:
+        return self.values.shape[0]
+
+
+def nm_compress(B: torch.Tensor, N: int, M: int, L: int, values_dtype=None, stream=None) -> NmWeight:
+    """nm_compress: magnitude-prune B (k x n) to vector-wise N:M and compress."""
+    _dev(B, "B")
+    k, n = B.shape
+    vdt = values_dtype or B.dtype
+    _check(lib().nm_check_config(N, M, L), "nm_check_config")
+    if k % M or n % L:
+        raise NmError(2, "nm_compress", "k % M and n % L must be 0 (caller pads, P:94)")
+    w, q = k // M * N, n // L
+    values = torch.empty((w, n), dtype=vdt, device=B.device)
+    idx = torch.empty((w, q), dtype=torch.uint8, device=B.device)
+    _check(lib().nm_compress(B.data_ptr(), _dt(B), k, n, N, M, L, values.data_ptr(), _dt(values), idx.data_ptr(),
+                             _stream(B, stream)), "nm_compress")
+    return NmWeight(values, idx, k, N, M, L)
+
+
+def nm_decompress(W: NmWeight, stream=None) -> torch.Tensor:
+    _dev(W.values, "values")
+    out = torch.empty((W.k, W.n), dtype=W.values.dtype, device=W.values.device)
+    _check(lib().nm_decompress(W.values.data_ptr(), _dt(W.values), W.idx.data_ptr(), W.k, W.n, W.N, W.M, W.L,
+                               out.data_ptr(), _stream(out, stream)), "nm_decompress")
+    return out
+
+
+def nm_validate(idx: torch.Tensor, k: int, n: int, N: int, M: int, L: int, stream=None) -> int:
+    """-1 if valid, else the first bad flat index."""
+    _dev(idx, "idx")
+    bad = ctypes.c_int64(0)
+    st = lib().nm_validate(idx.data_ptr(), k, n, N, M, L, ctypes.byref(bad), _stream(idx, stream))
+    if st not in (NM_OK, 6):
+        _check(st, "nm_validate")
+    return int(bad.value)
+
+
+def nm_spmm(A: torch.Tensor, W: NmWeight, out: torch.Tensor | None = None, out_dtype=None, math: str = "auto",
+            stream=None) -> torch.Tensor:
+    """C = A . decompress(W) (Eq. 1, unscaled) on the device."""
+    _dev(A, "A")
+    _dev(W.values, "values")
+    _dev(W.idx, "idx")
+    m, k = A.shape
+    if k != W.k:
+        raise NmError(2, "nm_spmm", f"A has k={k}, weight has k={W.k}")
+    if A.dtype != W.values.dtype:
+        raise TypeError("A and values must share a dtype")
+    cdt = out_dtype or A.dtype
+    if out is None:
+        out = torch.empty((m, W.n), dtype=cdt, device=A.device)
+    else:
+        _dev(out, "out")
+    _check(lib().nm_spmm(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), out.data_ptr(), m, W.n, k, W.N, W.M,
+                         W.L, _dt(A), _dt(out), MATH[math], _stream(A, stream)), "nm_spmm")
+    return out
+
+
+class HostSpmm:
+    """End-to-end path through nm_spmm_host: host (pinned) operands in, host C out;
+    the device workspace is allocated once by torch."""
+
+    def __init__(self, m, n, k, N, M, L, ab_dtype=torch.float32, c_dtype=None, math="auto", device="cuda"):
+        self.m, self.n, self.k, self.N, self.M, self.L = m, n, k, N, M, L
+        self.ab = NM_F32 if ab_dtype == torch.float32 else NM_BF16
+        cd = c_dtype or ab_dtype
+        self.cd = NM_F32 if cd == torch.float32 else NM_BF16
+        self.math = MATH[math]
+        ws = lib().nm_spmm_host_ws_bytes(m, n, k, N, M, L, self.ab, self.cd)
+        if ws < 0:
+            raise NmError(2, "nm_spmm_host_ws_bytes", "bad shape")
+        self.ws = torch.empty(ws, dtype=torch.uint8, device=device)
+
+    def __call__(self, A_host, values_host, idx_host, C_host, stream=None):
+        _check(lib().nm_spmm_host(A_host.data_ptr(), values_host.data_ptr(), idx_host.data_ptr(), C_host.data_ptr(),
+                                  self.m, self.n, self.k, self.N, self.M, self.L, self.ab, self.cd, self.math,
+                                  self.ws.data_ptr(), _stream(self.ws, stream)), "nm_spmm_host")
+        return C_host
+
+
+def nm_plan_query(m, n, k, N, M, L, dtype=torch.float32, math="auto", peak_flops=0.0, peak_hbm=0.0) -> dict:
+    p = Plan()
+    _check(lib().nm_plan_query(m, n, k, N, M, L, NM_F32 if dtype == torch.float32 else NM_BF16, MATH[math],
+                               float(peak_flops), float(peak_hbm), ctypes.byref(p)), "nm_plan_query")
+    return p.as_dict()
+
+
+def nm_unshard_columns(src: torch.Tensor, dst: torch.Tensor, G: int, m: int, nr: int, n: int, L: int, stream=None):
+    _dev(src, "src")
+    _dev(dst, "dst")
+    _check(lib().nm_unshard_columns(src.data_ptr(), dst.data_ptr(), G, m, nr, n, L, src.element_size(),
+                                    _stream(src, stream)), "nm_unshard_columns")
+    return dst

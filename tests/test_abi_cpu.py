@@ -1,0 +1,103 @@
+"""CPU-side checks of the C ABI: libnmspmm.so builds for sm_100a, loads, exports
+every symbol include/*.h declares, and rejects bad arguments synchronously.
+No kernel is launched here (there is no GPU in the dev container); without a
+device the compute entry points must fail loudly with NM_ERR_CUDA (no CPU
+fallback)."""
+import ctypes
+import glob
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    names = []
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        src = open(h).read()
+        src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+        names += re.findall(r"^\s*(?:const\s+)?[A-Za-z_][\w]*\s*\**\s*(nm_\w+)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2503_01253_b200 import build, nmspmm
+    build.build()
+    return nmspmm.lib()
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ["nm_compress", "nm_spmm", "nm_decompress", "nm_validate", "nm_plan_query", "nm_last_error"]:
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol(L):
+    from paper_2503_01253_b200 import nmspmm
+    out = subprocess.run(["nm", "-D", "--defined-only", nmspmm.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT\s+(nm_\w+)", out))
+    missing = [f for f in declared_functions() if f not in exported]
+    assert not missing, missing
+    assert set(nmspmm.EXPORTS) <= set(declared_functions())
+
+
+def test_library_is_sm100a_only(L):
+    from paper_2503_01253_b200 import nmspmm
+    out = subprocess.run(["cuobjdump", "--list-elf", nmspmm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert all("sm_100a" in line for line in out.splitlines() if line.strip())
+
+
+def test_sass_uses_tma(L):
+    from paper_2503_01253_b200 import nmspmm
+    sass = subprocess.run(["cuobjdump", "-sass", nmspmm.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass  # TMA loads in the tiled kernels
+
+
+def test_version_and_config(L):
+    assert L.nm_version().decode().startswith("nmspmm")
+    assert L.nm_check_config(2, 4, 4) == 0
+    for N, M, Lv in [(0, 4, 1), (5, 4, 1), (1, 257, 1), (1, 4, 0)]:
+        assert L.nm_check_config(N, M, Lv) == 1
+    assert b"N:M" in L.nm_last_error()
+
+
+def test_argument_errors_are_synchronous(L):
+    P = ctypes.c_void_p(16)  # never dereferenced: the shape check fails first
+    # k % M != 0
+    assert L.nm_spmm(P, P, P, P, 8, 8, 6, 2, 4, 1, 0, 0, 0, None) == 2
+    # n % L != 0
+    assert L.nm_spmm(P, P, P, P, 8, 6, 8, 2, 4, 4, 0, 0, 0, None) == 2
+    # bad config
+    assert L.nm_spmm(P, P, P, P, 8, 8, 8, 5, 4, 1, 0, 0, 0, None) == 1
+    # fp32 operands with bf16 C is unsupported -- but only reported once a device exists;
+    # NULL pointers
+    assert L.nm_spmm(None, None, None, None, 8, 8, 8, 2, 4, 1, 0, 0, 0, None) == 8
+    # empty problem is a no-op
+    assert L.nm_spmm(None, None, None, None, 0, 8, 8, 2, 4, 1, 0, 0, 0, None) == 0
+    assert L.nm_compress(P, 0, 6, 8, 2, 4, 1, P, 0, P, None) == 2
+
+
+def test_no_cpu_fallback_without_device(L):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a device is present")
+    P = ctypes.c_void_p(256)
+    st = L.nm_spmm(P, P, P, P, 8, 8, 8, 2, 4, 1, 0, 0, 0, None)
+    assert st == 7 and b"no CUDA device" in L.nm_last_error()
+
+
+def test_plan_query_model(L):
+    from paper_2503_01253_b200 import nmspmm
+    import torch
+    p = nmspmm.nm_plan_query(4096, 4096, 4096, 16, 32, 32, torch.float32)
+    assert p["kernel"] == 1 and p["bm"] == 128 and p["bk"] == 64 and p["bkw"] == 32
+    assert p["flops"] == 2 * 4096 * 4096 * 2048
+    assert p["bytes"] == 4 * 4096 * 4096 + 4 * 2048 * 4096 + 2048 * 128 + 4 * 4096 * 4096
+    assert p["bound"] == 0  # FMA-bound
+    q = nmspmm.nm_plan_query(256, 255, 256, 2, 4, 3, torch.float32)
+    assert q["kernel"] == 0  # L % 4 != 0 -> generic

@@ -1,0 +1,254 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bars (BASELINE.json north star): compression and indices
+bit-exact; fp32 CUDA-core C within 1e-5 relative Frobenius of the fp64 oracle
+(O2); tf32/bf16 within 5e-3; integer-valued inputs bit-exact on every path."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2503_01253_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL_F32 = 1e-5
+TOL_BF16 = 5e-3
+
+
+@pytest.fixture(scope="module")
+def nm():
+    from paper_2503_01253_b200 import nmspmm
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    nmspmm.lib()
+    return nmspmm
+
+
+def dev(x: np.ndarray, dtype=torch.float32):
+    t = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    return t.to(dtype) if t.dtype != dtype else t
+
+
+def bf16_bits(t: torch.Tensor) -> np.ndarray:
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+# --------------------------------------------------------------- compression
+COMPRESS_CASES = [(2, 4, 4), (3, 8, 1), (2, 8, 8), (1, 8, 4), (16, 32, 32), (12, 32, 32), (4, 32, 64),
+                  (8, 32, 32), (5, 8, 3), (1, 2, 1), (64, 128, 16), (4, 4, 4)]
+
+
+@pytest.mark.parametrize("N,M,L", COMPRESS_CASES)
+@pytest.mark.parametrize("kind", ["uniform", "integer"])
+def test_compress_bit_exact(nm, oracle, N, M, L, kind):
+    k, n = 3 * M, 5 * L
+    B = synth.make(kind, (k, n), 7 + N, synth.TID_B)
+    vals_o, D_o = oracle.compress(B, N, M, L)
+    W = nm.nm_compress(dev(B), N, M, L)
+    assert np.array_equal(W.idx.cpu().numpy(), D_o)
+    assert np.array_equal(W.values.cpu().numpy().view(np.uint32), vals_o.view(np.uint32))
+    assert nm.nm_validate(W.idx, k, n, N, M, L) == -1
+    dense = nm.nm_decompress(W)
+    assert np.array_equal(dense.cpu().numpy(), oracle.decompress(vals_o, D_o, k, N, M, L))
+
+
+@pytest.mark.parametrize("N,M,L", [(16, 32, 32), (2, 4, 4), (3, 8, 2)])
+def test_compress_bf16_bit_exact(nm, oracle, N, M, L):
+    k, n = 4 * M, 6 * L
+    B = synth.uniform((k, n), 3, synth.TID_B)
+    vals_o, D_o = oracle.compress(B, N, M, L, values_bf16=True)
+    W = nm.nm_compress(dev(B), N, M, L, values_dtype=torch.bfloat16)
+    assert np.array_equal(W.idx.cpu().numpy(), D_o)
+    assert np.array_equal(bf16_bits(W.values), vals_o)
+    Bh = synth.bf16grid((k, n), 4, synth.TID_B)
+    vh_o, Dh_o = oracle.compress(synth.to_bf16_bits(Bh), N, M, L)
+    Wh = nm.nm_compress(dev(Bh, torch.bfloat16), N, M, L)
+    assert np.array_equal(Wh.idx.cpu().numpy(), Dh_o) and np.array_equal(bf16_bits(Wh.values), vh_o)
+
+
+@pytest.mark.parametrize("k,n,N,M,L", [(4096, 4096, 16, 32, 32), (4096, 11008, 8, 32, 32), (8192, 22016, 4, 32, 32)])
+def test_compress_bit_exact_full_size(nm, oracle, k, n, N, M, L):
+    B = synth.uniform((k, n), 2, synth.TID_B)
+    vals_o, D_o = oracle.compress(B, N, M, L)
+    W = nm.nm_compress(dev(B), N, M, L)
+    assert np.array_equal(W.idx.cpu().numpy(), D_o)
+    assert np.array_equal(W.values.cpu().numpy().view(np.uint32), vals_o.view(np.uint32))
+
+
+def test_compress_nan_and_inf(nm):
+    B = synth.uniform((64, 64), 1, 2)
+    B[5, 7] = np.nan
+    with pytest.raises(nm.NmError) as e:
+        nm.nm_compress(dev(B), 2, 4, 4)
+    assert e.value.status == 4
+    B[5, 7] = np.inf
+    W = nm.nm_compress(dev(B), 1, 4, 4)
+    assert W.idx[1, 1].item() == 1
+
+
+def test_validate_matches_oracle(nm, oracle):
+    k, n, N, M, L = 64, 32, 4, 16, 4
+    D = synth.random_mask(k, n, N, M, L, seed=9)
+    assert nm.nm_validate(dev(D, torch.uint8), k, n, N, M, L) == -1 == oracle.validate(D, k, n, N, M, L)
+    bad = D.copy()
+    bad[5, 3] = M
+    bad[9, 1] = bad[8, 1]
+    assert nm.nm_validate(dev(bad, torch.uint8), k, n, N, M, L) == oracle.validate(bad, k, n, N, M, L)
+
+
+# --------------------------------------------------------------- fp32 SpMM
+SPMM_CASES = [
+    # (m, n, k, N, M, L): several tiles + ragged tails (m % 128, n % 128, partial last panel)
+    (256, 256, 256, 2, 4, 4),      # cfg1
+    (300, 288, 320, 16, 32, 32),
+    (130, 136, 96, 12, 32, 8),
+    (257, 384, 512, 8, 32, 32),
+    (64, 520, 256, 4, 32, 8),
+    (200, 192, 192, 1, 8, 4),
+    (128, 256, 128, 3, 8, 16),
+    (96, 128, 224, 32, 32, 32),    # N = M (dense)
+    (129, 128, 256, 16, 32, 64),
+    (33, 96, 96, 2, 8, 12),        # L not a divisor of the tile
+    (70, 64, 64, 2, 4, 1),         # L = 1 -> generic kernel
+    (70, 66, 64, 2, 8, 3),         # L = 3 -> generic kernel
+    (40, 64, 256, 64, 128, 16),    # M > 64 -> generic kernel
+    (1, 128, 64, 2, 4, 4),         # single row
+]
+
+
+def run_f32(nm, oracle, m, n, k, N, M, L, kind="uniform", seed=0):
+    A = synth.make(kind, (m, k), 100 + seed, synth.TID_A)
+    B = synth.make(kind, (k, n), 200 + seed, synth.TID_B)
+    vals, D = oracle.compress(B, N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A), W).cpu().numpy()
+    return A, vals, D, C
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", SPMM_CASES)
+def test_spmm_f32_vs_oracle(nm, oracle, m, n, k, N, M, L):
+    A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L)
+    ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)
+    err = oracle.rel_frobenius(C, ref)
+    assert err <= TOL_F32, err
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", SPMM_CASES)
+def test_spmm_f32_integer_bit_exact(nm, oracle, m, n, k, N, M, L):
+    A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L, kind="integer", seed=1)
+    ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)
+    assert np.array_equal(C.astype(np.float64), ref)
+
+
+def test_spmm_f32_identity_a(nm, oracle):
+    k, n, N, M, L = 256, 256, 8, 32, 32
+    B = synth.uniform((k, n), 5, synth.TID_B)
+    vals, D = oracle.compress(B, N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(torch.eye(k, device="cuda"), W)
+    assert torch.equal(C, nm.nm_decompress(W))
+
+
+def test_spmm_f32_all_ones(nm):
+    m, n, k, N, M, L = 130, 256, 192, 12, 32, 32
+    w = k // M * N
+    D = synth.random_mask(k, n, N, M, L, seed=4)
+    W = nm.NmWeight(torch.ones(w, n, device="cuda"), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(torch.ones(m, k, device="cuda"), W)
+    assert bool((C == w).all())
+
+
+def test_spmm_f32_dense_matches_cublas(nm):
+    """N = M: the method is a dense GEMM (pin i); compare with cuBLAS fp32 (TF32 off)."""
+    m, n, k = 512, 384, 256
+    torch.backends.cuda.matmul.allow_tf32 = False
+    A = dev(synth.uniform((m, k), 1, 1))
+    B = dev(synth.uniform((k, n), 2, 2))
+    W = nm.nm_compress(B, 32, 32, 32)
+    C = nm.nm_spmm(A, W)
+    ref = A.double() @ B.double()
+    assert ((C.double() - ref).norm() / ref.norm()).item() < TOL_F32
+    assert ((torch.mm(A, B).double() - ref).norm() / ref.norm()).item() < TOL_F32
+
+
+def test_spmm_f32_deterministic(nm, oracle):
+    m, n, k, N, M, L = 512, 512, 1024, 8, 32, 32
+    A = dev(synth.uniform((m, k), 3, 1))
+    W = nm.nm_compress(dev(synth.uniform((k, n), 4, 2)), N, M, L)
+    C1 = nm.nm_spmm(A, W)
+    C2 = nm.nm_spmm(A, W)
+    assert torch.equal(C1, C2)
+
+
+def test_spmm_empty_and_errors(nm):
+    W = nm.nm_compress(dev(synth.uniform((64, 64), 1, 2)), 2, 4, 4)
+    C = nm.nm_spmm(torch.empty(0, 64, device="cuda"), W)
+    assert C.shape == (0, 64)
+    with pytest.raises(nm.NmError):
+        nm.nm_spmm(torch.zeros(8, 64, device="cuda"), W, out_dtype=torch.bfloat16)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3_62", "cfg3_75", "cfg4_65b"])
+def test_spmm_f32_full_size_sampled(nm, oracle, cfg):
+    """BASELINE.json sizes, bench launch configuration; oracle on a row sample."""
+    m, n, k, N, M, L = {"cfg2": (4096, 4096, 4096, 16, 32, 32), "cfg3_62": (2048, 11008, 4096, 12, 32, 32),
+                        "cfg3_75": (2048, 11008, 4096, 8, 32, 32), "cfg4_65b": (2048, 22016, 8192, 4, 32, 32)}[cfg]
+    A = synth.uniform((m, k), 11, synth.TID_A)
+    B = synth.uniform((k, n), 12, synth.TID_B)
+    W = nm.nm_compress(dev(B), N, M, L)
+    C = nm.nm_spmm(dev(A), W)
+    rows = np.array([0, 1, 127, 128, m // 2 + 3, m - 1])
+    vals = W.values.cpu().numpy()
+    D = W.idx.cpu().numpy()
+    ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L, rows=rows)
+    err = oracle.rel_frobenius(C[torch.from_numpy(rows).cuda()].cpu().numpy(), ref)
+    assert err <= TOL_F32, err
+
+
+# --------------------------------------------------------------- bf16 SpMM
+@pytest.mark.parametrize("m,n,k,N,M,L", [(256, 256, 256, 16, 32, 32), (130, 192, 96, 4, 32, 32),
+                                         (64, 64, 64, 2, 4, 4)])
+@pytest.mark.parametrize("cdt", [torch.bfloat16, torch.float32])
+def test_spmm_bf16_vs_oracle(nm, oracle, m, n, k, N, M, L, cdt):
+    A = synth.bf16grid((m, k), 21, synth.TID_A)
+    B = synth.bf16grid((k, n), 22, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=cdt).float().cpu().numpy()
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
+    assert oracle.rel_frobenius(C, ref) <= TOL_BF16
+
+
+def test_spmm_bf16_integer_exact_fp32_out(nm, oracle):
+    m, n, k, N, M, L = 200, 256, 256, 8, 32, 32
+    A = synth.integer((m, k), 31, synth.TID_A)
+    B = synth.integer((k, n), 32, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
+
+
+# --------------------------------------------------------------- host path / assembly
+def test_spmm_host_path(nm, oracle):
+    m, n, k, N, M, L = 257, 256, 512, 16, 32, 32
+    A = synth.uniform((m, k), 41, 1)
+    B = synth.uniform((k, n), 42, 2)
+    vals, D = oracle.compress(B, N, M, L)
+    run = nm.HostSpmm(m, n, k, N, M, L)
+    C = torch.empty(m, n).pin_memory()
+    run(torch.from_numpy(A).pin_memory(), torch.from_numpy(vals).pin_memory(), torch.from_numpy(D).pin_memory(), C)
+    assert oracle.rel_frobenius(C.numpy(), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
+
+
+@pytest.mark.parametrize("G", [1, 2, 3, 8])
+def test_unshard_columns(nm, G):
+    m, L, q = 37, 8, 43
+    n = q * L
+    full = torch.arange(m * n, dtype=torch.float32, device="cuda").reshape(m, n)
+    nr = L * ((q + G - 1) // G)
+    src = torch.full((G, m, nr), -1.0, device="cuda")
+    for r in range(G):
+        g0, g1 = r * q // G, (r + 1) * q // G
+        src[r, :, :(g1 - g0) * L] = full[:, g0 * L:g1 * L]
+    dst = torch.empty(m, n, device="cuda")
+    nm.nm_unshard_columns(src, dst, G, m, nr, n, L)
+    assert torch.equal(dst, full)
