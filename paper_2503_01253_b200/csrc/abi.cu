@@ -120,6 +120,11 @@ bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, cudaStream_t s);
+bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
+                        int L);
+void tc_bf16_geometry(int N, int M, int* wp, int* bk, int* bkw, int* bkw_pad);
+nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
+                         int64_t k, int N, int M, int L, cudaStream_t s);
 
 // ---------------------------------------------------------- generic kernel
 // One thread per C element; correct for every valid (N, M, L) and alignment.
@@ -187,7 +192,7 @@ static nm_status select(const void* A, const void* Bv, const void* C, int64_t m,
     }
     if (math == NM_MATH_AUTO || math == NM_MATH_BF16_TC) {
         *used = NM_MATH_BF16_TC;
-        *kernel = K_GENERIC;
+        *kernel = tc_bf16_applicable(A, Bv, C, m, n, k, N, M, L) ? K_TC_BF16 : K_GENERIC;
         return NM_OK;
     }
     return fail(NM_ERR_UNSUPPORTED, "math mode not available for bf16 operands");
@@ -266,6 +271,7 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
     if (kernel == K_SIMT_F32)
         return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
                                static_cast<float*>(C), m, n, k, N, M, L, s);
+    if (kernel == K_TC_BF16) return tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
     if (ab_dt == NM_F32) return generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
     if (c_dt == NM_BF16) return generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);
     return generic_launch<__nv_bfloat16, float>(A, values, idx, C, m, n, k, N, M, L, s);
@@ -334,6 +340,17 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->threads = 256;
         out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
         out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
+    } else if (kernel == K_TC_BF16) {
+        int wp, bk, bkw, bkwp;
+        tc_bf16_geometry(N, M, &wp, &bk, &bkw, &bkwp);
+        out->bm = 128;
+        out->bn = 128;
+        out->bk = bk;
+        out->bkw = bkw;
+        out->stages = 3;
+        out->threads = 288;
+        out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
+        out->smem_bytes = 3 * 64 * 128 * 2 + 2 * 128 * (128 * 2 + 4) + 2 * 8 * 64 * 2 + 128 + 1024;
     } else {
         out->bm = 8;
         out->bn = 32;

@@ -252,3 +252,65 @@ def test_unshard_columns(nm, G):
     dst = torch.empty(m, n, device="cuda")
     nm.nm_unshard_columns(src, dst, G, m, nr, n, L)
     assert torch.equal(dst, full)
+
+
+# --------------------------------------------------------------- tcgen05 bf16 path
+TC_CASES = [
+    # (m, n, k, N, M, L)
+    (128, 128, 128, 16, 32, 32),
+    (256, 256, 256, 16, 32, 32),
+    (300, 384, 512, 16, 32, 32),    # ragged m, 3 column tiles, 4 panels
+    (128, 192, 96, 4, 32, 32),      # ragged n tile, single partial panel
+    (200, 256, 384, 12, 32, 32),    # BKW = 48
+    (130, 256, 256, 8, 32, 16),     # L = 16 (N = 16 MMAs)
+    (130, 256, 256, 8, 32, 64),     # L = 64 (128-byte swizzle)
+    (64, 256, 256, 8, 32, 128),     # L = 128 (two 64-column atoms per group)
+    (96, 128, 64, 8, 8, 32),        # M = 8 windows, dense N = M
+    (257, 128, 640, 2, 16, 32),     # BKW padded 40 -> 48
+]
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
+@pytest.mark.parametrize("cdt", [torch.bfloat16, torch.float32])
+def test_spmm_tc_bf16_vs_oracle(nm, oracle, m, n, k, N, M, L, cdt):
+    A = synth.bf16grid((m, k), 51, synth.TID_A)
+    B = synth.bf16grid((k, n), 52, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    plan = nm.nm_plan_query(m, n, k, N, M, L, torch.bfloat16, "bf16_tc")
+    assert plan["kernel"] == 2, plan  # the tcgen05 kernel, not the generic fallback
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=cdt, math="bf16_tc").float().cpu().numpy()
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
+    assert oracle.rel_frobenius(C, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
+def test_spmm_tc_bf16_integer_exact(nm, oracle, m, n, k, N, M, L):
+    """Integer inputs: every partial sum is exact in fp32 -> bit-exact C (fp32 out)."""
+    A = synth.integer((m, k), 61, synth.TID_A)
+    B = synth.integer((k, n), 62, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32, math="bf16_tc").cpu().numpy()
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
+
+
+def test_spmm_tc_bf16_deterministic(nm):
+    A = dev(synth.bf16grid((512, 1024), 1, 1), torch.bfloat16)
+    W = nm.nm_compress(dev(synth.bf16grid((1024, 512), 2, 2), torch.bfloat16), 8, 32, 32)
+    assert torch.equal(nm.nm_spmm(A, W), nm.nm_spmm(A, W))
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3_62", "cfg3_75", "cfg4_65b"])
+def test_spmm_tc_bf16_full_size_sampled(nm, oracle, cfg):
+    m, n, k, N, M, L = {"cfg2": (4096, 4096, 4096, 16, 32, 32), "cfg3_62": (2048, 11008, 4096, 12, 32, 32),
+                        "cfg3_75": (2048, 11008, 4096, 8, 32, 32), "cfg4_65b": (2048, 22016, 8192, 4, 32, 32)}[cfg]
+    A = synth.bf16grid((m, k), 71, synth.TID_A)
+    B = synth.bf16grid((k, n), 72, synth.TID_B)
+    W = nm.nm_compress(dev(B, torch.bfloat16), N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W)
+    rows = np.array([0, 5, 127, 128, m // 2 + 7, m - 1])
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), bf16_bits(W.values), W.idx.cpu().numpy(), k, N, M, L,
+                                 rows=rows)
+    got = C[torch.from_numpy(rows).cuda()].float().cpu().numpy()
+    assert oracle.rel_frobenius(got, ref) <= TOL_BF16
