@@ -63,6 +63,34 @@ static nm_status require_device() {
     return NM_OK;
 }
 
+// --------------------------------------------------------- scratch memory pool
+// Per-call scratch (the tcgen05 path's cell tables) comes from a library-owned
+// stream-ordered pool whose release threshold keeps freed blocks cached, so a
+// steady stream of nm_spmm calls allocates nothing after the first one.
+static std::once_flag g_pool_once;
+static cudaMemPool_t g_pool = nullptr;
+
+nm_status scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
+    std::call_once(g_pool_once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaMemPoolProps props{};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&g_pool, &props) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(g_pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        } else {
+            g_pool = nullptr;
+        }
+        cudaGetLastError();
+    });
+    cudaError_t e = g_pool ? cudaMallocFromPoolAsync(p, bytes, g_pool, s) : cudaMallocAsync(p, bytes, s);
+    if (e != cudaSuccess) return cuda_fail(e, "scratch allocation");
+    return NM_OK;
+}
+
 // ------------------------------------------------------------------ TMA
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -122,7 +150,7 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
                           int N, int M, int L, cudaStream_t s);
 bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                         int L);
-void tc_bf16_geometry(int N, int M, int* wp, int* bk, int* bkw, int* bkw_pad);
+void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn);
 nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                          int64_t k, int N, int M, int L, cudaStream_t s);
 
@@ -341,16 +369,16 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
         out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
     } else if (kernel == K_TC_BF16) {
-        int wp, bk, bkw, bkwp;
-        tc_bf16_geometry(N, M, &wp, &bk, &bkw, &bkwp);
+        int wp, bk, bkw, bkwp, bn;
+        tc_bf16_geometry(N, M, L, &wp, &bk, &bkw, &bkwp, &bn);
         out->bm = 128;
-        out->bn = 128;
+        out->bn = bn;
         out->bk = bk;
         out->bkw = bkw;
         out->stages = 3;
-        out->threads = 288;
-        out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
-        out->smem_bytes = 3 * 64 * 128 * 2 + 2 * 128 * (128 * 2 + 4) + 2 * 8 * 64 * 2 + 128 + 1024;
+        out->threads = 544;
+        out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, bn));
+        out->smem_bytes = 3 * 64 * bn * 2 + 2 * 128 * (128 * 2 + 4) + 2 * 3 * 256 * 4 + 15 * 8 + 16 + 1024;
     } else {
         out->bm = 8;
         out->bn = 32;
