@@ -40,7 +40,8 @@ CONFIGS = {
     "cfg4_65b": (2048, 22016, 8192, 4, 32, 32),
 }
 HEADLINE = "cfg2"
-VARIANTS = ["cfg3_62", "cfg3_75", "cfg4_65b"]
+VARIANTS = ["cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_65b:f32", "cfg3_62:bf16", "cfg3_75:bf16",
+            "cfg4_65b:bf16"]
 
 
 def load_peaks():
@@ -160,15 +161,21 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True):
     A, Bd, W = make_inputs(cfg, dtype, "cuda")
     C = torch.empty(cfg[0], cfg[1], dtype=dtype, device="cuda")
     math = "f32_simt" if dtype == torch.float32 else "auto"
-    ms = time_steps(lambda: nmspmm.nm_spmm(A, W, out=C, math=math), steps, warmup, stream, flush)
-    t = statistics.median(ms)
-    res = {"ms": t, "ms_mean": statistics.fmean(ms), "tflops": flop_count(cfg) / (t * 1e-3) / 1e12,
+    for _ in range(warmup):
+        nmspmm.nm_spmm(A, W, out=C, math=math)
+    nmspmm.nm_profile_begin()
+    ms = time_steps(lambda: nmspmm.nm_spmm(A, W, out=C, math=math), steps, 0, stream, flush)
+    k_ms, k_cnt, launches = nmspmm.nm_profile_end()
+    t = statistics.fmean(ms)
+    kms = k_ms / max(1, k_cnt)
+    res = {"ms": t, "tflops": flop_count(cfg) / (t * 1e-3) / 1e12, "kernel_ms": kms,
+           "kernel_tflops": flop_count(cfg) / (kms * 1e-3) / 1e12, "launches_per_step": launches / steps,
            "plan": nmspmm.nm_plan_query(*cfg, dtype=dtype, math=math)}
     if with_cublas:
         torch.backends.cuda.matmul.allow_tf32 = False
         Cd = torch.empty_like(C)
         msd = time_steps(lambda: torch.mm(A, Bd, out=Cd), steps, warmup, stream, flush)
-        td = statistics.median(msd)
+        td = statistics.fmean(msd)
         m, n, k = cfg[:3]
         res.update({"cublas_ms": td, "cublas_dense_tflops": 2.0 * m * n * k / (td * 1e-3) / 1e12,
                     "speedup_vs_cublas": td / t, "target_speedup": 0.7 * cfg[4] / cfg[3]})
@@ -302,12 +309,13 @@ def run_ours(args):
         sampler = ClockSampler(local)
         with sampler:
             t0 = time.perf_counter()
+            nmspmm.nm_profile_begin()
             ms = time_steps(step, args.steps, 0, stream, flush)
+            k_ms, k_cnt, launches = nmspmm.nm_profile_end()
             wall = time.perf_counter() - t0
         t_step = statistics.fmean(ms)
         value = flop_count(cfg) / (t_step * 1e-3) / 1e12
-        launches = args.steps
-        kernel_ms = t_step
+        kernel_ms = k_ms / max(1, k_cnt)  # dominant SpMM kernel, CUDA events on its stream
         del Bd
         if args.profile:
             print(json.dumps({"profile_run": True, "ms": t_step}), flush=True)
@@ -335,16 +343,20 @@ def run_ours(args):
                 "peak": round(peak, 2), "unit": "TFLOP/s", "frac": None,
                 "peak_source": f"derived: 148 SMs x 128 FP32 lanes x 2 FLOP x {sm_mhz:.0f} MHz (sm_max_mhz, {peaks_src})",
                 "kernel": "nm::simt::spmm_simt_f32_kernel",
+                "kernel_ms_per_launch": round(kernel_ms, 4), "kernel_share_of_step": round(kernel_ms / t_step, 4),
                 "algorithmic_flops_per_launch": flop_count(cfg),
                 "algorithmic_bytes_per_launch": alg_bytes(cfg, 4)}
     else:
         peak = peaks.get("bf16_tflops", 1590.0)
         roof = {"bound": "tensor", "achieved": round(flop_count(cfg) / (kernel_ms * 1e-3) / 1e12, 3),
                 "peak": peak, "unit": "TFLOP/s", "frac": None, "peak_source": f"bf16_tflops ({peaks_src})",
-                "kernel": "nm_spmm bf16", "algorithmic_flops_per_launch": flop_count(cfg),
+                "kernel": "nm::tc::spmm_tc_bf16_kernel", "kernel_ms_per_launch": round(kernel_ms, 4),
+                "kernel_share_of_step": round(kernel_ms / t_step, 4), "algorithmic_flops_per_launch": flop_count(cfg),
                 "algorithmic_bytes_per_launch": alg_bytes(cfg, 2)}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)
-    roof["traffic"] = traffic_for(f"{args.config}_{args.dtype}")
+    tr = traffic_for(f"{args.config}_{args.dtype}")
+    roof["traffic"] = tr["dram_bytes_per_launch"] if tr else None
+    roof["traffic_source"] = tr["source"] if tr else "no ncu capture for this config"
 
     line = {"metric": "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M; speedup vs cuBLAS dense",
             "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
@@ -358,14 +370,21 @@ def run_ours(args):
         line["e2e"] = e2e_measure(cfg, dtype, max(3, args.steps // 4), args.warmup)
         line["cpu_baseline"] = cpu_baseline(cfg, target_s=args.ref_seconds)
         variants = []
-        for name in args.variants.split(",") if args.variants else []:
+        for item in args.variants.split(",") if args.variants else []:
+            name, _, vdt = item.partition(":")
+            vdt = vdt or args.dtype
             vcfg = CONFIGS[name]
-            r, _ = measure_config(vcfg, dtype, max(5, args.steps // 2), args.warmup, flush)
-            variants.append({"config": name, "m_n_k": vcfg[:3], "N:M": f"{vcfg[3]}:{vcfg[4]}", "L": vcfg[5],
-                             "tflops": round(r["tflops"], 3), "ms": round(r["ms"], 4),
+            tdt = torch.float32 if vdt == "f32" else torch.bfloat16
+            r, _ = measure_config(vcfg, tdt, max(5, args.steps // 2), args.warmup, flush)
+            peak_v = fp32_alu_peak_tflops(sm_mhz) if vdt == "f32" else peaks.get("bf16_tflops", 1590.0)
+            variants.append({"config": name, "dtype": vdt, "m_n_k": vcfg[:3], "N:M": f"{vcfg[3]}:{vcfg[4]}",
+                             "L": vcfg[5], "tflops": round(r["tflops"], 3), "ms": round(r["ms"], 4),
+                             "kernel_tflops": round(r["kernel_tflops"], 3),
+                             "roofline_frac": round(r["kernel_tflops"] / peak_v, 4),
+                             "roofline_bound": "alu" if vdt == "f32" else "tensor",
                              "cublas_dense_tflops": round(r["cublas_dense_tflops"], 3),
                              "speedup_vs_cublas": round(r["speedup_vs_cublas"], 3),
-                             "target_speedup": r["target_speedup"]})
+                             "target_speedup": round(r["target_speedup"], 3)})
             torch.cuda.empty_cache()
         line["variants"] = variants
     print(json.dumps(line), flush=True)

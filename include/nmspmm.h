@@ -167,6 +167,18 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
 nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, int64_t nr, int64_t n, int L,
                              int elem_bytes, void* stream);
 
+/*
+ * nm_profile_begin / nm_profile_end -- launch accounting for measurement
+ * (bench.py).  Between the two calls the library counts every kernel it
+ * launches and records a CUDA event pair on the launching stream around each
+ * dominant SpMM kernel.  nm_profile_end synchronises on the last event and
+ * returns the summed duration of those kernels (*kernel_ms, their number in
+ * *kernel_count) and the total launch count (*launches); any pointer may be
+ * NULL.  Process-wide state, not intended for concurrent profiling sessions.
+ */
+nm_status nm_profile_begin(void);
+nm_status nm_profile_end(double* kernel_ms, int64_t* kernel_count, int64_t* launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -5,7 +5,9 @@
 #include <cuda_bf16.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -62,6 +64,33 @@ static nm_status require_device() {
                                             std::to_string(g_cc));
     return NM_OK;
 }
+
+// ------------------------------------------------------------ profiling
+struct ProfState {
+    bool on = false;
+    int64_t launches = 0;
+    std::vector<cudaEvent_t> ev;  // begin/end pairs
+    size_t used = 0;
+};
+static std::mutex g_prof_mu;
+static ProfState g_prof;
+
+void note_launch() {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (g_prof.on) ++g_prof.launches;
+}
+static void prof_record(cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    if (!g_prof.on) return;
+    if (g_prof.used == g_prof.ev.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        g_prof.ev.push_back(e);
+    }
+    cudaEventRecord(g_prof.ev[g_prof.used++], s);
+}
+void prof_begin(cudaStream_t s) { prof_record(s); }
+void prof_end(cudaStream_t s) { prof_record(s); }
 
 // --------------------------------------------------------- scratch memory pool
 // Per-call scratch (the tcgen05 path's cell tables) comes from a library-owned
@@ -147,7 +176,7 @@ bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, cudaStream_t s);
+                          int N, int M, int L, bool use_at, cudaStream_t s);
 bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                         int L);
 void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn);
@@ -197,13 +226,27 @@ static nm_status generic_launch(const void* A, const void* Bv, const uint8_t* D,
     const int64_t gy = ceil_div(m, 8);
     if (gy > 65535) return fail(NM_ERR_UNSUPPORTED, "generic kernel: m too large");
     const dim3 grid(static_cast<unsigned>(ceil_div(n, 32)), static_cast<unsigned>(gy));
+    prof_begin(s);
     spmm_generic_kernel<TA, TC><<<grid, block, 0, s>>>(static_cast<const TA*>(A), static_cast<const TA*>(Bv), D,
                                                        static_cast<TC*>(C), m, n, k, N, M, L);
+    prof_end(s);
+    note_launch();
     NM_LAUNCH_CHECK("spmm_generic_kernel");
     return NM_OK;
 }
 
 // ------------------------------------------------------------------ selector
+// A^T staging for the SIMT kernel costs one read + one write of A (2*4*m*k bytes at
+// HBM speed) and saves ~6 of ~22 non-FFMA instructions per 64 FFMA in the inner
+// loop; it pays once the FFMA time dwarfs the transpose, i.e. for more than a
+// couple of column tiles.  NM_SIMT_AT=0/1 overrides (ablation).
+static bool simt_use_at(int64_t m, int64_t n, int64_t k) {
+    const char* e = getenv("NM_SIMT_AT");
+    if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
+    (void)k;
+    return n >= 512 && m % 4 == 0;
+}
+
 enum KernelId { K_GENERIC = 0, K_SIMT_F32 = 1, K_TC_BF16 = 2, K_TC_TF32 = 3 };
 
 static nm_status select(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
@@ -298,7 +341,7 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
     if ((st = select(A, values, C, m, n, k, N, M, L, ab_dt, c_dt, math, &kernel, &used))) return st;
     if (kernel == K_SIMT_F32)
         return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
-                               static_cast<float*>(C), m, n, k, N, M, L, s);
+                               static_cast<float*>(C), m, n, k, N, M, L, simt_use_at(m, n, k), s);
     if (kernel == K_TC_BF16) return tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
     if (ab_dt == NM_F32) return generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
     if (c_dt == NM_BF16) return generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);
@@ -391,6 +434,34 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
     out->t_compute_us = out->flops / peak_flops * 1e6;
     out->t_memory_us = out->bytes / peak_hbm * 1e6;
     out->bound = out->t_memory_us > out->t_compute_us ? 1 : 0;
+    return NM_OK;
+}
+
+nm_status nm_profile_begin(void) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.on = true;
+    g_prof.launches = 0;
+    g_prof.used = 0;
+    return NM_OK;
+}
+
+nm_status nm_profile_end(double* kernel_ms, int64_t* kernel_count, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.on = false;
+    double tot = 0.0;
+    int64_t cnt = 0;
+    for (size_t i = 0; i + 1 < g_prof.used; i += 2) {
+        cudaError_t e = cudaEventSynchronize(g_prof.ev[i + 1]);
+        if (e != cudaSuccess) return cuda_fail(e, "nm_profile_end");
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, g_prof.ev[i], g_prof.ev[i + 1]) == cudaSuccess) {
+            tot += ms;
+            ++cnt;
+        }
+    }
+    if (kernel_ms) *kernel_ms = tot;
+    if (kernel_count) *kernel_count = cnt;
+    if (launches) *launches = g_prof.launches;
     return NM_OK;
 }
 

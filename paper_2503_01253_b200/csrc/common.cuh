@@ -33,6 +33,13 @@ nm_status cuda_fail(cudaError_t e, const char* what);
 int num_sms();  // cached device property (148 on B200)
 nm_status scratch_alloc(void** p, size_t bytes, cudaStream_t s);  // library-owned stream-ordered pool
 
+// Launch accounting for nm_profile_begin/end: every kernel launch of the product
+// path calls note_launch(); the dominant SpMM kernel is bracketed by
+// prof_begin/prof_end, which record CUDA events on its stream while profiling is on.
+void note_launch();
+void prof_begin(cudaStream_t s);
+void prof_end(cudaStream_t s);
+
 // TMA descriptor encoding (cuTensorMapEncodeTiled fetched via cudaGetDriverEntryPoint).
 // 2-D row-major tensor [rows][cols] of elem_bytes elements; box [box_rows][box_cols].
 // swizzle: 0 none, 128 = 128-byte swizzle.  OOB elements are zero-filled.

@@ -205,6 +205,7 @@ nm_status unshard_launch(const void* src, void* dst, int64_t G, int64_t m, int64
     else
         unshard_kernel<uint32_t><<<blocks, threads, 0, s>>>(static_cast<const uint32_t*>(src),
                                                             static_cast<uint32_t*>(dst), G, m, nr, q, L);
+    note_launch();
     NM_LAUNCH_CHECK("unshard_kernel");
     return NM_OK;
 }

@@ -46,7 +46,11 @@ __device__ __forceinline__ int a_col_offset(int kk) {
 }
 
 // TWO: the thread's two 4-column chunks may belong to different column groups (L < 32).
-template <bool TWO>
+// AT:  A arrives transposed (A^T, k x m, written by transpose_kernel): the panel is
+//      [BK k-rows][128 m] and a gathered fragment is two LDS.128 of row kabs
+//      (8 rows of A); otherwise the panel is [128 m][BK] (swizzled) and a fragment is
+//      eight LDS.32 of column kabs.
+template <bool TWO, bool AT>
 __global__ void __launch_bounds__(THREADS, 2)
     spmm_simt_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const Params p) {
@@ -74,13 +78,17 @@ __global__ void __launch_bounds__(THREADS, 2)
     }
     __syncthreads();
 
-    const uint32_t stage_tx = static_cast<uint32_t>(p.nboxA * A_BOX_BYTES + p.bkw * BN * 4);
+    const uint32_t stage_tx =
+        static_cast<uint32_t>((AT ? p.bk * BM * 4 : p.nboxA * A_BOX_BYTES) + p.bkw * BN * 4);
     auto issue = [&](int panel) {
         const int s = panel % STAGES;
         mbar_arrive_expect_tx(&bars[s], stage_tx);
         const int k0 = panel * p.bk, u0 = panel * p.bkw;
-        for (int b = 0; b < p.nboxA; ++b)
-            tma_load_2d(sA + s * A_STAGE_BYTES + b * A_BOX_BYTES, &tmA, &bars[s], k0 + b * A_BOX_COLS, m0);
+        if (AT)
+            tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &bars[s], m0, k0);
+        else
+            for (int b = 0; b < p.nboxA; ++b)
+                tma_load_2d(sA + s * A_STAGE_BYTES + b * A_BOX_BYTES, &tmA, &bars[s], k0 + b * A_BOX_COLS, m0);
         tma_load_2d(sB + s * B_STAGE_BYTES, &tmB, &bars[s], n0, u0);
     };
 
@@ -107,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             const int u = e / nslots, s = e - u * nslots;
             if (u < BKW && s < nslots) {
                 const int kk = ((u0 + u) / p.N - t0) * p.M + dreg[r];  // dense column inside the panel
-                kb[u * MAX_SLOTS + s] = a_col_offset(kk);
+                kb[u * MAX_SLOTS + s] = AT ? kk * (BM * 4) : a_col_offset(kk);
             }
         }
     };
@@ -122,8 +130,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     // columns past n (ragged tile) read a valid slot; their results are never stored
     const int slot0 = min((n0 + col0) / p.L - g_first, nslots - 1);
     const int slot1 = min((n0 + col0 + 16) / p.L - g_first, nslots - 1);
-    const int tmx = t_m << 4;
-    const int a_row = (wm * 64 + t_m) * 128;
+    const int tmx = AT ? 0 : (t_m << 4);
+    const int a_row = AT ? (wm * 64 + 4 * t_m) * 4 : (wm * 64 + t_m) * 128;
 
     float acc[8][8];
 #pragma unroll
@@ -151,12 +159,26 @@ __global__ void __launch_bounds__(THREADS, 2)
             const uint8_t* ap0 = aS + (krow[slot0] ^ tmx);
             b0 = *reinterpret_cast<const float4*>(bS + u * BN);
             b1 = *reinterpret_cast<const float4*>(bS + u * BN + 16);
+            if (AT) {
+                const float4 x0 = *reinterpret_cast<const float4*>(ap0);
+                const float4 x1 = *reinterpret_cast<const float4*>(ap0 + 128);
+                a0[0] = x0.x, a0[1] = x0.y, a0[2] = x0.z, a0[3] = x0.w;
+                a0[4] = x1.x, a0[5] = x1.y, a0[6] = x1.z, a0[7] = x1.w;
+            } else {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) a0[i] = *reinterpret_cast<const float*>(ap0 + i * 1024);
+                for (int i = 0; i < 8; ++i) a0[i] = *reinterpret_cast<const float*>(ap0 + i * 1024);
+            }
             if (TWO) {
                 const uint8_t* ap1 = aS + (krow[slot1] ^ tmx);
+                if (AT) {
+                    const float4 x0 = *reinterpret_cast<const float4*>(ap1);
+                    const float4 x1 = *reinterpret_cast<const float4*>(ap1 + 128);
+                    a1[0] = x0.x, a1[1] = x0.y, a1[2] = x0.z, a1[3] = x0.w;
+                    a1[4] = x1.x, a1[5] = x1.y, a1[6] = x1.z, a1[7] = x1.w;
+                } else {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) a1[i] = *reinterpret_cast<const float*>(ap1 + i * 1024);
+                    for (int i = 0; i < 8; ++i) a1[i] = *reinterpret_cast<const float*>(ap1 + i * 1024);
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) a1[i] = a0[i];
@@ -181,7 +203,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int gc0 = n0 + col0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const int row = m0 + wm * 64 + 8 * i + t_m;
+        const int row = m0 + wm * 64 + (AT ? (i & 3) + 4 * t_m + 32 * (i >> 2) : 8 * i + t_m);
         if (row >= p.m) continue;
         float* crow = p.C + static_cast<int64_t>(row) * p.n;
         if (gc0 < p.n) *reinterpret_cast<float4*>(crow + gc0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
@@ -212,8 +234,43 @@ void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw) {
     *bkw = w * N;
 }
 
+// A (m x k) -> A^T (k x m): 32x32 tiles through padded shared memory, coalesced both ways.
+__global__ void transpose_kernel(const float* __restrict__ A, float* __restrict__ AT, int m, int k) {
+    __shared__ float t[32][33];
+    const int k0 = blockIdx.x * 32, m0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int i = m0 + r, j = k0 + threadIdx.x;
+        if (i < m && j < k) t[r][threadIdx.x] = A[static_cast<int64_t>(i) * k + j];
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += 8) {
+        const int j = k0 + r, i = m0 + threadIdx.x;
+        if (i < m && j < k) AT[static_cast<int64_t>(j) * m + i] = t[threadIdx.x][r];
+    }
+}
+
+template <bool TWO, bool AT>
+static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, const simt::Params& p, dim3 grid,
+                             cudaStream_t s) {
+    using namespace simt;
+    static bool attr_done = false;
+    if (!attr_done) {
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         SMEM_BYTES));
+        attr_done = true;
+    }
+    prof_begin(s);
+    spmm_simt_f32_kernel<TWO, AT><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p);
+    prof_end(s);
+    note_launch();
+    NM_LAUNCH_CHECK("spmm_simt_f32_kernel");
+    return NM_OK;
+}
+
+// use_at: stage A transposed (one extra pass over A, 2 fewer shared-memory
+// instructions per 16 FFMA in the inner loop); the selector decides.
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, cudaStream_t s) {
+                          int N, int M, int L, bool use_at, cudaStream_t s) {
     using namespace simt;
     Params p{};
     p.D = D;
@@ -230,31 +287,36 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     p.npanels = (windows + p.wp - 1) / p.wp;
     p.nboxA = (p.bk + A_BOX_COLS - 1) / A_BOX_COLS;
     const int64_t w = k / M * N;
+    use_at = use_at && (m % 4 == 0);  // A^T rows (m floats) must be 16-B multiples for TMA
 
     CUtensorMap tmA, tmB;
-    nm_status st = make_tma_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, m, k, BM, A_BOX_COLS, 128);
+    nm_status st = make_tma_2d(&tmB, Bv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, w, n, p.bkw, BN, 0);
     if (st) return st;
-    st = make_tma_2d(&tmB, Bv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, w, n, p.bkw, BN, 0);
+    float* AT = nullptr;
+    if (use_at) {
+        st = scratch_alloc(reinterpret_cast<void**>(&AT), static_cast<size_t>(m * k) * sizeof(float), s);
+        if (st) return st;
+        const dim3 tg(static_cast<unsigned>(ceil_div(k, 32)), static_cast<unsigned>(ceil_div(m, 32)));
+        transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, AT, static_cast<int>(m), static_cast<int>(k));
+        note_launch();
+        NM_LAUNCH_CHECK("transpose_kernel");
+        st = make_tma_2d(&tmA, AT, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k, m, p.bk, BM, 0);
+    } else {
+        st = make_tma_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, m, k, BM, A_BOX_COLS, 128);
+    }
     if (st) return st;
 
     const dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(m, BM)));
     const bool two = L < 32;
-    static bool attr_done[2] = {false, false};
-    if (!attr_done[two]) {
-        if (two)
-            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             SMEM_BYTES));
-        else
-            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<false>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-        attr_done[two] = true;
-    }
-    if (two)
-        spmm_simt_f32_kernel<true><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p);
+    if (use_at)
+        st = two ? launch_simt<true, true>(tmA, tmB, p, grid, s) : launch_simt<false, true>(tmA, tmB, p, grid, s);
     else
-        spmm_simt_f32_kernel<false><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p);
-    NM_LAUNCH_CHECK("spmm_simt_f32_kernel");
-    return NM_OK;
+        st = two ? launch_simt<true, false>(tmA, tmB, p, grid, s) : launch_simt<false, false>(tmA, tmB, p, grid, s);
+    if (AT) {
+        cudaError_t e = cudaFreeAsync(AT, s);
+        if (e != cudaSuccess && st == NM_OK) st = cuda_fail(e, "cudaFreeAsync");
+    }
+    return st;
 }
 
 }  // namespace nm

@@ -505,7 +505,10 @@ static nm_status tc_launch_bn(const tc::Params& p, const CUtensorMap& tmA, const
         attr = true;
     }
     const dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(m, BM)));
+    prof_begin(s);
     spmm_tc_bf16_kernel<BN><<<grid, THREADS, Smem<BN>::BYTES, s>>>(tmA, tmB, p);
+    prof_end(s);
+    note_launch();
     NM_LAUNCH_CHECK("spmm_tc_bf16_kernel");
     return NM_OK;
 }
@@ -545,6 +548,7 @@ nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* 
     if (st) return st;
     build_cell_table_kernel<<<dim3(p.npanels, ntiles), 256, 0, s>>>(D, tbl, p.q, N, M, L, bn, p.bk, p.bkw, p.bkw_pad,
                                                                       p.npanels, static_cast<int>(w));
+    note_launch();
     NM_LAUNCH_CHECK("build_cell_table_kernel");
     p.tbl = tbl;
     st = bn == 256 ? tc_launch_bn<256>(p, tmA, tmB, m, n, s) : tc_launch_bn<128>(p, tmA, tmB, m, n, s);

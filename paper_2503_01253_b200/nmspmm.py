@@ -25,7 +25,8 @@ NM_F32, NM_BF16 = 0, 1
 MATH = {"auto": 0, "f32_simt": 1, "tf32_tc": 2, "bf16_tc": 3}
 
 EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_decompress", "nm_validate",
-           "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns"]
+           "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
+           "nm_profile_begin", "nm_profile_end"]
 
 
 class NmError(RuntimeError):
@@ -69,6 +70,8 @@ def lib():
         L.nm_plan_query.argtypes = [I64, I64, I64, I, I, I, I, I, ctypes.c_double, ctypes.c_double,
                                     ctypes.POINTER(Plan)]
         L.nm_unshard_columns.argtypes = [P, P, I64, I64, I64, I64, I, I, P]
+        L.nm_profile_begin.argtypes = []
+        L.nm_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         for name in EXPORTS[2:]:
             if name != "nm_spmm_host_ws_bytes":
                 getattr(L, name).restype = I
@@ -207,6 +210,17 @@ def nm_plan_query(m, n, k, N, M, L, dtype=torch.float32, math="auto", peak_flops
     _check(lib().nm_plan_query(m, n, k, N, M, L, NM_F32 if dtype == torch.float32 else NM_BF16, MATH[math],
                                float(peak_flops), float(peak_hbm), ctypes.byref(p)), "nm_plan_query")
     return p.as_dict()
+
+
+def nm_profile_begin():
+    _check(lib().nm_profile_begin(), "nm_profile_begin")
+
+
+def nm_profile_end():
+    '''(summed ms of the dominant SpMM kernels, their number, total kernel launches).'''
+    ms, cnt, nl = ctypes.c_double(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(lib().nm_profile_end(ctypes.byref(ms), ctypes.byref(cnt), ctypes.byref(nl)), "nm_profile_end")
+    return ms.value, cnt.value, nl.value
 
 
 def nm_unshard_columns(src: torch.Tensor, dst: torch.Tensor, G: int, m: int, nr: int, n: int, L: int, stream=None):
