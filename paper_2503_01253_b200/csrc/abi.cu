@@ -4,6 +4,7 @@
 // needs a CUDA device and returns NM_ERR_CUDA without one.
 #include <cuda_bf16.h>
 
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -176,7 +177,10 @@ bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, bool use_at, cudaStream_t s);
+                          int N, int M, int L, int mode, cudaStream_t s);
+bool simt_pipe_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
+nm_status simt_pipe_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
+                           int N, int M, int L, cudaStream_t s);
 bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                         int L);
 void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn);
@@ -236,15 +240,40 @@ static nm_status generic_launch(const void* A, const void* Bv, const uint8_t* D,
 }
 
 // ------------------------------------------------------------------ selector
-// A^T staging for the SIMT kernel costs one read + one write of A (2*4*m*k bytes at
-// HBM speed) and saves ~6 of ~22 non-FFMA instructions per 64 FFMA in the inner
-// loop; it pays once the FFMA time dwarfs the transpose, i.e. for more than a
-// couple of column tiles.  NM_SIMT_AT=0/1 overrides (ablation).
-static bool simt_use_at(int64_t m, int64_t n, int64_t k) {
+// A^T staging for the SIMT kernel costs one read + one write of A (8*m*k bytes,
+// measured ~2.9 TB/s) and saves ~15 % of the SpMM time (2 LDS.128 instead of 8 LDS.32
+// per gathered fragment; r01 profiles).  Break-even: 0.15 * 2*m*n*w / 48 TF/s >
+// 8*m*k / 2.9 TB/s  <=>  n*N/M > ~440.  NM_SIMT_AT=0/1 overrides (ablation).
+static bool simt_use_at(int64_t m, int64_t n, int64_t k, int N, int M) {
     const char* e = getenv("NM_SIMT_AT");
     if (e && (e[0] == '0' || e[0] == '1')) return e[0] == '1';
     (void)k;
-    return n >= 512 && m % 4 == 0;
+    return m % 4 == 0 && n * N >= 512 * static_cast<int64_t>(M);
+}
+
+// Packing (the paper's high-sparsity mode, Listing 3): fetch only the
+// union of the columns the G = 128/L groups of a column tile select.  For masks that
+// are independent across groups the expected union is 1 - (1 - N/M)^G of the panel
+// (16:32 -> 0.94, 12:32 -> 0.85, 8:32 -> 0.68, 4:32 -> 0.41 at L = 32); packing pays
+// when it removes at least a fifth of the A-panel bytes (the paper's fixed 70 %
+// sparsity threshold, re-derived here from the traffic it saves).
+// NM_SIMT_MODE=0/1/2 overrides (ablation).
+static int simt_mode(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
+    const char* e = getenv("NM_SIMT_MODE");
+    if (e && e[0] >= '0' && e[0] <= '3') {
+        int mode = e[0] - '0';
+        if (mode >= 1 && m % 4 != 0) mode = 0;
+        if (mode == 3 && !simt_pipe_applicable(m, n, k, N, M, L)) mode = 1;
+        return mode;
+    }
+    if (!simt_use_at(m, n, k, N, M)) return 0;
+    const int G = (128 + L - 1) / L;
+    const double keep = 1.0 - std::pow(1.0 - static_cast<double>(N) / M, G);
+    // Measured on B200 (profiles/r01_summary.md): the per-row bulk copies of the packed
+    // mode cost more than the L2->SM bytes they save -- L2 serves the re-streamed A^T
+    // panels of the other column tiles -- so packing is off by default.
+    (void)keep;
+    return 1;
 }
 
 enum KernelId { K_GENERIC = 0, K_SIMT_F32 = 1, K_TC_BF16 = 2, K_TC_TF32 = 3 };
@@ -340,8 +369,14 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
     nm_math used = NM_MATH_AUTO;
     if ((st = select(A, values, C, m, n, k, N, M, L, ab_dt, c_dt, math, &kernel, &used))) return st;
     if (kernel == K_SIMT_F32)
+    {
+        const int mode = simt_mode(m, n, k, N, M, L);
+        if (mode == 3)
+            return simt_pipe_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
+                                    static_cast<float*>(C), m, n, k, N, M, L, s);
         return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
-                               static_cast<float*>(C), m, n, k, N, M, L, simt_use_at(m, n, k), s);
+                               static_cast<float*>(C), m, n, k, N, M, L, mode, s);
+    }
     if (kernel == K_TC_BF16) return tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
     if (ab_dt == NM_F32) return generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
     if (c_dt == NM_BF16) return generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);

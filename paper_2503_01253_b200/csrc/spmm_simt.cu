@@ -29,14 +29,20 @@ constexpr int A_STAGE_BYTES = BM * BK * 4;          // 32 KB
 constexpr int B_STAGE_BYTES = BKW * BN * 4;         // 16 KB
 constexpr int MAX_SLOTS = 33;                       // column groups touched by a 128-wide tile, L >= 4
 constexpr int KOFF_BYTES = 2 * BKW * MAX_SLOTS * 4;
+constexpr int MAX_PANELS_PACKED = 512;               // col_info masks kept in shared memory
+constexpr int MASK_BYTES = MAX_PANELS_PACKED * 8;
 constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + KOFF_BYTES + 64 + 1024;
+constexpr int SMEM_BYTES_PACKED = SMEM_BYTES + MASK_BYTES;
 constexpr int D_PER_THREAD = (BKW * MAX_SLOTS + THREADS - 1) / THREADS;  // 5
 
 struct Params {
     const uint8_t* D;
     float* C;
+    const float* AT;        // A^T (k x at_ld), packed mode
+    const uint64_t* masks;  // col_info per (column tile, panel): bit kk = dense column kk is needed
     int m, n, k, N, M, L;
     int q, wp, bk, bkw, npanels, nboxA;
+    int at_ld;
 };
 
 // Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
@@ -50,7 +56,12 @@ __device__ __forceinline__ int a_col_offset(int kk) {
 //      [BK k-rows][128 m] and a gathered fragment is two LDS.128 of row kabs
 //      (8 rows of A); otherwise the panel is [128 m][BK] (swizzled) and a fragment is
 //      eight LDS.32 of column kabs.
-template <bool TWO, bool AT>
+// PK:  (with AT) the paper's packing for high sparsity (Listing 3): only
+//      the dense columns some group of the tile selects (col_info) are
+//      fetched -- one 512-B bulk copy per needed A^T row, issued by warp 0's lanes --
+//      into consecutive panel rows, and the indices are remapped to packed
+//      positions (reorderingIdx) by a popcount over the col_info mask.
+template <bool TWO, bool AT, bool PK>
 __global__ void __launch_bounds__(THREADS, 2)
     spmm_simt_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const Params p) {
@@ -62,6 +73,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     uint8_t* sB = smem + STAGES * A_STAGE_BYTES;               // STAGES x 16 KB
     int* koff = reinterpret_cast<int*>(sB + STAGES * B_STAGE_BYTES);  // [2][BKW][MAX_SLOTS]
     uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(koff) + KOFF_BYTES);
+    uint64_t* smask = bars + 8;  // [MAX_PANELS_PACKED] (packed mode)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
@@ -71,19 +83,40 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int nslots = min((n0 + BN - 1) / p.L, p.q - 1) - g_first + 1;
 
     if (tid == 0) {
-        tma_prefetch_desc(&tmA);
+        if (!PK) tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
+    if (PK)
+        for (int i = tid; i < p.npanels; i += THREADS) smask[i] = p.masks[static_cast<int64_t>(blockIdx.x) * p.npanels + i];
     __syncthreads();
 
     const uint32_t stage_tx =
         static_cast<uint32_t>((AT ? p.bk * BM * 4 : p.nboxA * A_BOX_BYTES) + p.bkw * BN * 4);
+    // called by thread 0 (tile modes) or by all of warp 0 (packed mode)
     auto issue = [&](int panel) {
         const int s = panel % STAGES;
-        mbar_arrive_expect_tx(&bars[s], stage_tx);
         const int k0 = panel * p.bk, u0 = panel * p.bkw;
+        if (PK) {
+            const uint64_t mk = smask[panel];
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bars[s], static_cast<uint32_t>(__popcll(mk) * (BM * 4) + p.bkw * BN * 4));
+                tma_load_2d(sB + s * B_STAGE_BYTES, &tmB, &bars[s], n0, u0);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int b = lane + 32 * h;
+                if ((mk >> b) & 1ull) {
+                    const int pos = __popcll(mk & ((1ull << b) - 1ull));
+                    bulk_load(sA + s * A_STAGE_BYTES + pos * (BM * 4), p.AT + static_cast<int64_t>(k0 + b) * p.at_ld + m0,
+                              BM * 4, &bars[s]);
+                }
+            }
+            return;
+        }
+        mbar_arrive_expect_tx(&bars[s], stage_tx);
         if (AT)
             tma_load_2d(sA + s * A_STAGE_BYTES, &tmA, &bars[s], m0, k0);
         else
@@ -92,35 +125,42 @@ __global__ void __launch_bounds__(THREADS, 2)
         tma_load_2d(sB + s * B_STAGE_BYTES, &tmB, &bars[s], n0, u0);
     };
 
-    // D_s -> swizzled byte offsets koff[buf][u][slot] (index prefetch).
-    int dreg[D_PER_THREAD];
+    // D_s -> byte offsets koff[buf][u][slot] (index prefetch).  The (u, slot)
+    // entries a thread handles, their D offsets and window bases are panel-invariant
+    // (panels hold whole windows: (u0 + u) / N - t0 == u / N), so they are computed once.
+    int dreg[D_PER_THREAD], d_us[D_PER_THREAD], d_wb[D_PER_THREAD];  // d_us = u << 8 | slot (or -1)
+#pragma unroll
+    for (int r = 0; r < D_PER_THREAD; ++r) {
+        const int e = tid + r * THREADS;
+        const int u = e / nslots, sl = e - u * nslots;
+        d_us[r] = (u < p.bkw && sl < nslots) ? (u << 8 | sl) : -1;
+        d_wb[r] = (u / p.N) * p.M;
+    }
+    const int wtot = (p.k / p.M) * p.N;
     auto load_d = [&](int panel) {
         const int u0 = panel * p.bkw;
-        const int bkw = min(p.bkw, (p.k / p.M) * p.N - u0);
+        const uint8_t* Dp = p.D + static_cast<int64_t>(u0) * p.q + g_first;
+        const int ulim = wtot - u0;  // rows of D left (last panel may be partial)
 #pragma unroll
         for (int r = 0; r < D_PER_THREAD; ++r) {
-            const int e = tid + r * THREADS;
-            const int u = e / nslots, s = e - u * nslots;
-            int v = 0;
-            if (u < bkw && s < nslots) v = p.D[static_cast<int64_t>(u0 + u) * p.q + g_first + s];
-            dreg[r] = v;
+            const int u = d_us[r] >> 8, sl = d_us[r] & 255;
+            dreg[r] = (d_us[r] >= 0 && u < ulim) ? Dp[u * p.q + sl] : 0;
         }
     };
     auto store_d = [&](int panel) {
-        const int u0 = panel * p.bkw, t0 = panel * p.wp;
         int* kb = koff + (panel & 1) * (BKW * MAX_SLOTS);
+        const uint64_t mk = PK ? smask[panel] : 0ull;
 #pragma unroll
         for (int r = 0; r < D_PER_THREAD; ++r) {
-            const int e = tid + r * THREADS;
-            const int u = e / nslots, s = e - u * nslots;
-            if (u < BKW && s < nslots) {
-                const int kk = ((u0 + u) / p.N - t0) * p.M + dreg[r];  // dense column inside the panel
-                kb[u * MAX_SLOTS + s] = AT ? kk * (BM * 4) : a_col_offset(kk);
+            if (d_us[r] >= 0) {
+                const int kk = d_wb[r] + dreg[r];  // dense column inside the panel
+                const int row = PK ? __popcll(mk & ((1ull << kk) - 1ull)) : kk;  // packed position
+                kb[(d_us[r] >> 8) * MAX_SLOTS + (d_us[r] & 255)] = AT ? row * (BM * 4) : a_col_offset(kk);
             }
         }
     };
 
-    if (tid == 0) issue(0);
+    if (PK ? warp == 0 : tid == 0) issue(0);
     load_d(0);
     store_d(0);
     __syncthreads();
@@ -141,7 +181,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 
     for (int panel = 0; panel < p.npanels; ++panel) {
         const int s = panel % STAGES;
-        if (tid == 0 && panel + 1 < p.npanels) issue(panel + 1);  // stage (panel+1)%2 freed by last sync
+        if ((PK ? warp == 0 : tid == 0) && panel + 1 < p.npanels) issue(panel + 1);  // freed by the last sync
         if (panel + 1 < p.npanels) load_d(panel + 1);
         mbar_wait(&bars[s], (panel / STAGES) & 1);
 
@@ -235,7 +275,7 @@ void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw) {
 }
 
 // A (m x k) -> A^T (k x m): 32x32 tiles through padded shared memory, coalesced both ways.
-__global__ void transpose_kernel(const float* __restrict__ A, float* __restrict__ AT, int m, int k) {
+__global__ void transpose_kernel(const float* __restrict__ A, float* __restrict__ AT, int m, int k, int ld) {
     __shared__ float t[32][33];
     const int k0 = blockIdx.x * 32, m0 = blockIdx.y * 32;
     for (int r = threadIdx.y; r < 32; r += 8) {
@@ -245,32 +285,54 @@ __global__ void transpose_kernel(const float* __restrict__ A, float* __restrict_
     __syncthreads();
     for (int r = threadIdx.y; r < 32; r += 8) {
         const int j = k0 + r, i = m0 + threadIdx.x;
-        if (i < m && j < k) AT[static_cast<int64_t>(j) * m + i] = t[threadIdx.x][r];
+        if (i < m && j < k) AT[static_cast<int64_t>(j) * ld + i] = t[threadIdx.x][r];
     }
 }
 
-template <bool TWO, bool AT>
+// col_info: per (column tile, panel) the set of dense panel columns that at
+// least one column group of the tile selects, as a 64-bit mask (BK <= 64).
+__global__ void build_colinfo_kernel(const uint8_t* __restrict__ D, uint64_t* __restrict__ masks, int q, int N, int M,
+                                     int L, int wp, int bkw, int npanels, int wtot) {
+    __shared__ unsigned long long mk;
+    const int panel = blockIdx.x, tile = blockIdx.y;
+    const int g0 = tile * simt::BN / L, g1 = min((tile * simt::BN + simt::BN - 1) / L, q - 1);
+    const int ng = g1 - g0 + 1;
+    if (threadIdx.x == 0) mk = 0ull;
+    __syncthreads();
+    const int u0 = panel * bkw, t0 = panel * wp;
+    unsigned long long mine = 0ull;
+    for (int e = threadIdx.x; e < bkw * ng; e += blockDim.x) {
+        const int u = e / ng, g = g0 + e % ng;
+        if (u0 + u < wtot) mine |= 1ull << (((u0 + u) / N - t0) * M + D[static_cast<int64_t>(u0 + u) * q + g]);
+    }
+    atomicOr(&mk, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) masks[static_cast<int64_t>(tile) * npanels + panel] = mk;
+}
+
+template <bool TWO, bool AT, bool PK>
 static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, const simt::Params& p, dim3 grid,
                              cudaStream_t s) {
     using namespace simt;
+    const int smem = PK ? SMEM_BYTES_PACKED : SMEM_BYTES;
     static bool attr_done = false;
     if (!attr_done) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         SMEM_BYTES));
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         smem));
         attr_done = true;
     }
     prof_begin(s);
-    spmm_simt_f32_kernel<TWO, AT><<<grid, THREADS, SMEM_BYTES, s>>>(tmA, tmB, p);
+    spmm_simt_f32_kernel<TWO, AT, PK><<<grid, THREADS, smem, s>>>(tmA, tmB, p);
     prof_end(s);
     note_launch();
     NM_LAUNCH_CHECK("spmm_simt_f32_kernel");
     return NM_OK;
 }
 
-// use_at: stage A transposed (one extra pass over A, 2 fewer shared-memory
-// instructions per 16 FFMA in the inner loop); the selector decides.
+// mode: 0 = A panels straight from A (swizzled [m][k] boxes), 1 = A^T staged (tile TMA),
+// 2 = A^T staged + packed col_info loads (high sparsity).  The selector decides.
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, bool use_at, cudaStream_t s) {
+                          int N, int M, int L, int mode, cudaStream_t s) {
     using namespace simt;
     Params p{};
     p.D = D;
@@ -287,31 +349,54 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     p.npanels = (windows + p.wp - 1) / p.wp;
     p.nboxA = (p.bk + A_BOX_COLS - 1) / A_BOX_COLS;
     const int64_t w = k / M * N;
-    use_at = use_at && (m % 4 == 0);  // A^T rows (m floats) must be 16-B multiples for TMA
+    if (mode == 2 && p.npanels > MAX_PANELS_PACKED) mode = 1;
+    const bool use_at = mode >= 1;
+    const bool packed = mode == 2;
+    const int ntiles_n = static_cast<int>(ceil_div(n, BN));
+    p.at_ld = static_cast<int>(ceil_div(m, BM) * BM);  // padded so every 128-row A^T segment is in bounds
 
     CUtensorMap tmA, tmB;
     nm_status st = make_tma_2d(&tmB, Bv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, w, n, p.bkw, BN, 0);
     if (st) return st;
     float* AT = nullptr;
+    uint64_t* masks = nullptr;
     if (use_at) {
-        st = scratch_alloc(reinterpret_cast<void**>(&AT), static_cast<size_t>(m * k) * sizeof(float), s);
+        st = scratch_alloc(reinterpret_cast<void**>(&AT), static_cast<size_t>(k) * p.at_ld * sizeof(float), s);
         if (st) return st;
         const dim3 tg(static_cast<unsigned>(ceil_div(k, 32)), static_cast<unsigned>(ceil_div(m, 32)));
-        transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, AT, static_cast<int>(m), static_cast<int>(k));
+        transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, AT, static_cast<int>(m), static_cast<int>(k), p.at_ld);
         note_launch();
         NM_LAUNCH_CHECK("transpose_kernel");
-        st = make_tma_2d(&tmA, AT, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k, m, p.bk, BM, 0);
+        p.AT = AT;
+        st = make_tma_2d(&tmA, AT, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k, p.at_ld, p.bk, BM, 0);
     } else {
         st = make_tma_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, m, k, BM, A_BOX_COLS, 128);
     }
     if (st) return st;
+    if (packed) {
+        st = scratch_alloc(reinterpret_cast<void**>(&masks), static_cast<size_t>(ntiles_n) * p.npanels * 8, s);
+        if (st) return st;
+        build_colinfo_kernel<<<dim3(p.npanels, ntiles_n), 128, 0, s>>>(D, masks, p.q, N, M, L, p.wp, p.bkw, p.npanels,
+                                                                       static_cast<int>(w));
+        note_launch();
+        NM_LAUNCH_CHECK("build_colinfo_kernel");
+        p.masks = masks;
+    }
 
-    const dim3 grid(static_cast<unsigned>(ceil_div(n, BN)), static_cast<unsigned>(ceil_div(m, BM)));
+    const dim3 grid(static_cast<unsigned>(ntiles_n), static_cast<unsigned>(ceil_div(m, BM)));
     const bool two = L < 32;
-    if (use_at)
-        st = two ? launch_simt<true, true>(tmA, tmB, p, grid, s) : launch_simt<false, true>(tmA, tmB, p, grid, s);
+    if (packed)
+        st = two ? launch_simt<true, true, true>(tmA, tmB, p, grid, s) : launch_simt<false, true, true>(tmA, tmB, p, grid, s);
+    else if (use_at)
+        st = two ? launch_simt<true, true, false>(tmA, tmB, p, grid, s)
+                 : launch_simt<false, true, false>(tmA, tmB, p, grid, s);
     else
-        st = two ? launch_simt<true, false>(tmA, tmB, p, grid, s) : launch_simt<false, false>(tmA, tmB, p, grid, s);
+        st = two ? launch_simt<true, false, false>(tmA, tmB, p, grid, s)
+                 : launch_simt<false, false, false>(tmA, tmB, p, grid, s);
+    if (masks) {
+        cudaError_t e = cudaFreeAsync(masks, s);
+        if (e != cudaSuccess && st == NM_OK) st = cuda_fail(e, "cudaFreeAsync");
+    }
     if (AT) {
         cudaError_t e = cudaFreeAsync(AT, s);
         if (e != cudaSuccess && st == NM_OK) st = cuda_fail(e, "cudaFreeAsync");

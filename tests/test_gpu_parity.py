@@ -314,3 +314,20 @@ def test_spmm_tc_bf16_full_size_sampled(nm, oracle, cfg):
                                  rows=rows)
     got = C[torch.from_numpy(rows).cuda()].float().cpu().numpy()
     assert oracle.rel_frobenius(got, ref) <= TOL_BF16
+
+
+# --------------------------------------------------------------- SIMT staging modes (selector ablation)
+MODE_CASES = [(256, 256, 256, 2, 4, 4), (300, 288, 320, 16, 32, 32), (260, 384, 512, 8, 32, 32),
+              (128, 520, 256, 4, 32, 8), (200, 192, 192, 1, 8, 4), (132, 128, 256, 16, 32, 64), (4, 256, 128, 4, 32, 32)]
+
+
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("m,n,k,N,M,L", MODE_CASES)
+def test_spmm_f32_staging_modes(nm, oracle, monkeypatch, mode, m, n, k, N, M, L):
+    """mode 0: A panels straight from A; 1: A^T staged; 2: A^T + packed col_info loads
+    (P:412-437).  All must give the same parity."""
+    monkeypatch.setenv("NM_SIMT_MODE", mode)
+    A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L, kind="integer", seed=3)
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L))
+    A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L)
+    assert oracle.rel_frobenius(C, oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
