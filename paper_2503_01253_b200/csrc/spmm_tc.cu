@@ -26,6 +26,8 @@
 // (P:546).  Everything else is B200-specific.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace nm {
@@ -37,7 +39,10 @@ constexpr int LOADER_THREADS = LOADER_WARPS * 32, GATHER_THREADS = GATHER_WARPS 
 constexpr int CONTROL_WARP = LOADER_WARPS + GATHER_WARPS;
 constexpr int THREADS = (CONTROL_WARP + 1) * 32;  // 544
 constexpr int B_STAGES = 3;
-constexpr int NAB = 3;        // TMEM A buffers: gathers run up to two panels ahead of the MMA
+// TMEM A buffers (gathers run up to NAB-1 panels ahead of the MMA) and B' panel rows:
+// BN = 128 -> 3 buffers, BKW <= 64; BN = 256 -> 2 buffers, BKW <= 32 (512 TMEM columns).
+template <int BN> constexpr int nab() { return BN == 256 ? 2 : 3; }
+template <int BN> constexpr int bkw_cap() { return BN == 256 ? 32 : 64; }
 constexpr int BK_MAX = 128;   // dense k per panel
 constexpr int BKW_MAX = 64;   // compressed rows per panel (padded to a multiple of 16)
 constexpr int CELLS_MAX = 256;  // (group, u-pair) cells per panel: G * bkw_pad / 2 <= (512 - BN) / 2
@@ -51,13 +56,13 @@ constexpr int STG_BYTES = STG_A_BYTES + TBL_BYTES;             // + the panel's 
 
 template <int BN>
 struct Smem {
-    static constexpr int B_STAGE_BYTES = BKW_MAX * BN * 2;
+    static constexpr int B_STAGE_BYTES = bkw_cap<BN>() * BN * 2;
     static constexpr int B = 0;                               // B_STAGES B' panels (1024-aligned)
     static constexpr int A = B + B_STAGES * B_STAGE_BYTES;    // 2 padded A panels
     static constexpr int STG = A + 2 * A_STAGE_BYTES;         // A_STAGES dense TMA panels (1024-aligned)
     static constexpr int T = STG + A_STAGES * STG_BYTES;      // 2 cell tables
     static constexpr int BAR = T + 2 * TBL_BYTES;             // mbarriers
-    static constexpr int NBAR = 2 * B_STAGES + 2 * A_STAGES + 2 * 2 + 2 * NAB + 1;
+    static constexpr int NBAR = 2 * B_STAGES + 2 * A_STAGES + 2 * 2 + 2 * nab<BN>() + 1;
     static constexpr int TMEM_SLOT = BAR + NBAR * 8;
     static constexpr int END = TMEM_SLOT + 16;
     static constexpr int BYTES = END + 1024;
@@ -97,9 +102,10 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
         : "memory");
 }
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+    // no "memory" clobber: shared-memory loads of the next cells may be hoisted above the
+    // store; ordering against the MMA is wait::st + fence::before_thread_sync + mbarrier
     asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
-                 : "memory");
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
 }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
@@ -143,6 +149,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     spmm_tc_bf16_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                         const Params p) {
     using S = Smem<BN>;
+    constexpr int NAB = nab<BN>();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sB = smem + S::B;
@@ -456,7 +463,15 @@ __global__ void build_cell_table_kernel(const uint8_t* __restrict__ D, uint32_t*
 
 }  // namespace tc
 
-static int tc_bn(int L) { return L <= 32 ? 128 : 128; }
+// Column-tile width: at high sparsity a 128-wide tile re-streams its dense A panel for
+// little MMA work per panel, so 256 columns (8 groups) share each A panel; at <= 4:1
+// density ratio the 128-wide tile wins (more CTAs, 3 TMEM A buffers).  Measured on B200
+// (profiles/r01_summary.md): 16:32 128 > 256; 8:32 and 4:32 256 > 128.
+static int tc_bn(int N, int M, int L) {
+    const char* e = getenv("NM_TC_BN");  // ablation override
+    if (e && (atoi(e) == 128 || atoi(e) == 256) && 256 % L == 0 && (atoi(e) / L) * 16 <= tc::CELLS_MAX) return atoi(e);
+    return (L == 32 && 4 * N <= M) ? 256 : 128;
+}
 
 bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                         int L) {
@@ -473,9 +488,11 @@ bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m,
 // BKW = WP*N compressed rows with G * BKW_pad <= 512 - BN TMEM columns for the two A
 // buffers, preferring BKW % 16 == 0 (no zero-padded MMA k-steps), then larger panels.
 void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn) {
-    const int BN = tc_bn(L), G = BN / L;
-    int cap = 2 * (512 - BN) / (tc::NAB * G);
-    cap = cap < tc::BKW_MAX ? cap : tc::BKW_MAX;
+    const int BN = tc_bn(N, M, L), G = BN / L;
+    const int nab = BN == 256 ? tc::nab<256>() : tc::nab<128>();
+    const int bcap = BN == 256 ? tc::bkw_cap<256>() : tc::bkw_cap<128>();
+    int cap = 2 * (512 - BN) / (nab * G);
+    cap = cap < bcap ? cap : bcap;
     cap = cap / 16 * 16;
     if (G * (cap / 2) > tc::CELLS_MAX) cap = 2 * (tc::CELLS_MAX / G) / 16 * 16;
     int best = 1, best_score = -1;
