@@ -17,6 +17,8 @@
 // tile 8 rows x 8 columns (two 4-column chunks 16 apart).  A panel: WP whole
 // windows (BK = WP*M <= 64 dense k, never straddling a window), i.e.
 // BKW = WP*N <= 32 compressed rows.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace nm {
@@ -43,6 +45,13 @@ struct Params {
     int m, n, k, N, M, L;
     int q, wp, bk, bkw, npanels, nboxA;
     int at_ld;
+    // tile schedule (1-D grid, n fastest so column tiles sharing an A panel run together);
+    // the last, partial wave is split along k ("stream-K lite"): tiles >= full_tiles are
+    // done by `split` CTAs each, whose partial sums meet in ws and are added in a fixed
+    // order by whichever CTA finishes last (deterministic, no atomics on data).
+    int ntn, full_tiles, split;
+    float* ws;
+    int* counters;
 };
 
 // Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
@@ -78,7 +87,14 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp & 1, wn = warp >> 1;
     const int t_m = lane & 7, t_n = lane >> 3;
-    const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+    int tile = blockIdx.x, part = 0, nparts = 1;
+    if (tile >= p.full_tiles) {
+        part = (tile - p.full_tiles) % p.split;
+        tile = p.full_tiles + (tile - p.full_tiles) / p.split;
+        nparts = p.split;
+    }
+    const int m0 = (tile / p.ntn) * BM, n0 = (tile % p.ntn) * BN;
+    const int p_begin = part * p.npanels / nparts, p_end = (part + 1) * p.npanels / nparts;
     const int g_first = n0 / p.L;
     const int nslots = min((n0 + BN - 1) / p.L, p.q - 1) - g_first + 1;
 
@@ -89,14 +105,14 @@ __global__ void __launch_bounds__(THREADS, 2)
         fence_mbar_init();
     }
     if (PK)
-        for (int i = tid; i < p.npanels; i += THREADS) smask[i] = p.masks[static_cast<int64_t>(blockIdx.x) * p.npanels + i];
+        for (int i = tid; i < p.npanels; i += THREADS) smask[i] = p.masks[static_cast<int64_t>(tile % p.ntn) * p.npanels + i];
     __syncthreads();
 
     const uint32_t stage_tx =
         static_cast<uint32_t>((AT ? p.bk * BM * 4 : p.nboxA * A_BOX_BYTES) + p.bkw * BN * 4);
     // called by thread 0 (tile modes) or by all of warp 0 (packed mode)
     auto issue = [&](int panel) {
-        const int s = panel % STAGES;
+        const int s = (panel - p_begin) % STAGES;
         const int k0 = panel * p.bk, u0 = panel * p.bkw;
         if (PK) {
             const uint64_t mk = smask[panel];
@@ -148,7 +164,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
     };
     auto store_d = [&](int panel) {
-        int* kb = koff + (panel & 1) * (BKW * MAX_SLOTS);
+        int* kb = koff + ((panel - p_begin) & 1) * (BKW * MAX_SLOTS);
         const uint64_t mk = PK ? smask[panel] : 0ull;
 #pragma unroll
         for (int r = 0; r < D_PER_THREAD; ++r) {
@@ -160,9 +176,9 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
     };
 
-    if (PK ? warp == 0 : tid == 0) issue(0);
-    load_d(0);
-    store_d(0);
+    if (PK ? warp == 0 : tid == 0) issue(p_begin);
+    load_d(p_begin);
+    store_d(p_begin);
     __syncthreads();
 
     // thread geometry
@@ -179,17 +195,17 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
 
-    for (int panel = 0; panel < p.npanels; ++panel) {
-        const int s = panel % STAGES;
-        if ((PK ? warp == 0 : tid == 0) && panel + 1 < p.npanels) issue(panel + 1);  // freed by the last sync
-        if (panel + 1 < p.npanels) load_d(panel + 1);
-        mbar_wait(&bars[s], (panel / STAGES) & 1);
+    for (int panel = p_begin; panel < p_end; ++panel) {
+        const int rel = panel - p_begin, s = rel % STAGES;
+        if ((PK ? warp == 0 : tid == 0) && panel + 1 < p_end) issue(panel + 1);  // freed by the last sync
+        if (panel + 1 < p_end) load_d(panel + 1);
+        mbar_wait(&bars[s], (rel / STAGES) & 1);
 
         const int u0 = panel * p.bkw;
         const int bkw = min(p.bkw, (p.k / p.M) * p.N - u0);
         const uint8_t* aS = sA + s * A_STAGE_BYTES + a_row;
         const float* bS = reinterpret_cast<const float*>(sB + s * B_STAGE_BYTES) + col0;
-        const int* kS = koff + (panel & 1) * (BKW * MAX_SLOTS);
+        const int* kS = koff + (rel & 1) * (BKW * MAX_SLOTS);
 
         float a0[8], a1[8];
         float4 b0, b1;
@@ -235,8 +251,42 @@ __global__ void __launch_bounds__(THREADS, 2)
                 acc[i][7] = fmaf(a1[i], b1.w, acc[i][7]);
             }
         }
-        if (panel + 1 < p.npanels) store_d(panel + 1);
+        if (panel + 1 < p_end) store_d(panel + 1);
         __syncthreads();
+    }
+
+    if (nparts > 1) {
+        // split tile: publish this part's partial sums, the last part to arrive adds all
+        // parts in order 0..split-1 (fixed order -> bit-reproducible) and stores C
+        const int ti = tile - p.full_tiles;
+        float4* mine = reinterpret_cast<float4*>(p.ws + (static_cast<int64_t>(ti) * p.split + part) * (BM * BN)) + tid * 16;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            mine[2 * i] = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+            mine[2 * i + 1] = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+        }
+        __threadfence();
+        __syncthreads();
+        int* last = reinterpret_cast<int*>(bars + 2);
+        if (tid == 0) *last = atomicAdd(&p.counters[ti], 1) == p.split - 1;
+        __syncthreads();
+        if (!*last) return;
+        __threadfence();
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+        for (int q2 = 0; q2 < p.split; ++q2) {
+            const float4* src =
+                reinterpret_cast<const float4*>(p.ws + (static_cast<int64_t>(ti) * p.split + q2) * (BM * BN)) + tid * 16;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float4 x = __ldcg(src + 2 * i), y = __ldcg(src + 2 * i + 1);
+                acc[i][0] += x.x, acc[i][1] += x.y, acc[i][2] += x.z, acc[i][3] += x.w;
+                acc[i][4] += y.x, acc[i][5] += y.y, acc[i][6] += y.z, acc[i][7] += y.w;
+            }
+        }
+        if (tid == 0) p.counters[ti] = 0;  // ready for the next launch
     }
 
     // epilogue: registers -> global (float4 stores, guarded for ragged m / n)
@@ -383,7 +433,33 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
         p.masks = masks;
     }
 
-    const dim3 grid(static_cast<unsigned>(ntiles_n), static_cast<unsigned>(ceil_div(m, BM)));
+    // schedule: full waves of whole tiles, the partial last wave split along k
+    p.ntn = ntiles_n;
+    const int ntiles = ntiles_n * static_cast<int>(ceil_div(m, BM));
+    const int resident = 2 * num_sms();  // 2 CTAs per SM (launch bounds, ~105 KB smem)
+    const int rem = ntiles % resident;
+    // Measured on B200 (cfg2-cfg4): splitting the partial wave gains nothing -- CTAs do
+    // not retire in lock-step waves -- so it is off unless NM_SIMT_SPLIT asks for it.
+    int split = 1;
+    const char* env_split = getenv("NM_SIMT_SPLIT");
+    if (env_split) split = atoi(env_split);
+    split = split > 4 ? 4 : split;
+    if (split > p.npanels / 2) split = p.npanels / 2;
+    (void)rem;
+    if (split < 2 || ntiles < resident) split = 1;
+    p.split = split;
+    p.full_tiles = split > 1 ? ntiles - rem : ntiles;
+    float* ws = nullptr;
+    int* counters = nullptr;
+    if (split > 1) {
+        st = scratch_alloc(reinterpret_cast<void**>(&ws), static_cast<size_t>(rem) * split * BM * BN * sizeof(float), s);
+        if (!st) st = scratch_alloc(reinterpret_cast<void**>(&counters), static_cast<size_t>(rem) * sizeof(int), s);
+        if (st) return st;
+        NM_CUDA_TRY(cudaMemsetAsync(counters, 0, static_cast<size_t>(rem) * sizeof(int), s));
+        p.ws = ws;
+        p.counters = counters;
+    }
+    const dim3 grid(static_cast<unsigned>(p.full_tiles + (ntiles - p.full_tiles) * split));
     const bool two = L < 32;
     if (packed)
         st = two ? launch_simt<true, true, true>(tmA, tmB, p, grid, s) : launch_simt<false, true, true>(tmA, tmB, p, grid, s);
@@ -393,6 +469,10 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     else
         st = two ? launch_simt<true, false, false>(tmA, tmB, p, grid, s)
                  : launch_simt<false, false, false>(tmA, tmB, p, grid, s);
+    if (ws) {
+        cudaError_t e1 = cudaFreeAsync(ws, s), e2 = cudaFreeAsync(counters, s);
+        if (st == NM_OK && (e1 != cudaSuccess || e2 != cudaSuccess)) st = cuda_fail(e1 != cudaSuccess ? e1 : e2, "cudaFreeAsync");
+    }
     if (masks) {
         cudaError_t e = cudaFreeAsync(masks, s);
         if (e != cudaSuccess && st == NM_OK) st = cuda_fail(e, "cudaFreeAsync");

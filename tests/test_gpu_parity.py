@@ -331,3 +331,21 @@ def test_spmm_f32_staging_modes(nm, oracle, monkeypatch, mode, m, n, k, N, M, L)
     assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L))
     A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L)
     assert oracle.rel_frobenius(C, oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
+
+
+@pytest.mark.parametrize("split", ["1", "2", "3", "4"])
+def test_spmm_f32_split_tail(nm, oracle, monkeypatch, split):
+    """Stream-K-lite tail split: every split factor gives the same parity, and results
+    are bit-reproducible run to run (fixed reduction order)."""
+    monkeypatch.setenv("NM_SIMT_SPLIT", split)
+    m, n, k, N, M, L = 4096, 1280, 1024, 16, 32, 32  # 320 tiles > 296 resident -> a partial wave
+    A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L, kind="integer", seed=5)
+    rows = np.arange(0, m, 97)
+    ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L, rows=rows)
+    assert np.array_equal(C[rows].astype(np.float64), ref)
+    A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L, seed=6)
+    ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L, rows=rows)
+    assert oracle.rel_frobenius(C[rows], ref) <= TOL_F32
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    Ad = dev(A)
+    assert torch.equal(nm.nm_spmm(Ad, W), nm.nm_spmm(Ad, W))
