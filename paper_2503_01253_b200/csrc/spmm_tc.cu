@@ -48,7 +48,8 @@ constexpr int BKW_MAX = 64;   // compressed rows per panel (padded to a multiple
 constexpr int CELLS_MAX = 256;  // (group, u-pair) cells per panel: G * bkw_pad / 2 <= (512 - BN) / 2
 constexpr int A_PITCH_MAX = BK_MAX * 2 + 4;
 constexpr int A_STAGE_BYTES = (BM * A_PITCH_MAX + 1023) / 1024 * 1024;  // 33,792 (keeps the next region aligned)
-constexpr int TBL_BYTES = 3 * CELLS_MAX * 4;     // offA[], offB[], sel[] (uint32)
+constexpr int TBL_WORDS = 2 * CELLS_MAX;         // [sel | offA << 16][offB] per cell (uint32)
+constexpr int TBL_BYTES = TBL_WORDS * 4;
 constexpr int LD_UNITS = BM * BK_MAX / 8 / LOADER_THREADS;  // 16-byte units per loader thread: 16
 constexpr int A_STAGES = 2;                                    // TMA staging ring for the dense A panel
 constexpr int STG_A_BYTES = BM * BK_MAX * 2;                   // 32 KB dense A panel
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                (static_cast<uint32_t>(L >> 3) << 17) | (static_cast<uint32_t>(BM >> 4) << 24);
         const uint32_t stage_tx = static_cast<uint32_t>(G * atoms * bkw * rb);
         const uint32_t a_tx = static_cast<uint32_t>(BM * bk * 2 + TBL_BYTES);
-        const uint32_t* tsrc = p.tbl + static_cast<int64_t>(blockIdx.x) * p.npanels * (3 * CELLS_MAX);
+        const uint32_t* tsrc = p.tbl + static_cast<int64_t>(blockIdx.x) * p.npanels * TBL_WORDS;
         const uint64_t gstep = static_cast<uint64_t>(gbytes >> 4), kstep = static_cast<uint64_t>((16 * rb) >> 4);
         const int nk = bkwp / 16;
         auto issue_b = [&](int panel) {
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int s = panel % A_STAGES;
                 mbar_arrive_expect_tx(&g_full[s], a_tx);
                 tma_load_2d(sStg + s * STG_BYTES, &tmA, &g_full[s], panel * bk, m0);
-                bulk_load(sStg + s * STG_BYTES + STG_A_BYTES, tsrc + static_cast<int64_t>(panel) * (3 * CELLS_MAX),
+                bulk_load(sStg + s * STG_BYTES + STG_A_BYTES, tsrc + static_cast<int64_t>(panel) * TBL_WORDS,
                           TBL_BYTES, &g_full[s]);
             }
         };
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             // prepacked cell table of the panel -> the gather-side table buffer
             const uint4* ts = reinterpret_cast<const uint4*>(src + STG_A_BYTES);
-            uint4* td = reinterpret_cast<uint4*>(sT + st * (3 * CELLS_MAX));
+            uint4* td = reinterpret_cast<uint4*>(sT + st * TBL_WORDS);
             for (int i = tid; i < TBL_BYTES / 16; i += LOADER_THREADS) td[i] = ts[i];
             mbar_arrive(&g_free[gs]);
             // the pad word of each row is the zero source for the k padding (sentinel column bk)
@@ -360,27 +361,26 @@ __global__ void __launch_bounds__(THREADS, 1)
                 tc_fence_after();
             }
             const uint8_t* arow = sA + st * A_STAGE_BYTES + row * a_pitch;
-            const uint32_t* tA = sT + st * (3 * CELLS_MAX);
+            const uint32_t* tA = sT + st * TBL_WORDS;
             const uint32_t* tB = tA + CELLS_MAX;
-            const uint32_t* tS = tA + 2 * CELLS_MAX;
             const uint32_t tm_a = tmem + lane_addr + BN + ab * a_cols;
             // items = blocks of 8 cells, cell index == TMEM column offset inside the buffer;
             // this warp takes blocks sub, sub+3, ... (cells of group g are [g*cells_g, +cells_g))
             const int ncells = G * cells_g;
             for (int cell0 = sub * 8; cell0 < ncells; cell0 += 24) {
-                uint32_t oa[8], ob[8], sl[8];
-                *reinterpret_cast<uint4*>(&oa[0]) = *reinterpret_cast<const uint4*>(tA + cell0);
-                *reinterpret_cast<uint4*>(&oa[4]) = *reinterpret_cast<const uint4*>(tA + cell0 + 4);
+                // word 1 = PRMT selector | offset of kabs(2c)'s word << 16 (PRMT reads only the
+                // low 16 selector bits), word 2 = offset of kabs(2c+1)'s word: 4 LDS.128 / 8 cells
+                uint32_t sa[8], ob[8];
+                *reinterpret_cast<uint4*>(&sa[0]) = *reinterpret_cast<const uint4*>(tA + cell0);
+                *reinterpret_cast<uint4*>(&sa[4]) = *reinterpret_cast<const uint4*>(tA + cell0 + 4);
                 *reinterpret_cast<uint4*>(&ob[0]) = *reinterpret_cast<const uint4*>(tB + cell0);
                 *reinterpret_cast<uint4*>(&ob[4]) = *reinterpret_cast<const uint4*>(tB + cell0 + 4);
-                *reinterpret_cast<uint4*>(&sl[0]) = *reinterpret_cast<const uint4*>(tS + cell0);
-                *reinterpret_cast<uint4*>(&sl[4]) = *reinterpret_cast<const uint4*>(tS + cell0 + 4);
                 uint32_t v[8];
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    const uint32_t wa = *reinterpret_cast<const uint32_t*>(arow + oa[c]);
+                    const uint32_t wa = *reinterpret_cast<const uint32_t*>(arow + (sa[c] >> 16));
                     const uint32_t wb = *reinterpret_cast<const uint32_t*>(arow + ob[c]);
-                    v[c] = prmt(wa, wb, sl[c]);
+                    v[c] = prmt(wa, wb, sa[c]);
                 }
                 tmem_st8(tm_a + cell0, v);
             }
@@ -441,7 +441,7 @@ __global__ void build_cell_table_kernel(const uint8_t* __restrict__ D, uint32_t*
                                         int M, int L, int BN, int bk, int bkw, int bkw_pad, int npanels, int wtot) {
     const int tile = blockIdx.y, panel = blockIdx.x;
     const int G = BN / L, cells_g = bkw_pad / 2;
-    uint32_t* t = tbl + (static_cast<int64_t>(tile) * npanels + panel) * (3 * CELLS_MAX);
+    uint32_t* t = tbl + (static_cast<int64_t>(tile) * npanels + panel) * TBL_WORDS;
     const int u0 = panel * bkw;
     for (int e = threadIdx.x; e < CELLS_MAX; e += blockDim.x) {
         const int g = e / cells_g, c = e - g * cells_g;
@@ -455,9 +455,9 @@ __global__ void build_cell_table_kernel(const uint8_t* __restrict__ D, uint32_t*
                     k2[h] = static_cast<uint32_t>((u / N) * M + D[static_cast<int64_t>(u0 + u) * q + gg]);
             }
         }
-        t[e] = (k2[0] >> 1) << 2;
+        const uint32_t sel = ((k2[0] & 1u) ? 0x32u : 0x10u) | ((k2[1] & 1u) ? 0x7600u : 0x5400u);
+        t[e] = sel | (((k2[0] >> 1) << 2) << 16);
         t[CELLS_MAX + e] = (k2[1] >> 1) << 2;
-        t[2 * CELLS_MAX + e] = ((k2[0] & 1u) ? 0x32u : 0x10u) | ((k2[1] & 1u) ? 0x7600u : 0x5400u);
     }
 }
 
