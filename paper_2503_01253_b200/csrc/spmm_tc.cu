@@ -28,7 +28,7 @@
 
 #include <cstdlib>
 
-#include "common.cuh"
+#include "tcgen05.cuh"
 
 namespace nm {
 namespace tc {
@@ -77,72 +77,6 @@ struct Params {
     int q, wp, bk, bkw, bkw_pad, npanels;
     int c_bf16;
 };
-
-// ------------------------------------------------------------------ PTX
-__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "r"(ncols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
-}
-// D[tmem] (+)= A[tmem] . B[smem]  (kind::f16, bf16 inputs, fp32 accumulate)
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-        "r"(a), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
-    // no "memory" clobber: shared-memory loads of the next cells may be hoisted above the
-    // store; ordering against the MMA is wait::st + fence::before_thread_sync + mbarrier
-    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(v[0]),
-                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
-}
-__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr)
-        : "memory");
-}
-__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ bool elect_one() {
-    uint32_t pred;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "elect.sync _|p, 0xffffffff;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(pred));
-    return pred != 0;
-}
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-    uint32_t d;
-    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-    return d;
-}
-
-// UMMA shared-memory descriptor (SM100 version 1): start, LBO, SBO (>>4), layout type.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
-    uint64_t d = 0;
-    d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
-    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
-    d |= static_cast<uint64_t>(1) << 46;  // version
-    d |= static_cast<uint64_t>(layout & 7) << 61;
-    return d;
-}
 
 // ------------------------------------------------------------------ kernel
 template <int BN>
@@ -511,6 +445,10 @@ void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_
     *bn = BN;
 }
 
+bool tc_pair_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L, int bn, int bkw_pad);
+nm_status tc_pair_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
+                         int64_t k, int N, int M, int L, int wp, int bk, int bkw, int bkwp, int bn, cudaStream_t s);
+
 template <int BN>
 static nm_status tc_launch_bn(const tc::Params& p, const CUtensorMap& tmA, const CUtensorMap& tmB, int64_t m, int64_t n,
                               cudaStream_t s) {
@@ -546,6 +484,10 @@ nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* 
     p.c_bf16 = c_bf16 ? 1 : 0;
     int bn = 128;
     tc_bf16_geometry(N, M, L, &p.wp, &p.bk, &p.bkw, &p.bkw_pad, &bn);
+    // token-pair gather (spmm_tc_pair.cu) when its layout constraints hold; NM_TC_PAIR=0 disables
+    const char* pe = getenv("NM_TC_PAIR");
+    if (!(pe && pe[0] == '0') && tc_pair_applicable(m, n, k, N, M, L, bn, p.bkw_pad))
+        return tc_pair_launch(A, Bv, D, C, c_bf16, m, n, k, N, M, L, p.wp, p.bk, p.bkw, p.bkw_pad, bn, s);
     const int windows = static_cast<int>(k / M);
     p.npanels = (windows + p.wp - 1) / p.wp;
     const int64_t w = k / M * N;
