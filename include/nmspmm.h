@@ -168,6 +168,38 @@ nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, i
                              int elem_bytes, void* stream);
 
 /*
+ * Weight prepack -- the paper's offline PreProcessing step (Listing 3, P:470-475:
+ * queryColInfo / reoderingIdx / transformLayout), done once per weight.  For the
+ * tcgen05 token-pair path it computes, from B' and D alone: a per-(panel, column
+ * group) order of the compressed rows that keeps the gather's shared-memory loads
+ * conflict-free, the correspondingly reordered B' and the gather's cell tables.
+ * Other paths keep using `values` / `idx` directly (kind 0).
+ *   nm_prepack_bytes : device bytes needed in `buf` (0 for kind 0; -1 on bad args).
+ *   nm_prepack       : fills `buf` (device, caller-owned) and the host descriptor
+ *                      `*out`; `values` and `idx` must stay alive and unmodified
+ *                      while `*out` is used.  Asynchronous on `stream`.
+ *   nm_spmm_prepacked: C (m x n, c_dt) = A (m x k) . decompress(values, idx), same
+ *                      semantics and parity as nm_spmm.  Asynchronous.
+ */
+typedef struct {
+    int32_t magic;   /* 0x4B504D4E ("NMPK") once filled */
+    int32_t kind;    /* 0 = plain (values/idx used directly), 1 = tcgen05 token-pair prepack */
+    int32_t dtype, N, M, L;
+    int64_t n, k;
+    int32_t bn, wp, bk, bkw, bkw_pad, npanels;
+    const void* values;
+    const uint8_t* idx;
+    void* perm;      /* inside buf (kind 1) */
+    void* tbl;
+    void* bperm;
+} nm_prepacked;
+
+int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt);
+nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                     void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
+nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt, void* stream);
+
+/*
  * nm_profile_begin / nm_profile_end -- launch accounting for measurement
  * (bench.py).  Between the two calls the library counts every kernel it
  * launches and records a CUDA event pair on the launching stream around each

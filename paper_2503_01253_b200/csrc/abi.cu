@@ -472,6 +472,102 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
     return NM_OK;
 }
 
+// ------------------------------------------------------------------ prepack
+}  // extern "C"
+namespace nm {
+void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn);
+bool tc_pair_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L, int bn, int bkw_pad);
+void tc_pair_sizes(int64_t n, int64_t k, int N, int M, int L, int wp, int bkwp, int bn, size_t* perm_bytes,
+                   size_t* tbl_bytes, size_t* bp_bytes);
+nm_status tc_pair_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, int wp, int bk,
+                          int bkw, int bkwp, int bn, uint8_t* perm, uint32_t* tbl, void* bp, cudaStream_t s);
+nm_status tc_pair_run(const void* A, const uint32_t* tbl, const void* bp, void* C, bool c_bf16, int64_t m, int64_t n,
+                      int64_t k, int N, int M, int L, int wp, int bk, int bkw, int bkwp, int bn, cudaStream_t s);
+
+static const int32_t kPrepackMagic = 0x4B504D4E;
+static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+
+// kind 1 iff the bf16 tcgen05 token-pair kernel would run for this weight
+static bool prepack_kind1(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, int* g) {
+    if (dt != NM_BF16) return false;
+    static const float dummy[4] = {0, 0, 0, 0};
+    if (!tc_bf16_applicable(dummy, dummy, dummy, 1, n, k, N, M, L)) return false;
+    const char* pe = getenv("NM_TC_PAIR");
+    if (pe && pe[0] == '0') return false;
+    tc_bf16_geometry(N, M, L, &g[0], &g[1], &g[2], &g[3], &g[4]);
+    return tc_pair_applicable(1, n, k, N, M, L, g[4], g[3]);
+}
+}  // namespace nm
+extern "C" {
+
+int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
+    if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16) return -1;
+    int g[5];
+    if (!prepack_kind1(n, k, N, M, L, dt, g)) return 0;
+    size_t pb, tb, bb;
+    tc_pair_sizes(n, k, N, M, L, g[0], g[3], g[4], &pb, &tb, &bb);
+    return static_cast<int64_t>(al256(pb) + al256(tb) + al256(bb));
+}
+
+nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                     void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream) {
+    nm_status st = check_common(0, n, k, N, M, L);
+    if (st) return st;
+    if (!out || (n * k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_prepack: NULL pointer");
+    if (dt > NM_BF16) return fail(NM_ERR_UNSUPPORTED, "dtype");
+    *out = nm_prepacked{};
+    out->dtype = dt;
+    out->N = N;
+    out->M = M;
+    out->L = L;
+    out->n = n;
+    out->k = k;
+    out->values = values;
+    out->idx = idx;
+    int g[5];
+    if (prepack_kind1(n, k, N, M, L, dt, g)) {
+        const int64_t need = nm_prepack_bytes(n, k, N, M, L, dt);
+        if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
+        if ((st = require_device())) return st;
+        size_t pb, tb, bb;
+        tc_pair_sizes(n, k, N, M, L, g[0], g[3], g[4], &pb, &tb, &bb);
+        uint8_t* base = static_cast<uint8_t*>(buf);
+        out->perm = base;
+        out->tbl = base + al256(pb);
+        out->bperm = base + al256(pb) + al256(tb);
+        out->wp = g[0];
+        out->bk = g[1];
+        out->bkw = g[2];
+        out->bkw_pad = g[3];
+        out->bn = g[4];
+        out->npanels = static_cast<int32_t>((k / M + g[0] - 1) / g[0]);
+        out->kind = 1;
+        st = tc_pair_prepack(values, idx, n, k, N, M, L, g[0], g[1], g[2], g[3], g[4], static_cast<uint8_t*>(out->perm),
+                             static_cast<uint32_t*>(out->tbl), out->bperm, static_cast<cudaStream_t>(stream));
+        if (st) return st;
+    }
+    out->magic = kPrepackMagic;
+    return NM_OK;
+}
+
+nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt, void* stream) {
+    if (!w || w->magic != kPrepackMagic) return fail(NM_ERR_NULL, "nm_spmm_prepacked: descriptor not filled by nm_prepack");
+    if (w->kind == 1) {
+        nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
+        if (st) return st;
+        if (m == 0 || w->n == 0) return NM_OK;
+        if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
+        if ((st = require_device())) return st;
+        // the token-pair kernel needs 16-B aligned A / C; otherwise fall through to the plain path
+        if (((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(C)) & 15) == 0 && w->k > 0)
+            return tc_pair_run(A, static_cast<const uint32_t*>(w->tbl), w->bperm, C, c_dt == NM_BF16, m, w->n, w->k,
+                               w->N, w->M, w->L, w->wp, w->bk, w->bkw, w->bkw_pad, w->bn,
+                               static_cast<cudaStream_t>(stream));
+    }
+    return nm_spmm(A, w->values, w->idx, C, m, w->n, w->k, w->N, w->M, w->L, static_cast<nm_dtype>(w->dtype), c_dt,
+                   NM_MATH_AUTO, stream);
+}
+
 nm_status nm_profile_begin(void) {
     std::lock_guard<std::mutex> lk(g_prof_mu);
     g_prof.on = true;

@@ -434,9 +434,42 @@ static nm_status pair_launch_bn(const tcp::Params& p, const CUtensorMap& tmA, co
     return NM_OK;
 }
 
-// geometry comes from tc_bf16_geometry (spmm_tc.cu) so both variants tile identically
-nm_status tc_pair_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                         int64_t k, int N, int M, int L, int wp, int bk, int bkw, int bkwp, int bn, cudaStream_t s) {
+// Sizes of the weight-side prepack (everything derived from B' and D alone).
+void tc_pair_sizes(int64_t n, int64_t k, int N, int M, int L, int wp, int bkwp, int bn, size_t* perm_bytes,
+                   size_t* tbl_bytes, size_t* bp_bytes) {
+    const int64_t npanels = (k / M + wp - 1) / wp, q = n / L, ntiles = ceil_div(n, bn);
+    *perm_bytes = static_cast<size_t>(npanels * q * 64);
+    *tbl_bytes = static_cast<size_t>(ntiles * npanels) * tcp::TBL_BYTES;
+    *bp_bytes = static_cast<size_t>(npanels * bkwp * n) * sizeof(__nv_bfloat16);
+}
+
+// The paper's offline PreProcessing (Listing 3) for the token-pair path:
+// per-group k order (perm), cell tables (tbl) and the reordered B' (bp).
+nm_status tc_pair_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, int wp, int bk,
+                          int bkw, int bkwp, int bn, uint8_t* perm, uint32_t* tbl, void* bp, cudaStream_t s) {
+    using namespace tcp;
+    const int q = static_cast<int>(n / L);
+    const int npanels = static_cast<int>((k / M + wp - 1) / wp);
+    const int wtot = static_cast<int>(k / M * N);
+    size_t pb, tb, bb;
+    tc_pair_sizes(n, k, N, M, L, wp, bkwp, bn, &pb, &tb, &bb);
+    NM_CUDA_TRY(cudaMemsetAsync(tbl, 0, tb, s));
+    const int nt = npanels * q;
+    pair_perm_kernel<<<static_cast<unsigned>(ceil_div(nt, 128)), 128, 0, s>>>(D, perm, tbl, q, N, M, bn, L, bk, bkw,
+                                                                             bkwp, npanels, wtot);
+    note_launch();
+    NM_LAUNCH_CHECK("pair_perm_kernel");
+    const int64_t units = static_cast<int64_t>(npanels) * bkwp * (n / 8);
+    pair_bperm_kernel<<<static_cast<unsigned>(ceil_div(units, 256)), 256, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(Bv), perm, static_cast<__nv_bfloat16*>(bp), static_cast<int>(n), q, L, bkw,
+        bkwp, npanels, wtot);
+    note_launch();
+    NM_LAUNCH_CHECK("pair_bperm_kernel");
+    return NM_OK;
+}
+
+nm_status tc_pair_run(const void* A, const uint32_t* tbl, const void* bp, void* C, bool c_bf16, int64_t m, int64_t n,
+                      int64_t k, int N, int M, int L, int wp, int bk, int bkw, int bkwp, int bn, cudaStream_t s) {
     using namespace tcp;
     Params p{};
     p.C = C;
@@ -451,39 +484,32 @@ nm_status tc_pair_launch(const void* A, const void* Bv, const uint8_t* D, void* 
     p.bkw = bkw;
     p.bkw_pad = bkwp;
     p.c_bf16 = c_bf16 ? 1 : 0;
-    const int windows = static_cast<int>(k / M);
-    p.npanels = (windows + wp - 1) / wp;
-    const int wtot = static_cast<int>(k / M * N);
-    const int ntiles = static_cast<int>(ceil_div(n, bn));
-
-    uint8_t* perm = nullptr;
-    uint32_t* tbl = nullptr;
-    __nv_bfloat16* Bp = nullptr;
-    nm_status st = scratch_alloc(reinterpret_cast<void**>(&perm), static_cast<size_t>(p.npanels) * p.q * 64, s);
-    if (!st) st = scratch_alloc(reinterpret_cast<void**>(&tbl), static_cast<size_t>(ntiles) * p.npanels * TBL_BYTES, s);
-    if (!st)
-        st = scratch_alloc(reinterpret_cast<void**>(&Bp), static_cast<size_t>(p.npanels) * bkwp * n * sizeof(__nv_bfloat16), s);
-    if (st) return st;
-    NM_CUDA_TRY(cudaMemsetAsync(tbl, 0, static_cast<size_t>(ntiles) * p.npanels * TBL_BYTES, s));
-    const int nt = p.npanels * p.q;
-    pair_perm_kernel<<<static_cast<unsigned>(ceil_div(nt, 128)), 128, 0, s>>>(D, perm, tbl, p.q, N, M, bn, L, bk, bkw,
-                                                                             bkwp, p.npanels, wtot);
-    note_launch();
-    NM_LAUNCH_CHECK("pair_perm_kernel");
-    const int64_t units = static_cast<int64_t>(p.npanels) * bkwp * (n / 8);
-    pair_bperm_kernel<<<static_cast<unsigned>(ceil_div(units, 256)), 256, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(Bv), perm, Bp, static_cast<int>(n), p.q, L, bkw, bkwp, p.npanels, wtot);
-    note_launch();
-    NM_LAUNCH_CHECK("pair_bperm_kernel");
+    p.npanels = static_cast<int>((k / M + wp - 1) / wp);
     p.tbl = tbl;
-
     CUtensorMap tmA, tmB;
     const int box_cols = L >= 64 ? 64 : L;
-    st = make_tma_2d(&tmB, Bp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, static_cast<int64_t>(p.npanels) * bkwp, n, bkwp,
-                     box_cols, box_cols * 2);
+    nm_status st = make_tma_2d(&tmB, bp, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, static_cast<int64_t>(p.npanels) * bkwp, n,
+                               bkwp, box_cols, box_cols * 2);
     if (!st) st = make_tma_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, m, k, BM, 64, 128);
     if (!st) st = bn == 256 ? pair_launch_bn<256>(p, tmA, tmB, m, n, s) : pair_launch_bn<128>(p, tmA, tmB, m, n, s);
-    cudaError_t e1 = cudaFreeAsync(Bp, s), e2 = cudaFreeAsync(tbl, s), e3 = cudaFreeAsync(perm, s);
+    return st;
+}
+
+// nm_spmm without a prepacked weight: prepack into pooled scratch, run, release.
+nm_status tc_pair_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
+                         int64_t k, int N, int M, int L, int wp, int bk, int bkw, int bkwp, int bn, cudaStream_t s) {
+    size_t pb, tb, bb;
+    tc_pair_sizes(n, k, N, M, L, wp, bkwp, bn, &pb, &tb, &bb);
+    uint8_t* perm = nullptr;
+    uint32_t* tbl = nullptr;
+    void* bp = nullptr;
+    nm_status st = scratch_alloc(reinterpret_cast<void**>(&perm), pb, s);
+    if (!st) st = scratch_alloc(reinterpret_cast<void**>(&tbl), tb, s);
+    if (!st) st = scratch_alloc(&bp, bb, s);
+    if (st) return st;
+    st = tc_pair_prepack(Bv, D, n, k, N, M, L, wp, bk, bkw, bkwp, bn, perm, tbl, bp, s);
+    if (!st) st = tc_pair_run(A, tbl, bp, C, c_bf16, m, n, k, N, M, L, wp, bk, bkw, bkwp, bn, s);
+    cudaError_t e1 = cudaFreeAsync(bp, s), e2 = cudaFreeAsync(tbl, s), e3 = cudaFreeAsync(perm, s);
     if (st == NM_OK && (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess)) st = cuda_fail(e1, "cudaFreeAsync");
     return st;
 }

@@ -26,13 +26,22 @@ MATH = {"auto": 0, "f32_simt": 1, "tf32_tc": 2, "bf16_tc": 3}
 
 EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_decompress", "nm_validate",
            "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
-           "nm_profile_begin", "nm_profile_end"]
+           "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked"]
 
 
 class NmError(RuntimeError):
     def __init__(self, status: int, fn: str, msg: str):
         super().__init__(f"{fn}: {STATUS.get(status, status)}: {msg}")
         self.status = status
+
+
+class Prepacked(ctypes.Structure):
+    _fields_ = [("magic", ctypes.c_int32), ("kind", ctypes.c_int32), ("dtype", ctypes.c_int32), ("N", ctypes.c_int32),
+                ("M", ctypes.c_int32), ("L", ctypes.c_int32), ("n", ctypes.c_int64), ("k", ctypes.c_int64),
+                ("bn", ctypes.c_int32), ("wp", ctypes.c_int32), ("bk", ctypes.c_int32), ("bkw", ctypes.c_int32),
+                ("bkw_pad", ctypes.c_int32), ("npanels", ctypes.c_int32), ("values", ctypes.c_void_p),
+                ("idx", ctypes.c_void_p), ("perm", ctypes.c_void_p), ("tbl", ctypes.c_void_p),
+                ("bperm", ctypes.c_void_p)]
 
 
 class Plan(ctypes.Structure):
@@ -71,9 +80,13 @@ def lib():
                                     ctypes.POINTER(Plan)]
         L.nm_unshard_columns.argtypes = [P, P, I64, I64, I64, I64, I, I, P]
         L.nm_profile_begin.argtypes = []
+        L.nm_prepack_bytes.argtypes = [I64, I64, I, I, I, I]
+        L.nm_prepack_bytes.restype = I64
+        L.nm_prepack.argtypes = [P, P, I64, I64, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
+        L.nm_spmm_prepacked.argtypes = [P, ctypes.POINTER(Prepacked), P, I64, I, P]
         L.nm_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         for name in EXPORTS[2:]:
-            if name != "nm_spmm_host_ws_bytes":
+            if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes"):
                 getattr(L, name).restype = I
         _lib = L
     return _lib
@@ -180,6 +193,48 @@ def nm_spmm(A: torch.Tensor, W: NmWeight, out: torch.Tensor | None = None, out_d
         _dev(out, "out")
     _check(lib().nm_spmm(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), out.data_ptr(), m, W.n, k, W.N, W.M,
                          W.L, _dt(A), _dt(out), MATH[math], _stream(A, stream)), "nm_spmm")
+    return out
+
+
+class PrepackedWeight:
+    '''A weight after nm_prepack (the paper's offline PreProcessing): keeps the
+    original NmWeight (referenced by the descriptor), the device buffer and the descriptor.'''
+
+    def __init__(self, W: NmWeight, stream=None):
+        self.W = W
+        dt = _dt(W.values)
+        nbytes = lib().nm_prepack_bytes(W.n, W.k, W.N, W.M, W.L, dt)
+        if nbytes < 0:
+            raise NmError(2, "nm_prepack_bytes", "bad shape")
+        self.buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=W.values.device)
+        self.desc = Prepacked()
+        _check(lib().nm_prepack(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt,
+                                self.buf.data_ptr(), int(nbytes), ctypes.byref(self.desc), _stream(W.values, stream)),
+               "nm_prepack")
+
+    @property
+    def kind(self) -> int:
+        return int(self.desc.kind)
+
+    def __getattr__(self, name):  # n, k, N, M, L, values, idx ... of the underlying weight
+        return getattr(self.W, name)
+
+
+def nm_prepack(W: NmWeight, stream=None) -> PrepackedWeight:
+    return PrepackedWeight(W, stream)
+
+
+def nm_spmm_prepacked(A: torch.Tensor, PW: PrepackedWeight, out: torch.Tensor | None = None, out_dtype=None,
+                      stream=None) -> torch.Tensor:
+    _dev(A, "A")
+    m, k = A.shape
+    if k != PW.W.k:
+        raise NmError(2, "nm_spmm_prepacked", f"A has k={k}, weight has k={PW.W.k}")
+    cdt = out_dtype or A.dtype
+    if out is None:
+        out = torch.empty((m, PW.W.n), dtype=cdt, device=A.device)
+    _check(lib().nm_spmm_prepacked(A.data_ptr(), ctypes.byref(PW.desc), out.data_ptr(), m, _dt(out),
+                                   _stream(A, stream)), "nm_spmm_prepacked")
     return out
 
 

@@ -349,3 +349,31 @@ def test_spmm_f32_split_tail(nm, oracle, monkeypatch, split):
     W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
     Ad = dev(A)
     assert torch.equal(nm.nm_spmm(Ad, W), nm.nm_spmm(Ad, W))
+
+
+# --------------------------------------------------------------- prepacked weights (P:470-475 offline step)
+@pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES[:6])
+@pytest.mark.parametrize("pair", ["1", "0"])
+def test_spmm_tc_prepacked_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L, pair):
+    monkeypatch.setenv("NM_TC_PAIR", pair)
+    A = synth.integer((m, k), 81, synth.TID_A)
+    B = synth.integer((k, n), 82, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    PW = nm.nm_prepack(W)
+    C = nm.nm_spmm_prepacked(dev(A, torch.bfloat16), PW, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
+    C2 = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(C, C2)
+
+
+def test_spmm_prepacked_fp32_plain(nm, oracle):
+    m, n, k, N, M, L = 200, 256, 256, 8, 32, 32
+    A = synth.uniform((m, k), 91, 1)
+    B = synth.uniform((k, n), 92, 2)
+    vals, D = oracle.compress(B, N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    PW = nm.nm_prepack(W)
+    assert PW.kind == 0
+    C = nm.nm_spmm_prepacked(dev(A), PW).cpu().numpy()
+    assert oracle.rel_frobenius(C, oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
