@@ -182,7 +182,7 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True):
     kms = k_ms / max(1, k_cnt)
     res = {"ms": t, "tflops": flop_count(cfg) / (t * 1e-3) / 1e12, "kernel_ms": kms,
            "kernel_tflops": flop_count(cfg) / (kms * 1e-3) / 1e12, "launches_per_step": launches / steps,
-           "plan": nmspmm.nm_plan_query(*cfg, dtype=dtype, math=math)}
+           "plan": nmspmm.nm_plan_query(*cfg, dtype=dtype, math="f32_simt" if dtype == torch.float32 else "auto")}
     if with_cublas:
         torch.backends.cuda.matmul.allow_tf32 = False
         Cd = torch.empty_like(C)
