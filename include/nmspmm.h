@@ -191,7 +191,7 @@ typedef struct {
     const uint8_t* idx;
     void* perm;      /* inside buf (kind 1) */
     void* tbl;
-    void* bperm;
+    void* bperm;     /* reordered B' as per-(column tile, panel) swizzled shared-memory images */
 } nm_prepacked;
 
 int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt);
