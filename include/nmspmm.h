@@ -183,7 +183,8 @@ nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, i
  */
 typedef struct {
     int32_t magic;   /* 0x4B504D4E ("NMPK") once filled */
-    int32_t kind;    /* 0 = plain (values/idx used directly), 1 = tcgen05 token-pair prepack */
+    int32_t kind;    /* 0 = plain (values/idx used directly), 1 = tcgen05 token-pair prepack,
+                        2 = sparse-tensor-core slot prepack (whole buffer at `bperm`) */
     int32_t dtype, N, M, L;
     int64_t n, k;
     int32_t bn, wp, bk, bkw, bkw_pad, npanels;

@@ -164,6 +164,30 @@ nm_status make_tma_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt
     return NM_OK;
 }
 
+nm_status make_tma_2d_pitched(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t rows,
+                              int64_t cols, int64_t pitch_elems, int box_rows, int box_cols, int swizzle) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return fail(NM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t gdim[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t gstride[1] = {static_cast<cuuint64_t>(pitch_elems) * elem_bytes};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    CUtensorMapSwizzle sw = swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                            : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                            : swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                            : CU_TENSOR_MAP_SWIZZLE_NONE;
+    CUresult r = enc(map, dt, 2, const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char buf[256];
+        snprintf(buf, sizeof(buf), "cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld pitch=%lld box=%dx%d",
+                 static_cast<int>(r), static_cast<long long>(rows), static_cast<long long>(cols),
+                 static_cast<long long>(pitch_elems), box_rows, box_cols);
+        return fail(NM_ERR_ALIGNMENT, buf);
+    }
+    return NM_OK;
+}
+
 // ---------------------------------------------------------- kernels (extern)
 nm_status compress_launch(const void* B, nm_dtype b_dt, int64_t k, int64_t n, int N, int M, int L, void* values,
                           nm_dtype v_dt, uint8_t* idx, cudaStream_t s);
@@ -186,6 +210,23 @@ bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m,
 void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn);
 nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                          int64_t k, int N, int M, int L, cudaStream_t s);
+bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k);
+nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, void* buf,
+                        cudaStream_t s);
+nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k,
+                    cudaStream_t s);
+nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
+                       int64_t k, int N, int M, int L, cudaStream_t s);
+
+// Sparse-tensor-core slot path (spmm_tc_sp.cu): bf16, L in {16, 32, 64, 128}, A 16-B aligned with
+// k % 8 == 0 (the per-call transpose reads 16-B chunks), C 4-B aligned.  NM_TC_SP=0 disables it.
+static bool tc_sp_ok(const void* A, const void* C, int64_t m, int64_t n, int64_t k, int N, int M, int L) {
+    const char* e = getenv("NM_TC_SP");
+    if (e && e[0] == '0') return false;
+    return tc_sp_applicable(m, n, k, N, M, L) && k % 8 == 0 && (reinterpret_cast<uintptr_t>(A) & 15) == 0 &&
+           (reinterpret_cast<uintptr_t>(C) & 3) == 0;
+}
 
 // ---------------------------------------------------------- generic kernel
 // One thread per C element; correct for every valid (N, M, L) and alignment.
@@ -276,7 +317,7 @@ static int simt_mode(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     return 1;
 }
 
-enum KernelId { K_GENERIC = 0, K_SIMT_F32 = 1, K_TC_BF16 = 2, K_TC_TF32 = 3 };
+enum KernelId { K_GENERIC = 0, K_SIMT_F32 = 1, K_TC_BF16 = 2, K_TC_TF32 = 3, K_TC_SP = 4 };
 
 static nm_status select(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                         int L, nm_dtype ab, nm_dtype cd, nm_math math, int* kernel, nm_math* used) {
@@ -292,7 +333,9 @@ static nm_status select(const void* A, const void* Bv, const void* C, int64_t m,
     }
     if (math == NM_MATH_AUTO || math == NM_MATH_BF16_TC) {
         *used = NM_MATH_BF16_TC;
-        *kernel = tc_bf16_applicable(A, Bv, C, m, n, k, N, M, L) ? K_TC_BF16 : K_GENERIC;
+        *kernel = tc_sp_ok(A, C, m, n, k, N, M, L)                  ? K_TC_SP
+                  : tc_bf16_applicable(A, Bv, C, m, n, k, N, M, L) ? K_TC_BF16
+                                                                    : K_GENERIC;
         return NM_OK;
     }
     return fail(NM_ERR_UNSUPPORTED, "math mode not available for bf16 operands");
@@ -377,6 +420,7 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
         return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
                                static_cast<float*>(C), m, n, k, N, M, L, mode, s);
     }
+    if (kernel == K_TC_SP) return tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
     if (kernel == K_TC_BF16) return tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
     if (ab_dt == NM_F32) return generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
     if (c_dt == NM_BF16) return generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);
@@ -446,6 +490,16 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->threads = 256;
         out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
         out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
+    } else if (kernel == K_TC_SP) {
+        // tokens x output columns per CTA (MMA N x M), 64 slots (2 sparse MMAs) per stage
+        out->bm = 256;
+        out->bn = 128;
+        out->bk = 64;
+        out->bkw = 32;
+        out->stages = 5;
+        out->threads = 192;
+        out->grid = static_cast<int32_t>(ceil_div(m, 256) * ceil_div(n, 128));
+        out->smem_bytes = 5 * (64 * 256 * 2 + 128 * 64 + 128 * 16) + 1024 + 256;
     } else if (kernel == K_TC_BF16) {
         int wp, bk, bkw, bkwp, bn;
         tc_bf16_geometry(N, M, L, &wp, &bk, &bkw, &bkwp, &bn);
@@ -497,11 +551,17 @@ static bool prepack_kind1(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt
     tc_bf16_geometry(N, M, L, &g[0], &g[1], &g[2], &g[3], &g[4]);
     return tc_pair_applicable(1, n, k, N, M, L, g[4], g[3]);
 }
+// kind 2 iff the sparse-tensor-core slot kernel would run (aligned operands assumed)
+static bool prepack_kind2(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
+    static const float dummy[4] = {0, 0, 0, 0};
+    return dt == NM_BF16 && k > 0 && tc_sp_ok(dummy, dummy, 1, n, k, N, M, L);
+}
 }  // namespace nm
 extern "C" {
 
 int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
     if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16) return -1;
+    if (prepack_kind2(n, k, N, M, L, dt)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k));
     int g[5];
     if (!prepack_kind1(n, k, N, M, L, dt, g)) return 0;
     size_t pb, tb, bb;
@@ -525,7 +585,15 @@ nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t 
     out->values = values;
     out->idx = idx;
     int g[5];
-    if (prepack_kind1(n, k, N, M, L, dt, g)) {
+    if (prepack_kind2(n, k, N, M, L, dt)) {
+        const int64_t need = nm_prepack_bytes(n, k, N, M, L, dt);
+        if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
+        if ((st = require_device())) return st;
+        out->kind = 2;
+        out->bperm = buf;
+        st = tc_sp_prepack(values, idx, n, k, N, M, L, buf, static_cast<cudaStream_t>(stream));
+        if (st) return st;
+    } else if (prepack_kind1(n, k, N, M, L, dt, g)) {
         const int64_t need = nm_prepack_bytes(n, k, N, M, L, dt);
         if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
         if ((st = require_device())) return st;
@@ -552,6 +620,15 @@ nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t 
 
 nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt, void* stream) {
     if (!w || w->magic != kPrepackMagic) return fail(NM_ERR_NULL, "nm_spmm_prepacked: descriptor not filled by nm_prepack");
+    if (w->kind == 2) {
+        nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
+        if (st) return st;
+        if (m == 0 || w->n == 0) return NM_OK;
+        if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
+        if ((st = require_device())) return st;
+        if (tc_sp_ok(A, C, m, w->n, w->k, w->N, w->M, w->L))
+            return tc_sp_run(A, w->bperm, C, c_dt == NM_BF16, m, w->n, w->k, static_cast<cudaStream_t>(stream));
+    }
     if (w->kind == 1) {
         nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
         if (st) return st;

@@ -46,6 +46,10 @@ void prof_end(cudaStream_t s);
 nm_status make_tma_2d(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem_bytes,
                       int64_t rows, int64_t cols, int box_rows, int box_cols, int swizzle);
 
+// Same with an explicit row pitch (elements) >= cols.
+nm_status make_tma_2d_pitched(CUtensorMap* map, const void* base, CUtensorMapDataType dt, int elem_bytes, int64_t rows,
+                              int64_t cols, int64_t pitch_elems, int box_rows, int box_cols, int swizzle);
+
 // --------------------------------------------------------------- device PTX
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

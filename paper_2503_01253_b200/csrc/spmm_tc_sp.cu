@@ -1,0 +1,559 @@
+// spmm_tc_sp.cu -- bf16 vector-wise N:M SpMM on the sparse tensor cores (tcgen05.mma.sp, sm_100a).
+//
+// Eq. 1 computed as C^T = B~^T . A^T with the weight as the MMA's sparse A operand:
+//   * MMA M = 128 output columns (128 / L column groups), MMA N = 256 tokens, MMA K = 32 "slots".
+//   * Per column tile, the union of the k rows its groups keep (the paper's col_info)
+//     is arranged offline into a slot sequence kappa(s) in which every aligned quad of slots holds
+//     at most two rows kept by any one group (sp_pack_kernel: the paper's offline index
+//     reordering).  Each output column then is 2:4 sparse along the slots, which is
+//     exactly what the sparse tensor core contracts at twice the dense rate: per quad, two
+//     values of B' plus a 4-bit metadata nibble naming their slots.
+//   * The dense operand is the token tile of A gathered by slot: rows kappa(s) of A^T (A
+//     transposed once per call), one 512-B row (256 tokens) per warp-wide 16-B cp.async,
+//     written straight into the 128-B-swizzled MN-major layout the MMA reads.  (TMA
+//     tile::gather4 does the same with no SM instructions but measured ~80 clk per 4 rows
+//     per SM on B200 -- 6x slower than this kernel needs.)
+//   * Compressed weights + metadata are prepacked per (column tile, 64-slot stage) as the exact
+//     shared-memory images (one bulk copy each); metadata goes to TMEM by tcgen05.cp.
+// Roles: warps 0-3 gather (16 slot rows each per stage; warp 0 also bulk-copies the weight
+// image) and then the epilogue (TMEM -> registers -> C); warp 4 MMA issuer (tcgen05.cp + 2
+// tcgen05.mma.sp per stage).
+#include <cuda_bf16.h>
+
+#include <cstdlib>
+
+#include "tcgen05.cuh"
+
+namespace nm {
+namespace tcs {
+
+using namespace nm::tc;
+
+constexpr int MC = 128;                    // output columns per CTA (MMA M)
+constexpr int NT = 256;                    // tokens per CTA (MMA N)
+constexpr int SLOTS = 64;                  // logical k slots per stage (2 MMAs of K = 32)
+constexpr int STAGES = 5;
+constexpr int A_BYTES = MC * SLOTS;        // 128 rows x 32 compressed bf16 (64 B rows, 64-B swizzle)
+constexpr int E_BYTES = MC * 16;           // metadata: 128 TMEM lanes x 16 B (columns 0, 1 used)
+constexpr int W_BYTES = A_BYTES + E_BYTES; // per (column tile, stage) weight image
+constexpr int B_BYTES = SLOTS * NT * 2;    // gathered tokens: 4 token atoms x 64 slot rows x 128 B
+constexpr int GATHER_WARPS = 4;            // also the epilogue warps (TMEM lane quarter = warp)
+constexpr int MMA_WARP = GATHER_WARPS;
+constexpr int THREADS = (GATHER_WARPS + 1) * 32;
+constexpr int SMEM_BYTES = STAGES * (W_BYTES + B_BYTES) + 1024 + 256;
+constexpr int TMEM_COLS = 512;             // accumulator 256 + metadata ring 4 x STAGES
+constexpr int META_COL = NT;
+
+struct Params {
+    const uint8_t* wimg;   // [ntiles][max_stages][W_BYTES]
+    const int* slots;      // [ntiles][smax] row of A^T per slot (k = padding, TMA zero fill)
+    const int* nstages;    // [ntiles]
+    void* C;
+    int m, n, k, mp, smax, max_stages, c_bf16;
+    int dbg;  // NM_SP_DBG (timing studies only): 1 skip gathers, 2 skip MMAs, 8 skip C stores, 16 skip weights
+};
+
+// 16-B global -> shared copy (L2 only); src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mma_sp(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc,
+                                       uint32_t emeta) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t}" ::"r"(d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(emeta)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc) {
+    asm volatile("tcgen05.cp.cta_group::1.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+
+// NM_SP_DBG & 64: CTA (0,0) records clock64 per stage into C (timing study only)
+#define SP_TS(st, slot)                                                                                \
+    do {                                                                                               \
+        if ((p.dbg & 64) && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0)                           \
+            static_cast<long long*>(p.C)[(st) * 8 + (slot)] = clock64();                               \
+    } while (0)
+
+__global__ void __launch_bounds__(THREADS, 1)
+    spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* sB = smem;                               // STAGES x B_BYTES (1024-aligned: 128-B swizzle atoms)
+    uint8_t* sW = smem + STAGES * B_BYTES;            // STAGES x W_BYTES (A image 64-B swizzle, then metadata)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sW + STAGES * W_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // token tiles vary fastest: the CTAs that share a column tile's weight stream run together,
+    // so it is read from DRAM once and served from L2 to the others
+    const int tile = blockIdx.y;
+    const int m0 = blockIdx.x * NT;
+    const int nst = p.nstages[tile];
+
+    if (warp == MMA_WARP) {
+        if (lane == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(&full[s], 1 + 32 * GATHER_WARPS);
+                mbar_init(&empty[s], 1);
+            }
+            mbar_init(acc_full, 1);
+            fence_mbar_init();
+        }
+        __syncwarp();
+        tmem_alloc(tmem_slot, TMEM_COLS);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp < GATHER_WARPS) {
+        // ============ gather: one slot row (all 256 tokens, 512 B) per warp instruction ============
+        // lane l copies tokens [8l, 8l+8) of the row: token atom l/8, 16-B chunk l%8 of the
+        // 128-B swizzled row (chunk ^= row % 8).  Warp wg owns rows [16 wg, 16 wg + 16) of a stage.
+        // Completion: cp.async.mbarrier.arrive.noinc per thread (no wait in the loop).
+        const uint8_t* wsrc = p.wimg + static_cast<int64_t>(tile) * p.max_stages * W_BYTES;
+        const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * 16 + (lane & 15);
+        const int tok = m0 + 8 * lane;
+        const bool tok_ok = tok < p.mp;
+        const __nv_bfloat16* src_base = At + (tok_ok ? tok : 0);
+        const uint32_t dst_lane = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128));
+        const uint32_t chunk = static_cast<uint32_t>(lane & 7);
+        // slot rows are prefetched 4 stages ahead (a global load per stage on the critical path
+        // would cost one L2 latency per stage): rotating registers, loop unrolled by 4
+        int kq[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) kq[u] = u < nst ? ssrc[u * SLOTS] : 0;
+        for (int st0 = 0; st0 < nst; st0 += 4) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int st = st0 + u;
+                if (st >= nst) break;
+                const int s = st % STAGES;
+                const int kap = kq[u];
+                if (st + 4 < nst) kq[u] = ssrc[(st + 4) * SLOTS];
+                if (warp == 0) SP_TS(st, 0);
+                if (st >= STAGES) mbar_wait(&empty[s], ((st / STAGES) - 1) & 1);
+                if (warp == 0) SP_TS(st, 1);
+                if (warp == 0 && lane == 0) {
+                    if (p.dbg & 16) {
+                        mbar_arrive(&full[s]);
+                    } else {
+                        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(W_BYTES));
+                        bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(st) * W_BYTES, W_BYTES, &full[s]);
+                    }
+                }
+                if (!(p.dbg & 1)) {
+                    const uint32_t bstage = smem_u32(sB + s * B_BYTES) + dst_lane;
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int r = warp * 16 + i;  // row within the stage
+                        const int kr = __shfl_sync(0xffffffffu, kap, i);
+                        const uint32_t dst = bstage + static_cast<uint32_t>(r * 128) + ((chunk ^ (r & 7)) << 4);
+                        const bool ok = tok_ok && kr < p.k;
+                        cp_async16(dst, src_base + (ok ? static_cast<int64_t>(kr) * p.mp : 0), ok ? 16u : 0u);
+                    }
+                }
+                // arrives on full[s] once this thread's copies have landed (counts as one of the
+                // barrier's expected arrivals: 32 x GATHER_WARPS + 1)
+                cp_async_arrive_noinc(&full[s]);
+                if (warp == 0) SP_TS(st, 2);
+            }
+        }
+    } else {
+        // ============ MMA issuer: metadata -> TMEM, two sparse MMAs per stage ============
+        constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+                                   (static_cast<uint32_t>(NT >> 3) << 17) | (static_cast<uint32_t>(MC >> 4) << 24);
+        for (int st = 0; st < nst; ++st) {
+            const int s = st % STAGES;
+            SP_TS(st, 3);
+            mbar_wait(&full[s], (st / STAGES) & 1);
+            SP_TS(st, 4);
+            tc_fence_after();
+            if (elect_one() && !(p.dbg & 2)) {
+                const uint32_t wa = smem_u32(sW + s * W_BYTES);
+                const uint32_t ecol = tmem + META_COL + 4 * s;
+                tmem_cp_128x128b(ecol, smem_desc(wa + A_BYTES, 2048, 128, 0));
+                const uint32_t ba = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    mma_sp(tmem, smem_desc(wa + 32 * j, 16, 512, 4), smem_desc(ba + 4096 * j, SLOTS * 128, 1024, 2),
+                           idesc | static_cast<uint32_t>(j), (st | j) ? 1u : 0u, ecol);
+            }
+            if (elect_one()) tc_commit(&empty[s]);
+            __syncwarp();
+            SP_TS(st, 5);
+        }
+        if (elect_one()) tc_commit(acc_full);
+        __syncwarp();
+    }
+
+    if (warp < GATHER_WARPS) {
+        // ============ epilogue: TMEM lane = output column, TMEM column = token ============
+        const int qw = warp;
+        const int col = tile * MC + qw * 32 + lane;        // this lane's output column
+        const int pc = tile * MC + qw * 32 + (lane & ~1);  // column pair base
+        const bool odd = lane & 1;
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+        for (int t0 = 0; t0 < NT; t0 += 32) {
+            uint32_t v[32];
+            if (nst > 0) {
+                tmem_ld32(tmem + (static_cast<uint32_t>(qw * 32) << 16) + t0, v);
+                tmem_wait_ld();
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = 0u;
+            }
+            if (p.c_bf16) {
+                // lanes (2p, 2p+1) swap so each stores a bf16 pair (columns pc, pc+1): even lane token i, odd i+1
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const uint32_t x = odd ? v[i] : v[i + 1];
+                    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
+                    const float lo = __uint_as_float(odd ? y : v[i]);
+                    const float hi = __uint_as_float(odd ? v[i + 1] : y);
+                    const int t = m0 + t0 + i + (odd ? 1 : 0);
+                    if (t < p.m && pc < p.n && !(p.dbg & (8 | 64))) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+                        *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.C) +
+                                                           static_cast<int64_t>(t) * p.n + pc) = h;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const int t = m0 + t0 + i;
+                    if (t < p.m && col < p.n && !(p.dbg & (8 | 64)))
+                        static_cast<float*>(p.C)[static_cast<int64_t>(t) * p.n + col] = __uint_as_float(v[i]);
+                }
+            }
+        }
+        tc_fence_before();
+    }
+    __syncthreads();
+    if (warp == MMA_WARP) {
+        tc_fence_after();
+        tmem_dealloc(tmem, TMEM_COLS);
+    }
+}
+
+// A (m x k bf16, row-major) -> At (k x mp, mp = m rounded up to 8): 64 x 64 tiles through shared memory.
+__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ A, __nv_bfloat16* __restrict__ At, int m,
+                                      int k, int mp) {
+    __shared__ __nv_bfloat16 t[64][66];
+    const int k0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
+    const int tid = threadIdx.x;  // 256 threads
+    // load: 64 rows x 8 chunks of 8 k (16 B)
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+        const int e = tid + it * 256;
+        const int r = e >> 3, c = (e & 7) * 8;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (r0 + r < m && k0 + c < k) v = *reinterpret_cast<const uint4*>(A + static_cast<int64_t>(r0 + r) * k + k0 + c);
+        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) t[r][c + j] = h[j];
+    }
+    __syncthreads();
+    // store: 64 k rows x 8 chunks of 8 tokens
+#pragma unroll
+    for (int it = 0; it < 2; ++it) {
+        const int e = tid + it * 256;
+        const int kr = e >> 3, c = (e & 7) * 8;
+        if (k0 + kr < k && r0 + c < mp) {
+            __align__(16) __nv_bfloat16 h[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h[j] = t[c + j][kr];
+            *reinterpret_cast<uint4*>(At + static_cast<int64_t>(k0 + kr) * mp + r0 + c) = *reinterpret_cast<uint4*>(h);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------- offline prepack
+// Slot packing for one column tile (one thread per tile; the paper's offline PreProcessing slot,
+// Listing 3).  Item = k row kept by at least one of the tile's G groups, type = G-bit
+// membership mask.  Greedy: fill each quad with the heaviest type that still fits (no group above
+// two rows per quad), ties to the type with the most items left.  Every quad takes >= 2 items,
+// so a tile needs at most 2 |U| + 4 slots.
+__global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ slots, uint8_t* __restrict__ stype,
+                               int* __restrict__ nstages, int* __restrict__ qbuf, int n, int k, int N, int M, int L,
+                               int smax) {
+    const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ntiles = (n + MC - 1) / MC;
+    if (tile >= ntiles) return;
+    const int q = n / L, G = MC / L, g0 = tile * G;
+    const int gcount = min(G, q - g0);
+    const int T = 1 << G;
+    int* qk = qbuf + static_cast<int64_t>(tile) * (k + 256 + 1);  // per-type queues of k rows ([k]) + counts
+    int* cnt = qk + k;                                             // [T <= 256]
+    // membership per k row, accumulated in the queue area first (as masks), then bucketed
+    for (int i = 0; i < k; ++i) qk[i] = 0;
+    const int windows = k / M;
+    for (int gi = 0; gi < gcount; ++gi)
+        for (int t = 0; t < windows; ++t)
+            for (int s = 0; s < N; ++s) {
+                const int off = D[static_cast<int64_t>(t * N + s) * q + g0 + gi];
+                qk[t * M + off] |= 1 << gi;
+            }
+    for (int t = 0; t < T; ++t) cnt[t] = 0;
+    for (int i = 0; i < k; ++i) cnt[qk[i]]++;
+    // bucket in place: start offsets per type, then a second array would be needed -- use the
+    // slot array of this tile as temporary storage for the masks
+    int* sl = slots + static_cast<int64_t>(tile) * smax;
+    uint8_t* ty = stype + static_cast<int64_t>(tile) * smax;
+    for (int i = 0; i < k; ++i) sl[i] = qk[i];
+    int start[257];
+    int acc = 0;
+    for (int t = 0; t < T; ++t) {
+        start[t] = acc;
+        acc += cnt[t];
+    }
+    start[T] = acc;
+    int fillp[256];
+    for (int t = 0; t < T; ++t) fillp[t] = start[t];
+    for (int i = 0; i < k; ++i) qk[fillp[sl[i]]++] = i;
+    int head[256];
+    for (int t = 0; t < T; ++t) head[t] = start[t];
+    int remaining = k - cnt[0];
+    int ns = 0;  // slots written
+    while (remaining > 0) {
+        uint32_t once = 0, twice = 0;
+        int placed = 0;
+        for (int sidx = 0; sidx < 4; ++sidx) {
+            int best = -1, bkey = -1;
+            for (int t = 1; t < T; ++t) {
+                const int left = start[t + 1] - head[t];
+                if (left == 0 || (static_cast<uint32_t>(t) & twice)) continue;
+                const int key = (__popc(t) << 20) + left;
+                if (key > bkey) bkey = key, best = t;
+            }
+            if (best < 0) break;
+            sl[ns] = qk[head[best]++];
+            ty[ns] = static_cast<uint8_t>(best);
+            ++ns;
+            twice |= once & static_cast<uint32_t>(best);
+            once |= static_cast<uint32_t>(best);
+            --remaining;
+            ++placed;
+        }
+        for (; placed < 4; ++placed) {
+            sl[ns] = k;  // padding slot: out-of-range row, TMA zero fill
+            ty[ns] = 0;
+            ++ns;
+        }
+    }
+    const int padded = (ns + SLOTS - 1) / SLOTS * SLOTS;
+    for (; ns < padded; ++ns) {
+        sl[ns] = k;
+        ty[ns] = 0;
+    }
+    nstages[tile] = padded / SLOTS;
+}
+
+// Weight images: one thread per (tile, stage, output row r of the tile).  Per quad: the (<= 2)
+// slots whose row the thread's group keeps -> 2 compressed values (A image, 64-B swizzled
+// K-major) + the metadata nibble (slot index of value 0 | slot index of value 1 << 2) at the
+// TMEM position of (row r, chunk) for tcgen05.mma.sp kind::f16:
+//   lane = r%8 + 8 (chunk/4 of the MMA) + 16 (r/16), bit = 16 ((r/8)%2) + 4 (chunk%4).
+__global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint8_t* __restrict__ D,
+                                const int* __restrict__ slots, const uint8_t* __restrict__ stype,
+                                const int* __restrict__ nstages, uint8_t* __restrict__ wimg, int n, int k, int N, int M,
+                                int L, int smax, int max_stages) {
+    const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int r = static_cast<int>(gid % MC);
+    const int64_t ts = gid / MC;
+    const int st = static_cast<int>(ts % max_stages);
+    const int tile = static_cast<int>(ts / max_stages);
+    const int ntiles = (n + MC - 1) / MC;
+    if (tile >= ntiles || st >= nstages[tile]) return;
+    const int q = n / L;
+    const int j = tile * MC + r;
+    const int g = j / L, gi = r / L;
+    const bool live = j < n;
+    uint8_t* img = wimg + (static_cast<int64_t>(tile) * max_stages + st) * W_BYTES;
+    uint32_t* meta = reinterpret_cast<uint32_t*>(img + A_BYTES);
+    const int* sl = slots + static_cast<int64_t>(tile) * smax + st * SLOTS;
+    const uint8_t* ty = stype + static_cast<int64_t>(tile) * smax + st * SLOTS;
+    for (int qd = 0; qd < SLOTS / 4; ++qd) {
+        int pos[2] = {-1, -1};
+        int npos = 0;
+        for (int i = 0; i < 4; ++i)
+            if (live && ((ty[4 * qd + i] >> gi) & 1)) pos[npos++] = i;
+        // fill unused value positions with distinct unused slots (value 0)
+        for (int i = 0; npos < 2 && i < 4; ++i)
+            if (i != pos[0]) pos[npos++] = i;
+        if (pos[0] > pos[1]) {
+            const int t = pos[0];
+            pos[0] = pos[1];
+            pos[1] = t;
+        }
+        for (int h = 0; h < 2; ++h) {
+            __nv_bfloat16 v = __float2bfloat16(0.f);
+            const int kk = sl[4 * qd + pos[h]];
+            if (live && kk < k && ((ty[4 * qd + pos[h]] >> gi) & 1)) {
+                const int t = kk / M, off = kk % M;
+                int lo = 0, hi = N - 1;  // D ascending within the window (R7)
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (D[static_cast<int64_t>(t * N + mid) * q + g] < off) lo = mid + 1;
+                    else hi = mid;
+                }
+                v = Bv[static_cast<int64_t>(t * N + lo) * n + j];
+            }
+            const int pidx = 2 * qd + h;  // compressed element of the row (0..31)
+            const int b = 2 * pidx;
+            const int off = (r / 8) * 512 + (r % 8) * 64 + ((((b >> 4) ^ ((r % 8) >> 1)) & 3) << 4) + (b & 15);
+            *reinterpret_cast<__nv_bfloat16*>(img + off) = v;
+        }
+        const int mma = qd / 8, c = qd % 8;
+        const int ln = (r % 8) + 8 * (c / 4) + 16 * (r / 16);
+        const int bit = 16 * ((r / 8) % 2) + 4 * (c % 4);
+        atomicOr(&meta[ln * 4 + mma], static_cast<uint32_t>(pos[0] | (pos[1] << 2)) << bit);
+    }
+}
+
+}  // namespace tcs
+
+bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
+    (void)m;
+    (void)N;
+    return (L == 16 || L == 32 || L == 64 || L == 128) && n % 2 == 0 && k > 0 && k < (1 << 30) && M <= 256;
+}
+
+void tc_sp_sizes(int64_t n, int64_t k, size_t* off_slots, size_t* off_stype, size_t* off_nst, size_t* off_q,
+                 size_t* off_img, size_t* total, int* smax, int* max_stages) {
+    using namespace tcs;
+    const int64_t ntiles = (n + MC - 1) / MC;
+    const int64_t sm = ((2 * k + 4) + SLOTS - 1) / SLOTS * SLOTS;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    size_t o = 0;
+    *off_slots = o;
+    o += al(static_cast<size_t>(ntiles * sm) * 4);
+    *off_stype = o;
+    o += al(static_cast<size_t>(ntiles * sm));
+    *off_nst = o;
+    o += al(static_cast<size_t>(ntiles) * 4);
+    *off_q = o;
+    o += al(static_cast<size_t>(ntiles * (k + 257)) * 4);
+    *off_img = o;
+    o += static_cast<size_t>(ntiles * (sm / SLOTS)) * W_BYTES;
+    *total = o;
+    *smax = static_cast<int>(sm);
+    *max_stages = static_cast<int>(sm / SLOTS);
+}
+
+nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, void* buf,
+                        cudaStream_t s) {
+    using namespace tcs;
+    size_t os, ot, on, oq, oi, tot;
+    int smax, mst;
+    tc_sp_sizes(n, k, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    uint8_t* b = static_cast<uint8_t*>(buf);
+    const int ntiles = static_cast<int>((n + MC - 1) / MC);
+    NM_CUDA_TRY(cudaMemsetAsync(b + oi, 0, tot - oi, s));
+    sp_pack_kernel<<<static_cast<unsigned>(ceil_div(ntiles, 32)), 32, 0, s>>>(
+        D, reinterpret_cast<int*>(b + os), b + ot, reinterpret_cast<int*>(b + on), reinterpret_cast<int*>(b + oq),
+        static_cast<int>(n), static_cast<int>(k), N, M, L, smax);
+    note_launch();
+    NM_LAUNCH_CHECK("sp_pack_kernel");
+    const int64_t threads = static_cast<int64_t>(ntiles) * mst * MC;
+    sp_image_kernel<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, s>>>(
+        static_cast<const __nv_bfloat16*>(Bv), D, reinterpret_cast<const int*>(b + os), b + ot,
+        reinterpret_cast<const int*>(b + on), b + oi, static_cast<int>(n), static_cast<int>(k), N, M, L, smax, mst);
+    note_launch();
+    NM_LAUNCH_CHECK("sp_image_kernel");
+    return NM_OK;
+}
+
+nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k,
+                    cudaStream_t s) {
+    using namespace tcs;
+    size_t os, ot, on, oq, oi, tot;
+    int smax, mst;
+    tc_sp_sizes(n, k, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    const uint8_t* b = static_cast<const uint8_t*>(buf);
+    const int64_t mp = (m + 7) / 8 * 8;
+    __nv_bfloat16* at = nullptr;
+    nm_status st = scratch_alloc(reinterpret_cast<void**>(&at), static_cast<size_t>(k * mp) * 2, s);
+    if (st) return st;
+    const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(mp, 64)));
+    transpose_bf16_kernel<<<tg, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(A), at, static_cast<int>(m),
+                                             static_cast<int>(k), static_cast<int>(mp));
+    note_launch();
+    NM_LAUNCH_CHECK("transpose_bf16_kernel");
+    {
+        static bool attr = false;
+        if (!attr) {
+            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+            attr = true;
+        }
+        Params p{};
+        p.wimg = b + oi;
+        p.slots = reinterpret_cast<const int*>(b + os);
+        p.nstages = reinterpret_cast<const int*>(b + on);
+        p.C = C;
+        p.m = static_cast<int>(m);
+        p.n = static_cast<int>(n);
+        p.k = static_cast<int>(k);
+        p.mp = static_cast<int>(mp);
+        p.smax = smax;
+        p.max_stages = mst;
+        p.c_bf16 = c_bf16 ? 1 : 0;
+        const char* dbg = std::getenv("NM_SP_DBG");
+        p.dbg = dbg ? std::atoi(dbg) : 0;
+        const dim3 grid(static_cast<unsigned>(ceil_div(m, NT)), static_cast<unsigned>(ceil_div(n, MC)));
+        prof_begin(s);
+        spmm_tc_sp_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(at, p);
+        prof_end(s);
+        note_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) st = cuda_fail(e, "spmm_tc_sp_kernel");
+    }
+    const cudaError_t e = cudaFreeAsync(at, s);
+    if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
+    return st;
+}
+
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k) {
+    size_t os, ot, on, oq, oi, tot;
+    int smax, mst;
+    tc_sp_sizes(n, k, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    return tot;
+}
+
+// nm_spmm without a prepacked weight: prepack into pooled scratch, run, release.
+nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
+                       int64_t k, int N, int M, int L, cudaStream_t s) {
+    void* buf = nullptr;
+    nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k), s);
+    if (st) return st;
+    st = tc_sp_prepack(Bv, D, n, k, N, M, L, buf, s);
+    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, s);
+    const cudaError_t e = cudaFreeAsync(buf, s);
+    if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
+    return st;
+}
+
+}  // namespace nm

@@ -270,23 +270,37 @@ TC_CASES = [
 ]
 
 
+TC_PATHS = {"sp": ("1", "1", 4), "pair": ("0", "1", 2), "plain": ("0", "0", 2)}  # NM_TC_SP, NM_TC_PAIR, kernel id
+
+
+def use_tc_path(monkeypatch, path):
+    sp, pair, kid = TC_PATHS[path]
+    monkeypatch.setenv("NM_TC_SP", sp)
+    monkeypatch.setenv("NM_TC_PAIR", pair)
+    return kid
+
+
 @pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
 @pytest.mark.parametrize("cdt", [torch.bfloat16, torch.float32])
-def test_spmm_tc_bf16_vs_oracle(nm, oracle, m, n, k, N, M, L, cdt):
+@pytest.mark.parametrize("path", ["sp", "pair"])
+def test_spmm_tc_bf16_vs_oracle(nm, oracle, monkeypatch, m, n, k, N, M, L, cdt, path):
+    kid = use_tc_path(monkeypatch, path)
     A = synth.bf16grid((m, k), 51, synth.TID_A)
     B = synth.bf16grid((k, n), 52, synth.TID_B)
     vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
     W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
     plan = nm.nm_plan_query(m, n, k, N, M, L, torch.bfloat16, "bf16_tc")
-    assert plan["kernel"] == 2, plan  # the tcgen05 kernel, not the generic fallback
+    assert plan["kernel"] == kid, plan  # the tcgen05 kernel, not the generic fallback
     C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=cdt, math="bf16_tc").float().cpu().numpy()
     ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
     assert oracle.rel_frobenius(C, ref) <= TOL_BF16
 
 
 @pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
-def test_spmm_tc_bf16_integer_exact(nm, oracle, m, n, k, N, M, L):
+@pytest.mark.parametrize("path", ["sp", "pair"])
+def test_spmm_tc_bf16_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L, path):
     """Integer inputs: every partial sum is exact in fp32 -> bit-exact C (fp32 out)."""
+    use_tc_path(monkeypatch, path)
     A = synth.integer((m, k), 61, synth.TID_A)
     B = synth.integer((k, n), 62, synth.TID_B)
     vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
@@ -302,7 +316,9 @@ def test_spmm_tc_bf16_deterministic(nm):
 
 
 @pytest.mark.parametrize("cfg", ["cfg2", "cfg3_62", "cfg3_75", "cfg4_65b"])
-def test_spmm_tc_bf16_full_size_sampled(nm, oracle, cfg):
+@pytest.mark.parametrize("path", ["sp", "pair"])
+def test_spmm_tc_bf16_full_size_sampled(nm, oracle, monkeypatch, cfg, path):
+    use_tc_path(monkeypatch, path)
     m, n, k, N, M, L = {"cfg2": (4096, 4096, 4096, 16, 32, 32), "cfg3_62": (2048, 11008, 4096, 12, 32, 32),
                         "cfg3_75": (2048, 11008, 4096, 8, 32, 32), "cfg4_65b": (2048, 22016, 8192, 4, 32, 32)}[cfg]
     A = synth.bf16grid((m, k), 71, synth.TID_A)
@@ -352,10 +368,10 @@ def test_spmm_f32_split_tail(nm, oracle, monkeypatch, split):
 
 
 # --------------------------------------------------------------- prepacked weights (P:470-475 offline step)
-@pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES[:6])
-@pytest.mark.parametrize("pair", ["1", "0"])
-def test_spmm_tc_prepacked_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L, pair):
-    monkeypatch.setenv("NM_TC_PAIR", pair)
+@pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
+@pytest.mark.parametrize("path", ["sp", "pair", "plain"])
+def test_spmm_tc_prepacked_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L, path):
+    use_tc_path(monkeypatch, path)
     A = synth.integer((m, k), 81, synth.TID_A)
     B = synth.integer((k, n), 82, synth.TID_B)
     vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
@@ -363,6 +379,7 @@ def test_spmm_tc_prepacked_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M,
     PW = nm.nm_prepack(W)
     C = nm.nm_spmm_prepacked(dev(A, torch.bfloat16), PW, out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
+    assert PW.kind == {"sp": 2, "pair": 1}.get(path, PW.kind)
     C2 = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(C, C2)
 
@@ -377,3 +394,29 @@ def test_spmm_prepacked_fp32_plain(nm, oracle):
     assert PW.kind == 0
     C = nm.nm_spmm_prepacked(dev(A), PW).cpu().numpy()
     assert oracle.rel_frobenius(C, oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
+
+
+# --------------------------------------------------------------- sparse-tensor-core slot path edge cases
+SP_EDGE = [
+    (1, 128, 64, 16, 32, 32),        # single token (one partial token atom)
+    (255, 160, 128, 16, 32, 16),     # n not a multiple of the 128-column tile; L = 16 (8 groups, 256 types)
+    (513, 384, 1024, 1, 32, 32),     # very sparse (1:32): many padding slots
+    (64, 256, 256, 32, 32, 32),      # N = M: dense windows (2 rows per group per quad exactly)
+    (300, 256, 768, 3, 8, 64),       # odd N, M = 8
+    (96, 128, 512, 5, 256, 128),     # M = 256 windows (uint8 offsets up to 255), L = 128 (one group per tile)
+]
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", SP_EDGE)
+def test_spmm_tc_sp_edges_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L):
+    kid = use_tc_path(monkeypatch, "sp")
+    assert nm.nm_plan_query(m, n, k, N, M, L, torch.bfloat16, "bf16_tc")["kernel"] == kid
+    A = synth.integer((m, k), 101, synth.TID_A)
+    B = synth.integer((k, n), 102, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(C.astype(np.float64), ref)
+    Cb = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.bfloat16).float().cpu().numpy()
+    assert oracle.rel_frobenius(Cb, ref) <= TOL_BF16
