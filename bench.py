@@ -291,6 +291,17 @@ def run_reference(args):
     return 0
 
 
+def bf16_kernel_name(cfg):
+    """Name of the bf16 SpMM kernel the selector picks for cfg (nm_plan_query kernel id)."""
+    from paper_2503_01253_b200 import nmspmm
+    import torch
+    m, n, k, N, M, L = cfg
+    plan = nmspmm.nm_plan_query(m, n, k, N, M, L, torch.bfloat16, "bf16_tc")
+    return {4: f"nm::tcs::spmm_tc_sp_kernel<{plan['bn'] // 128}> (sparse tensor cores, {plan['bn']} columns x "
+               f"{plan['bm']} tokens per CTA)",
+            2: "nm::spmm_tc_pair_kernel / nm::tc::spmm_tc_bf16_kernel"}.get(plan["kernel"], "spmm_generic_kernel")
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -361,7 +372,7 @@ def run_ours(args):
         peak = peaks.get("bf16_tflops", 1590.0)
         roof = {"bound": "tensor", "achieved": round(flop_count(cfg) / (kernel_ms * 1e-3) / 1e12, 3),
                 "peak": peak, "unit": "TFLOP/s", "frac": None, "peak_source": f"bf16_tflops ({peaks_src})",
-                "kernel": "nm::tc::spmm_tc_bf16_kernel", "kernel_ms_per_launch": round(kernel_ms, 4),
+                "kernel": bf16_kernel_name(cfg), "kernel_ms_per_launch": round(kernel_ms, 4),
                 "kernel_share_of_step": round(kernel_ms / t_step, 4), "algorithmic_flops_per_launch": flop_count(cfg),
                 "algorithmic_bytes_per_launch": alg_bytes(cfg, 2)}
     roof["frac"] = round(roof["achieved"] / roof["peak"], 4)

@@ -211,11 +211,11 @@ void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_
 nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                          int64_t k, int N, int M, int L, cudaStream_t s);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
-size_t tc_sp_prepack_bytes(int64_t n, int64_t k);
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L);
 nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, void* buf,
                         cudaStream_t s);
-nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k,
-                    cudaStream_t s);
+nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
+                    int M, int L, cudaStream_t s);
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                        int64_t k, int N, int M, int L, cudaStream_t s);
 
@@ -491,15 +491,16 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
         out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
     } else if (kernel == K_TC_SP) {
-        // tokens x output columns per CTA (MMA N x M), 64 slots (2 sparse MMAs) per stage
-        out->bm = 256;
-        out->bn = 128;
+        // tokens x output columns per CTA (MMA N x M per column half), 64 slots per stage
+        const int hh = (L >= 32 && 2 * N >= M) ? 2 : 1;  // spmm_tc_sp.cu sp_halves()
+        out->bm = hh == 2 ? 192 : 256;
+        out->bn = 128 * hh;
         out->bk = 64;
         out->bkw = 32;
         out->stages = 5;
-        out->threads = 192;
-        out->grid = static_cast<int32_t>(ceil_div(m, 256) * ceil_div(n, 128));
-        out->smem_bytes = 5 * (64 * 256 * 2 + 128 * 64 + 128 * 16) + 1024 + 256;
+        out->threads = 288;
+        out->grid = static_cast<int32_t>(ceil_div(m, out->bm) * ceil_div(n, out->bn));
+        out->smem_bytes = 5 * (64 * out->bm * 2 + hh * (128 * 64 + 128 * 16)) + 1024 + 256;
     } else if (kernel == K_TC_BF16) {
         int wp, bk, bkw, bkwp, bn;
         tc_bf16_geometry(N, M, L, &wp, &bk, &bkw, &bkwp, &bn);
@@ -561,7 +562,7 @@ extern "C" {
 
 int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
     if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16) return -1;
-    if (prepack_kind2(n, k, N, M, L, dt)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k));
+    if (prepack_kind2(n, k, N, M, L, dt)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L));
     int g[5];
     if (!prepack_kind1(n, k, N, M, L, dt, g)) return 0;
     size_t pb, tb, bb;
@@ -627,7 +628,8 @@ nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64
         if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
         if ((st = require_device())) return st;
         if (tc_sp_ok(A, C, m, w->n, w->k, w->N, w->M, w->L))
-            return tc_sp_run(A, w->bperm, C, c_dt == NM_BF16, m, w->n, w->k, static_cast<cudaStream_t>(stream));
+            return tc_sp_run(A, w->bperm, C, c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L,
+                             static_cast<cudaStream_t>(stream));
     }
     if (w->kind == 1) {
         nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);

@@ -29,23 +29,47 @@ namespace tcs {
 
 using namespace nm::tc;
 
-constexpr int MC = 128;                    // output columns per CTA (MMA M)
-constexpr int NT = 256;                    // tokens per CTA (MMA N)
+// Geometry.  H = column halves per CTA: each half is one MMA M = 128 with its own accumulator,
+// weight image and metadata, and both halves share the gathered token tile (the slot sequence
+// is packed over all 128 H / L groups), so the gathered bytes per MAC halve at H = 2.
+// H = 2 (L >= 32): 256 columns x 192 tokens; H = 1 (L = 16, where 256 columns would be 16
+// groups): 128 columns x 256 tokens.
 constexpr int SLOTS = 64;                  // logical k slots per stage (2 MMAs of K = 32)
 constexpr int STAGES = 5;
-constexpr int A_BYTES = MC * SLOTS;        // 128 rows x 32 compressed bf16 (64 B rows, 64-B swizzle)
-constexpr int E_BYTES = MC * 16;           // metadata: 128 TMEM lanes x 16 B (columns 0, 1 used)
-constexpr int W_BYTES = A_BYTES + E_BYTES; // per (column tile, stage) weight image
-constexpr int B_BYTES = SLOTS * NT * 2;    // gathered tokens: 4 token atoms x 64 slot rows x 128 B
-constexpr int GATHER_WARPS = 4;            // also the epilogue warps (TMEM lane quarter = warp)
+constexpr int A_BYTES = 128 * SLOTS;       // per half: 128 rows x 32 compressed bf16 (64 B rows, 64-B swizzle)
+constexpr int E_BYTES = 128 * 16;          // per half: metadata, 128 TMEM lanes x 16 B (columns 0, 1 used)
+constexpr int WH_BYTES = A_BYTES + E_BYTES;
+constexpr int GATHER_WARPS = 8;            // also the epilogue warps (TMEM lane quarter = warp % 4)
+constexpr int ROWS_PER_WARP = SLOTS / GATHER_WARPS;
 constexpr int MMA_WARP = GATHER_WARPS;
 constexpr int THREADS = (GATHER_WARPS + 1) * 32;
-constexpr int SMEM_BYTES = STAGES * (W_BYTES + B_BYTES) + 1024 + 256;
-constexpr int TMEM_COLS = 512;             // accumulator 256 + metadata ring 4 x STAGES
-constexpr int META_COL = NT;
+constexpr int TMEM_COLS = 512;
+
+template <int H>
+struct Cfg {
+    static constexpr int MC = 128 * H;                    // output columns per CTA
+    static constexpr int NT = H == 2 ? 192 : 256;         // tokens per CTA (MMA N)
+    static constexpr int B_BYTES = SLOTS * NT * 2;        // NT/64 token atoms x 64 slot rows x 128 B
+    static constexpr int W_BYTES = H * WH_BYTES;          // per (column tile, stage) weight image
+    static constexpr int SMEM_BYTES = STAGES * (W_BYTES + B_BYTES) + 1024 + 256;
+    static constexpr int META_COL = H * NT;               // metadata ring: 4 H columns per stage
+    static_assert(META_COL + 4 * H * STAGES <= TMEM_COLS, "TMEM budget");
+    static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+};
+
+// Column halves per CTA (NM_SP_H=1/2 overrides, ablation).  H = 2 halves the gathered bytes per
+// MAC but packs 8 groups per slot sequence instead of 4; measured on B200 it wins
+// only at N/M >= 1/2 (the union is the whole window either way), and loses at 62.5-87.5 %
+// sparsity (8-group quads fill worse) -- so H = 2 iff L >= 32 and 2N >= M.
+static int sp_halves(int L, int N, int M) {
+    const char* e = std::getenv("NM_SP_H");
+    if (e && e[0] == '1') return 1;
+    if (e && e[0] == '2' && L >= 32) return 2;
+    return (L >= 32 && 2 * N >= M) ? 2 : 1;
+}
 
 struct Params {
-    const uint8_t* wimg;   // [ntiles][max_stages][W_BYTES]
+    const uint8_t* wimg;   // [ntiles][max_stages][H][WH_BYTES]
     const int* slots;      // [ntiles][smax] row of A^T per slot (k = padding, TMA zero fill)
     const int* nstages;    // [ntiles]
     void* C;
@@ -93,12 +117,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
             static_cast<long long*>(p.C)[(st) * 8 + (slot)] = clock64();                               \
     } while (0)
 
+template <int H>
 __global__ void __launch_bounds__(THREADS, 1)
     spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const Params p) {
+    using CF = Cfg<H>;
+    constexpr int NT = CF::NT, MC = CF::MC, B_BYTES = CF::B_BYTES, W_BYTES = CF::W_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sB = smem;                               // STAGES x B_BYTES (1024-aligned: 128-B swizzle atoms)
-    uint8_t* sW = smem + STAGES * B_BYTES;            // STAGES x W_BYTES (A image 64-B swizzle, then metadata)
+    uint8_t* sW = smem + STAGES * B_BYTES;            // STAGES x H x (A image 64-B swizzle, metadata)
     uint64_t* full = reinterpret_cast<uint64_t*>(sW + STAGES * W_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* acc_full = empty + STAGES;
@@ -129,30 +156,33 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp < GATHER_WARPS) {
-        // ============ gather: one slot row (all 256 tokens, 512 B) per warp instruction ============
+        // ============ gather: one slot row (NT tokens) per warp instruction ============
         // lane l copies tokens [8l, 8l+8) of the row: token atom l/8, 16-B chunk l%8 of the
-        // 128-B swizzled row (chunk ^= row % 8).  Warp wg owns rows [16 wg, 16 wg + 16) of a stage.
+        // 128-B swizzled row (chunk ^= row % 8).  Warp wg owns ROWS_PER_WARP consecutive rows of a stage.
         // Completion: cp.async.mbarrier.arrive.noinc per thread (no wait in the loop).
         const uint8_t* wsrc = p.wimg + static_cast<int64_t>(tile) * p.max_stages * W_BYTES;
-        const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * 16 + (lane & 15);
+        const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * ROWS_PER_WARP + (lane % ROWS_PER_WARP);
         const int tok = m0 + 8 * lane;
-        const bool tok_ok = tok < p.mp;
+        const bool lane_on = lane < NT / 8;
+        const bool tok_ok = lane_on && tok < p.mp;
         const __nv_bfloat16* src_base = At + (tok_ok ? tok : 0);
         const uint32_t dst_lane = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128));
         const uint32_t chunk = static_cast<uint32_t>(lane & 7);
-        // slot rows are prefetched 4 stages ahead (a global load per stage on the critical path
-        // would cost one L2 latency per stage): rotating registers, loop unrolled by 4
-        int kq[4];
+        // slot rows are prefetched PF stages ahead in rotating registers (loop unrolled by PF): a
+        // register is reloaded only after PF iterations, so the load latency (~1-2k clk under load)
+        // is not paid per stage -- at PF = 4 it was, and it paced the whole pipeline
+        constexpr int PF = 16;
+        int kq[PF];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) kq[u] = u < nst ? ssrc[u * SLOTS] : 0;
-        for (int st0 = 0; st0 < nst; st0 += 4) {
+        for (int u = 0; u < PF; ++u) kq[u] = u < nst ? ssrc[u * SLOTS] : 0;
+        for (int st0 = 0; st0 < nst; st0 += PF) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < PF; ++u) {
                 const int st = st0 + u;
                 if (st >= nst) break;
                 const int s = st % STAGES;
                 const int kap = kq[u];
-                if (st + 4 < nst) kq[u] = ssrc[(st + 4) * SLOTS];
+                if (st + PF < nst) kq[u] = ssrc[(st + PF) * SLOTS];
                 if (warp == 0) SP_TS(st, 0);
                 if (st >= STAGES) mbar_wait(&empty[s], ((st / STAGES) - 1) & 1);
                 if (warp == 0) SP_TS(st, 1);
@@ -167,12 +197,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (!(p.dbg & 1)) {
                     const uint32_t bstage = smem_u32(sB + s * B_BYTES) + dst_lane;
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const int r = warp * 16 + i;  // row within the stage
+                    for (int i = 0; i < ROWS_PER_WARP; ++i) {
+                        const int r = warp * ROWS_PER_WARP + i;  // row within the stage
                         const int kr = __shfl_sync(0xffffffffu, kap, i);
                         const uint32_t dst = bstage + static_cast<uint32_t>(r * 128) + ((chunk ^ (r & 7)) << 4);
                         const bool ok = tok_ok && kr < p.k;
-                        cp_async16(dst, src_base + (ok ? static_cast<int64_t>(kr) * p.mp : 0), ok ? 16u : 0u);
+                        if (lane_on)
+                            cp_async16(dst, src_base + (ok ? static_cast<int64_t>(kr) * p.mp : 0), ok ? 16u : 0u);
                     }
                 }
                 // arrives on full[s] once this thread's copies have landed (counts as one of the
@@ -182,9 +213,9 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     } else {
-        // ============ MMA issuer: metadata -> TMEM, two sparse MMAs per stage ============
+        // ============ MMA issuer: per stage and half, metadata -> TMEM and two sparse MMAs ============
         constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
-                                   (static_cast<uint32_t>(NT >> 3) << 17) | (static_cast<uint32_t>(MC >> 4) << 24);
+                                   (static_cast<uint32_t>(NT >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
         for (int st = 0; st < nst; ++st) {
             const int s = st % STAGES;
             SP_TS(st, 3);
@@ -192,16 +223,23 @@ __global__ void __launch_bounds__(THREADS, 1)
             SP_TS(st, 4);
             tc_fence_after();
             if (elect_one() && !(p.dbg & 2)) {
-                const uint32_t wa = smem_u32(sW + s * W_BYTES);
-                const uint32_t ecol = tmem + META_COL + 4 * s;
-                tmem_cp_128x128b(ecol, smem_desc(wa + A_BYTES, 2048, 128, 0));
                 const uint32_t ba = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    mma_sp(tmem, smem_desc(wa + 32 * j, 16, 512, 4), smem_desc(ba + 4096 * j, SLOTS * 128, 1024, 2),
-                           idesc | static_cast<uint32_t>(j), (st | j) ? 1u : 0u, ecol);
+                for (int h = 0; h < H; ++h) {
+                    const uint32_t wa = smem_u32(sW + s * W_BYTES + h * WH_BYTES);
+                    const uint32_t ecol = tmem + CF::META_COL + 4 * (H * s + h);
+                    tmem_cp_128x128b(ecol, smem_desc(wa + A_BYTES, 2048, 128, 0));
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        mma_sp(tmem + h * NT, smem_desc(wa + 32 * j, 16, 512, 4),
+                               smem_desc(ba + 4096 * j, SLOTS * 128, 1024, 2), idesc | static_cast<uint32_t>(j),
+                               (st | j) ? 1u : 0u, ecol);
+                }
             }
-            if (elect_one()) tc_commit(&empty[s]);
+            if (elect_one()) {
+                if (p.dbg & 128) mbar_arrive(&empty[s]);  // timing study: plain arrive instead of commit
+                else tc_commit(&empty[s]);
+            }
             __syncwarp();
             SP_TS(st, 5);
         }
@@ -211,42 +249,46 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (warp < GATHER_WARPS) {
         // ============ epilogue: TMEM lane = output column, TMEM column = token ============
-        const int qw = warp;
-        const int col = tile * MC + qw * 32 + lane;        // this lane's output column
-        const int pc = tile * MC + qw * 32 + (lane & ~1);  // column pair base
         const bool odd = lane & 1;
         mbar_wait(acc_full, 0);
         tc_fence_after();
-        for (int t0 = 0; t0 < NT; t0 += 32) {
-            uint32_t v[32];
-            if (nst > 0) {
-                tmem_ld32(tmem + (static_cast<uint32_t>(qw * 32) << 16) + t0, v);
-                tmem_wait_ld();
-            } else {
+#pragma unroll 1
+        for (int h = 0; h < H; ++h) {
+            const int qw = warp & 3;
+            const int col = tile * MC + h * 128 + qw * 32 + lane;        // this lane's output column
+            const int pc = tile * MC + h * 128 + qw * 32 + (lane & ~1);  // column pair base
+#pragma unroll 1
+            for (int t0 = (warp >> 2) * 32; t0 < NT; t0 += 32 * (GATHER_WARPS / 4)) {
+                uint32_t v[32];
+                if (nst > 0) {
+                    tmem_ld32(tmem + (static_cast<uint32_t>(qw * 32) << 16) + h * NT + t0, v);
+                    tmem_wait_ld();
+                } else {
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = 0u;
-            }
-            if (p.c_bf16) {
-                // lanes (2p, 2p+1) swap so each stores a bf16 pair (columns pc, pc+1): even lane token i, odd i+1
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const uint32_t x = odd ? v[i] : v[i + 1];
-                    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
-                    const float lo = __uint_as_float(odd ? y : v[i]);
-                    const float hi = __uint_as_float(odd ? v[i + 1] : y);
-                    const int t = m0 + t0 + i + (odd ? 1 : 0);
-                    if (t < p.m && pc < p.n && !(p.dbg & (8 | 64))) {
-                        __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
-                        *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.C) +
-                                                           static_cast<int64_t>(t) * p.n + pc) = h;
-                    }
+                    for (int i = 0; i < 32; ++i) v[i] = 0u;
                 }
-            } else {
+                if (p.c_bf16) {
+                    // lanes (2p, 2p+1) swap so each stores a bf16 pair (columns pc, pc+1): even lane token i, odd i+1
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int t = m0 + t0 + i;
-                    if (t < p.m && col < p.n && !(p.dbg & (8 | 64)))
-                        static_cast<float*>(p.C)[static_cast<int64_t>(t) * p.n + col] = __uint_as_float(v[i]);
+                    for (int i = 0; i < 32; i += 2) {
+                        const uint32_t x = odd ? v[i] : v[i + 1];
+                        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
+                        const float lo = __uint_as_float(odd ? y : v[i]);
+                        const float hi = __uint_as_float(odd ? v[i + 1] : y);
+                        const int t = m0 + t0 + i + (odd ? 1 : 0);
+                        if (t < p.m && pc < p.n && !(p.dbg & (8 | 64))) {
+                            __nv_bfloat162 hh = __floats2bfloat162_rn(lo, hi);
+                            *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.C) +
+                                                               static_cast<int64_t>(t) * p.n + pc) = hh;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const int t = m0 + t0 + i;
+                        if (t < p.m && col < p.n && !(p.dbg & (8 | 64)))
+                            static_cast<float*>(p.C)[static_cast<int64_t>(t) * p.n + col] = __uint_as_float(v[i]);
+                    }
                 }
             }
         }
@@ -299,8 +341,9 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ A, __nv_
 // so a tile needs at most 2 |U| + 4 slots.
 __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ slots, uint8_t* __restrict__ stype,
                                int* __restrict__ nstages, int* __restrict__ qbuf, int n, int k, int N, int M, int L,
-                               int smax) {
+                               int smax, int H) {
     const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+    const int MC = 128 * H;
     const int ntiles = (n + MC - 1) / MC;
     if (tile >= ntiles) return;
     const int q = n / L, G = MC / L, g0 = tile * G;
@@ -380,8 +423,9 @@ __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ 
 __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint8_t* __restrict__ D,
                                 const int* __restrict__ slots, const uint8_t* __restrict__ stype,
                                 const int* __restrict__ nstages, uint8_t* __restrict__ wimg, int n, int k, int N, int M,
-                                int L, int smax, int max_stages) {
+                                int L, int smax, int max_stages, int H) {
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int MC = 128 * H;
     const int r = static_cast<int>(gid % MC);
     const int64_t ts = gid / MC;
     const int st = static_cast<int>(ts % max_stages);
@@ -392,7 +436,8 @@ __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint
     const int j = tile * MC + r;
     const int g = j / L, gi = r / L;
     const bool live = j < n;
-    uint8_t* img = wimg + (static_cast<int64_t>(tile) * max_stages + st) * W_BYTES;
+    const int hf = r / 128;
+    uint8_t* img = wimg + ((static_cast<int64_t>(tile) * max_stages + st) * H + hf) * WH_BYTES;
     uint32_t* meta = reinterpret_cast<uint32_t*>(img + A_BYTES);
     const int* sl = slots + static_cast<int64_t>(tile) * smax + st * SLOTS;
     const uint8_t* ty = stype + static_cast<int64_t>(tile) * smax + st * SLOTS;
@@ -409,10 +454,10 @@ __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint
             pos[0] = pos[1];
             pos[1] = t;
         }
-        for (int h = 0; h < 2; ++h) {
+        for (int e = 0; e < 2; ++e) {
             __nv_bfloat16 v = __float2bfloat16(0.f);
-            const int kk = sl[4 * qd + pos[h]];
-            if (live && kk < k && ((ty[4 * qd + pos[h]] >> gi) & 1)) {
+            const int kk = sl[4 * qd + pos[e]];
+            if (live && kk < k && ((ty[4 * qd + pos[e]] >> gi) & 1)) {
                 const int t = kk / M, off = kk % M;
                 int lo = 0, hi = N - 1;  // D ascending within the window (R7)
                 while (lo < hi) {
@@ -422,14 +467,16 @@ __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint
                 }
                 v = Bv[static_cast<int64_t>(t * N + lo) * n + j];
             }
-            const int pidx = 2 * qd + h;  // compressed element of the row (0..31)
+            const int pidx = 2 * qd + e;  // compressed element of the row (0..31)
             const int b = 2 * pidx;
-            const int off = (r / 8) * 512 + (r % 8) * 64 + ((((b >> 4) ^ ((r % 8) >> 1)) & 3) << 4) + (b & 15);
+            const int rr = r % 128;
+            const int off = (rr / 8) * 512 + (rr % 8) * 64 + ((((b >> 4) ^ ((rr % 8) >> 1)) & 3) << 4) + (b & 15);
             *reinterpret_cast<__nv_bfloat16*>(img + off) = v;
         }
+        const int rr = r % 128;
         const int mma = qd / 8, c = qd % 8;
-        const int ln = (r % 8) + 8 * (c / 4) + 16 * (r / 16);
-        const int bit = 16 * ((r / 8) % 2) + 4 * (c % 4);
+        const int ln = (rr % 8) + 8 * (c / 4) + 16 * (rr / 16);
+        const int bit = 16 * ((rr / 8) % 2) + 4 * (c % 4);
         atomicOr(&meta[ln * 4 + mma], static_cast<uint32_t>(pos[0] | (pos[1] << 2)) << bit);
     }
 }
@@ -442,10 +489,11 @@ bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     return (L == 16 || L == 32 || L == 64 || L == 128) && n % 2 == 0 && k > 0 && k < (1 << 30) && M <= 256;
 }
 
-void tc_sp_sizes(int64_t n, int64_t k, size_t* off_slots, size_t* off_stype, size_t* off_nst, size_t* off_q,
+void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, size_t* off_slots, size_t* off_stype, size_t* off_nst, size_t* off_q,
                  size_t* off_img, size_t* total, int* smax, int* max_stages) {
     using namespace tcs;
-    const int64_t ntiles = (n + MC - 1) / MC;
+    const int H = sp_halves(L, N, M);
+    const int64_t ntiles = (n + 128 * H - 1) / (128 * H);
     const int64_t sm = ((2 * k + 4) + SLOTS - 1) / SLOTS * SLOTS;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     size_t o = 0;
@@ -458,7 +506,7 @@ void tc_sp_sizes(int64_t n, int64_t k, size_t* off_slots, size_t* off_stype, siz
     *off_q = o;
     o += al(static_cast<size_t>(ntiles * (k + 257)) * 4);
     *off_img = o;
-    o += static_cast<size_t>(ntiles * (sm / SLOTS)) * W_BYTES;
+    o += static_cast<size_t>(ntiles * (sm / SLOTS) * H) * WH_BYTES;
     *total = o;
     *smax = static_cast<int>(sm);
     *max_stages = static_cast<int>(sm / SLOTS);
@@ -469,30 +517,51 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
     using namespace tcs;
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
-    tc_sp_sizes(n, k, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    tc_sp_sizes(n, k, N, M, L, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
     uint8_t* b = static_cast<uint8_t*>(buf);
-    const int ntiles = static_cast<int>((n + MC - 1) / MC);
+    const int mc = 128 * sp_halves(L, N, M);
+    const int ntiles = static_cast<int>((n + mc - 1) / mc);
     NM_CUDA_TRY(cudaMemsetAsync(b + oi, 0, tot - oi, s));
     sp_pack_kernel<<<static_cast<unsigned>(ceil_div(ntiles, 32)), 32, 0, s>>>(
         D, reinterpret_cast<int*>(b + os), b + ot, reinterpret_cast<int*>(b + on), reinterpret_cast<int*>(b + oq),
-        static_cast<int>(n), static_cast<int>(k), N, M, L, smax);
+        static_cast<int>(n), static_cast<int>(k), N, M, L, smax, sp_halves(L, N, M));
     note_launch();
     NM_LAUNCH_CHECK("sp_pack_kernel");
-    const int64_t threads = static_cast<int64_t>(ntiles) * mst * MC;
+    const int64_t threads = static_cast<int64_t>(ntiles) * mst * mc;
     sp_image_kernel<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, s>>>(
         static_cast<const __nv_bfloat16*>(Bv), D, reinterpret_cast<const int*>(b + os), b + ot,
-        reinterpret_cast<const int*>(b + on), b + oi, static_cast<int>(n), static_cast<int>(k), N, M, L, smax, mst);
+        reinterpret_cast<const int*>(b + on), b + oi, static_cast<int>(n), static_cast<int>(k), N, M, L, smax, mst,
+        sp_halves(L, N, M));
     note_launch();
     NM_LAUNCH_CHECK("sp_image_kernel");
     return NM_OK;
 }
 
-nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k,
+template <int H>
+static nm_status sp_launch_h(const __nv_bfloat16* at, const tcs::Params& p, int64_t m, int64_t n, cudaStream_t s) {
+    using namespace tcs;
+    using CF = Cfg<H>;
+    static bool attr = false;
+    if (!attr) {
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         CF::SMEM_BYTES));
+        attr = true;
+    }
+    const dim3 grid(static_cast<unsigned>(ceil_div(m, CF::NT)), static_cast<unsigned>(ceil_div(n, CF::MC)));
+    prof_begin(s);
+    spmm_tc_sp_kernel<H><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, p);
+    prof_end(s);
+    note_launch();
+    NM_LAUNCH_CHECK("spmm_tc_sp_kernel");
+    return NM_OK;
+}
+
+nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M, int L,
                     cudaStream_t s) {
     using namespace tcs;
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
-    tc_sp_sizes(n, k, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    tc_sp_sizes(n, k, N, M, L, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
     const uint8_t* b = static_cast<const uint8_t*>(buf);
     const int64_t mp = (m + 7) / 8 * 8;
     __nv_bfloat16* at = nullptr;
@@ -502,13 +571,9 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
     transpose_bf16_kernel<<<tg, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(A), at, static_cast<int>(m),
                                              static_cast<int>(k), static_cast<int>(mp));
     note_launch();
-    NM_LAUNCH_CHECK("transpose_bf16_kernel");
-    {
-        static bool attr = false;
-        if (!attr) {
-            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
-            attr = true;
-        }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) st = cuda_fail(e, "transpose_bf16_kernel");
+    if (!st) {
         Params p{};
         p.wimg = b + oi;
         p.slots = reinterpret_cast<const int*>(b + os);
@@ -523,23 +588,17 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
         p.c_bf16 = c_bf16 ? 1 : 0;
         const char* dbg = std::getenv("NM_SP_DBG");
         p.dbg = dbg ? std::atoi(dbg) : 0;
-        const dim3 grid(static_cast<unsigned>(ceil_div(m, NT)), static_cast<unsigned>(ceil_div(n, MC)));
-        prof_begin(s);
-        spmm_tc_sp_kernel<<<grid, THREADS, SMEM_BYTES, s>>>(at, p);
-        prof_end(s);
-        note_launch();
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) st = cuda_fail(e, "spmm_tc_sp_kernel");
+        st = sp_halves(L, N, M) == 2 ? sp_launch_h<2>(at, p, m, n, s) : sp_launch_h<1>(at, p, m, n, s);
     }
-    const cudaError_t e = cudaFreeAsync(at, s);
+    e = cudaFreeAsync(at, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;
 }
 
-size_t tc_sp_prepack_bytes(int64_t n, int64_t k) {
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L) {
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
-    tc_sp_sizes(n, k, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    tc_sp_sizes(n, k, N, M, L, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
     return tot;
 }
 
@@ -547,10 +606,10 @@ size_t tc_sp_prepack_bytes(int64_t n, int64_t k) {
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                        int64_t k, int N, int M, int L, cudaStream_t s) {
     void* buf = nullptr;
-    nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k), s);
+    nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k, N, M, L), s);
     if (st) return st;
     st = tc_sp_prepack(Bv, D, n, k, N, M, L, buf, s);
-    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, s);
+    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, s);
     const cudaError_t e = cudaFreeAsync(buf, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;

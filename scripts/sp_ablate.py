@@ -13,10 +13,11 @@ PW = nmspmm.nm_prepack(W)
 C = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
 flops = 2.0 * m * n * (k // M * N)
 names = {0: "full", 1: "no gather", 2: "no MMA", 3: "no gather, no MMA", 8: "no C stores",
-         11: "no gather/MMA/stores", 16: "no weights", 27: "sync skeleton"}
+         11: "no gather/MMA/stores", 16: "no weights", 27: "sync skeleton", 155: "skeleton, arrive not commit",
+         131: "no gather/MMA, arrive"}
 lib = nmspmm.lib()
 import ctypes
-for dbg in [0, 1, 2, 3, 8, 11, 16, 27]:
+for dbg in [int(x) for x in os.environ.get('SP_DBGS', '0 1 2 3 8 11 16 27 155 131').split()]:
     os.environ["NM_SP_DBG"] = str(dbg)
     for _ in range(3):
         nmspmm.nm_spmm_prepacked(A, PW, out=C)
