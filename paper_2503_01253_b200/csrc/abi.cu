@@ -212,6 +212,7 @@ nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* 
                          int64_t k, int N, int M, int L, cudaStream_t s);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L);
+void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int* tokens);
 nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, void* buf,
                         cudaStream_t s);
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
@@ -492,15 +493,20 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
     } else if (kernel == K_TC_SP) {
         // tokens x output columns per CTA (MMA N x M per column half), 64 slots per stage
-        const int hh = (L >= 32 && 2 * N >= M) ? 2 : 1;  // spmm_tc_sp.cu sp_halves()
-        out->bm = hh == 2 ? 192 : 256;
+        int hh = 1, nt = 256;
+        tc_sp_geometry(m, n, N, M, L, &hh, &nt);
+        out->bm = nt;
         out->bn = 128 * hh;
         out->bk = 64;
         out->bkw = 32;
-        out->stages = 5;
         out->threads = 288;
         out->grid = static_cast<int32_t>(ceil_div(m, out->bm) * ceil_div(n, out->bn));
-        out->smem_bytes = 5 * (64 * out->bm * 2 + hh * (128 * 64 + 128 * 16)) + 1024 + 256;
+        {
+            const int per = 64 * ((nt + 63) / 64) * 128 + hh * (128 * 64 + 128 * 16);
+            const int st = std::min(8, (232448 - 1280) / per);
+            out->stages = st;
+            out->smem_bytes = st * per + 1280;
+        }
     } else if (kernel == K_TC_BF16) {
         int wp, bk, bkw, bkwp, bn;
         tc_bf16_geometry(N, M, L, &wp, &bk, &bkw, &bkwp, &bn);

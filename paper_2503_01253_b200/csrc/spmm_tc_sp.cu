@@ -12,7 +12,8 @@
 //     transposed once per call), one 512-B row (256 tokens) per warp-wide 16-B cp.async,
 //     written straight into the 128-B-swizzled MN-major layout the MMA reads.  (TMA
 //     tile::gather4 does the same with no SM instructions but measured ~80 clk per 4 rows
-//     per SM on B200 -- 6x slower than this kernel needs.)
+//     per SM on B200 -- 6x slower than this kernel needs; giving it a quarter or half of the
+//     rows beside the cp.async warps was slower too.)
 //   * Compressed weights + metadata are prepacked per (column tile, 64-slot stage) as the exact
 //     shared-memory images (one bulk copy each); metadata goes to TMEM by tcgen05.cp.
 // Roles: warps 0-3 gather (16 slot rows each per stage; warp 0 also bulk-copies the weight
@@ -35,7 +36,6 @@ using namespace nm::tc;
 // H = 2 (L >= 32): 256 columns x 192 tokens; H = 1 (L = 16, where 256 columns would be 16
 // groups): 128 columns x 256 tokens.
 constexpr int SLOTS = 64;                  // logical k slots per stage (2 MMAs of K = 32)
-constexpr int STAGES = 5;
 constexpr int A_BYTES = 128 * SLOTS;       // per half: 128 rows x 32 compressed bf16 (64 B rows, 64-B swizzle)
 constexpr int E_BYTES = 128 * 16;          // per half: metadata, 128 TMEM lanes x 16 B (columns 0, 1 used)
 constexpr int WH_BYTES = A_BYTES + E_BYTES;
@@ -45,27 +45,50 @@ constexpr int MMA_WARP = GATHER_WARPS;
 constexpr int THREADS = (GATHER_WARPS + 1) * 32;
 constexpr int TMEM_COLS = 512;
 
-template <int H>
+template <int H, int NT_>
 struct Cfg {
     static constexpr int MC = 128 * H;                    // output columns per CTA
-    static constexpr int NT = H == 2 ? 192 : 256;         // tokens per CTA (MMA N)
-    static constexpr int B_BYTES = SLOTS * NT * 2;        // NT/64 token atoms x 64 slot rows x 128 B
+    static constexpr int NT = NT_;                        // tokens per CTA (MMA N)
+    static constexpr int ATOMS = (NT + 63) / 64;
+    static constexpr int B_BYTES = SLOTS * ATOMS * 128;   // token atoms x 64 slot rows x 128 B
     static constexpr int W_BYTES = H * WH_BYTES;          // per (column tile, stage) weight image
-    static constexpr int SMEM_BYTES = STAGES * (W_BYTES + B_BYTES) + 1024 + 256;
+    static constexpr int ST0 = (232448 - 1024 - 256) / (W_BYTES + B_BYTES);
+    static constexpr int ST = ST0 > 8 ? 8 : ST0;          // pipeline stages (shared-memory bound)
+    static constexpr int SMEM_BYTES = ST * (W_BYTES + B_BYTES) + 1024 + 256;
     static constexpr int META_COL = H * NT;               // metadata ring: 4 H columns per stage
-    static_assert(META_COL + 4 * H * STAGES <= TMEM_COLS, "TMEM budget");
+    static_assert(NT % 16 == 0 && NT <= 256, "MMA N");
+    static_assert(META_COL + 4 * H * ST <= TMEM_COLS, "TMEM budget");
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
+// Tokens per CTA (MMA N); NM_SP_NT overrides (ablation).  H = 1: 256 (a full 512-B row per
+// warp-wide cp.async).  H = 2: the candidate minimising waves x stage time, with the stage times
+// measured on B200 at k = 4096: 160 / 192 / 224 tokens -> 1.03 / 1.00 / 1.07
+// (TMEM caps N at 224 with two accumulators), i.e. the fewest waves, 192 on ties.
+static int sp_tokens(int H, int64_t m, int64_t n) {
+    const char* e = std::getenv("NM_SP_NT");
+    if (e) return std::atoi(e);
+    if (H == 1) return 256;
+    const int64_t sms = num_sms(), col_tiles = (n + 255) / 256;
+    int best = 192;
+    int64_t best_cost = -1;
+    for (const int nt : {192, 160, 224}) {
+        const int64_t tiles = col_tiles * ((m + nt - 1) / nt);
+        const int64_t cost = ((tiles + sms - 1) / sms) * (nt == 192 ? 100 : nt == 160 ? 103 : 107);
+        if (best_cost < 0 || cost < best_cost) best_cost = cost, best = nt;
+    }
+    return best;
+}
+
 // Column halves per CTA (NM_SP_H=1/2 overrides, ablation).  H = 2 halves the gathered bytes per
 // MAC but packs 8 groups per slot sequence instead of 4; measured on B200 it wins
-// only at N/M >= 1/2 (the union is the whole window either way), and loses at 62.5-87.5 %
-// sparsity (8-group quads fill worse) -- so H = 2 iff L >= 32 and 2N >= M.
+// at N/M >= 1/4 and loses at 87.5 % sparsity, where the 8-group union (66 % of k) needs 1.6x the
+// slots of the 4-group one -- so H = 2 iff L >= 32 and 4N >= M.
 static int sp_halves(int L, int N, int M) {
     const char* e = std::getenv("NM_SP_H");
     if (e && e[0] == '1') return 1;
     if (e && e[0] == '2' && L >= 32) return 2;
-    return (L >= 32 && 2 * N >= M) ? 2 : 1;
+    return (L >= 32 && 4 * N >= M) ? 2 : 1;
 }
 
 struct Params {
@@ -80,6 +103,14 @@ struct Params {
 // 16-B global -> shared copy (L2 only); src_bytes = 0 zero-fills the destination
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+// predicated form (no branch around the copy)
+__device__ __forceinline__ void cp_async16_pred(uint32_t dst, const void* src, uint32_t src_bytes, bool on) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\t"
+        "@p cp.async.cg.shared.global [%0], [%1], 16, %2;\n\t}" ::"r"(dst),
+        "l"(src), "r"(src_bytes), "r"(static_cast<uint32_t>(on))
+        : "memory");
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -117,11 +148,11 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
             static_cast<long long*>(p.C)[(st) * 8 + (slot)] = clock64();                               \
     } while (0)
 
-template <int H>
+template <int H, int NT_>
 __global__ void __launch_bounds__(THREADS, 1)
     spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const Params p) {
-    using CF = Cfg<H>;
-    constexpr int NT = CF::NT, MC = CF::MC, B_BYTES = CF::B_BYTES, W_BYTES = CF::W_BYTES;
+    using CF = Cfg<H, NT_>;
+    constexpr int NT = CF::NT, MC = CF::MC, B_BYTES = CF::B_BYTES, W_BYTES = CF::W_BYTES, STAGES = CF::ST;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sB = smem;                               // STAGES x B_BYTES (1024-aligned: 128-B swizzle atoms)
@@ -162,12 +193,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         // Completion: cp.async.mbarrier.arrive.noinc per thread (no wait in the loop).
         const uint8_t* wsrc = p.wimg + static_cast<int64_t>(tile) * p.max_stages * W_BYTES;
         const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * ROWS_PER_WARP + (lane % ROWS_PER_WARP);
+        // per-lane constants: source = A^T row base + 2 (m0 + 8 lane) bytes (row k of A^T is a zero
+        // row, the padding slots' source); destination = stage + this lane's (atom, swizzled chunk)
+        // of each of the warp's rows -- row r % 8 = i because ROWS_PER_WARP = 8, so the XOR is static
+        static_assert(ROWS_PER_WARP == 8, "rows per warp = swizzle period");
         const int tok = m0 + 8 * lane;
         const bool lane_on = lane < NT / 8;
         const bool tok_ok = lane_on && tok < p.mp;
-        const __nv_bfloat16* src_base = At + (tok_ok ? tok : 0);
-        const uint32_t dst_lane = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128));
-        const uint32_t chunk = static_cast<uint32_t>(lane & 7);
+        const uint32_t srcsz = tok_ok ? 16u : 0u;
+        const char* src_base = reinterpret_cast<const char*>(At) + 2 * static_cast<int64_t>(tok_ok ? tok : 0);
+        const uint32_t pitch = static_cast<uint32_t>(p.mp) * 2u;
+        uint32_t dl[ROWS_PER_WARP];
+#pragma unroll
+        for (int i = 0; i < ROWS_PER_WARP; ++i)
+            dl[i] = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128) + (warp * ROWS_PER_WARP + i) * 128) +
+                    ((static_cast<uint32_t>(lane & 7) ^ static_cast<uint32_t>(i)) << 4);
         // slot rows are prefetched PF stages ahead in rotating registers (loop unrolled by PF): a
         // register is reloaded only after PF iterations, so the load latency (~1-2k clk under load)
         // is not paid per stage -- at PF = 4 it was, and it paced the whole pipeline
@@ -181,7 +221,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int st = st0 + u;
                 if (st >= nst) break;
                 const int s = st % STAGES;
-                const int kap = kq[u];
+                const uint32_t off = static_cast<uint32_t>(kq[u]) * pitch;  // byte offset of this lane's row
                 if (st + PF < nst) kq[u] = ssrc[(st + PF) * SLOTS];
                 if (warp == 0) SP_TS(st, 0);
                 if (st >= STAGES) mbar_wait(&empty[s], ((st / STAGES) - 1) & 1);
@@ -195,15 +235,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
                 if (!(p.dbg & 1)) {
-                    const uint32_t bstage = smem_u32(sB + s * B_BYTES) + dst_lane;
+                    const uint32_t bstage = smem_u32(sB + s * B_BYTES);
 #pragma unroll
                     for (int i = 0; i < ROWS_PER_WARP; ++i) {
-                        const int r = warp * ROWS_PER_WARP + i;  // row within the stage
-                        const int kr = __shfl_sync(0xffffffffu, kap, i);
-                        const uint32_t dst = bstage + static_cast<uint32_t>(r * 128) + ((chunk ^ (r & 7)) << 4);
-                        const bool ok = tok_ok && kr < p.k;
-                        if (lane_on)
-                            cp_async16(dst, src_base + (ok ? static_cast<int64_t>(kr) * p.mp : 0), ok ? 16u : 0u);
+                        const uint32_t o = __shfl_sync(0xffffffffu, off, i);
+                        cp_async16_pred(bstage + dl[i], src_base + o, srcsz, lane_on);
                     }
                 }
                 // arrives on full[s] once this thread's copies have landed (counts as one of the
@@ -212,7 +248,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (warp == 0) SP_TS(st, 2);
             }
         }
-    } else {
+    } else if (warp == MMA_WARP) {
         // ============ MMA issuer: per stage and half, metadata -> TMEM and two sparse MMAs ============
         constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
                                    (static_cast<uint32_t>(NT >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
@@ -250,8 +286,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp < GATHER_WARPS) {
         // ============ epilogue: TMEM lane = output column, TMEM column = token ============
         const bool odd = lane & 1;
+        if (warp == 0) SP_TS(nst, 6);
         mbar_wait(acc_full, 0);
         tc_fence_after();
+        if (warp == 0) SP_TS(nst, 7);
 #pragma unroll 1
         for (int h = 0; h < H; ++h) {
             const int qw = warp & 3;
@@ -293,6 +331,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         tc_fence_before();
+        if (warp == 0) SP_TS(nst, 0);
     }
     __syncthreads();
     if (warp == MMA_WARP) {
@@ -537,19 +576,19 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
     return NM_OK;
 }
 
-template <int H>
+template <int H, int NT>
 static nm_status sp_launch_h(const __nv_bfloat16* at, const tcs::Params& p, int64_t m, int64_t n, cudaStream_t s) {
     using namespace tcs;
-    using CF = Cfg<H>;
+    using CF = Cfg<H, NT>;
     static bool attr = false;
     if (!attr) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          CF::SMEM_BYTES));
         attr = true;
     }
     const dim3 grid(static_cast<unsigned>(ceil_div(m, CF::NT)), static_cast<unsigned>(ceil_div(n, CF::MC)));
     prof_begin(s);
-    spmm_tc_sp_kernel<H><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, p);
+    spmm_tc_sp_kernel<H, NT><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, p);
     prof_end(s);
     note_launch();
     NM_LAUNCH_CHECK("spmm_tc_sp_kernel");
@@ -565,8 +604,14 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
     const uint8_t* b = static_cast<const uint8_t*>(buf);
     const int64_t mp = (m + 7) / 8 * 8;
     __nv_bfloat16* at = nullptr;
-    nm_status st = scratch_alloc(reinterpret_cast<void**>(&at), static_cast<size_t>(k * mp) * 2, s);
+    // k + 1 rows: row k is zero, the source of the padding slots (kappa = k)
+    nm_status st = scratch_alloc(reinterpret_cast<void**>(&at), static_cast<size_t>((k + 1) * mp) * 2, s);
     if (st) return st;
+    if (static_cast<uint64_t>(k + 1) * static_cast<uint64_t>(mp) * 2u >= (1ull << 32)) {
+        cudaFreeAsync(at, s);
+        return fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: A^T larger than 4 GiB (32-bit row offsets)");
+    }
+    NM_CUDA_TRY(cudaMemsetAsync(at + k * mp, 0, static_cast<size_t>(mp) * 2, s));
     const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(mp, 64)));
     transpose_bf16_kernel<<<tg, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(A), at, static_cast<int>(m),
                                              static_cast<int>(k), static_cast<int>(mp));
@@ -588,11 +633,27 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
         p.c_bf16 = c_bf16 ? 1 : 0;
         const char* dbg = std::getenv("NM_SP_DBG");
         p.dbg = dbg ? std::atoi(dbg) : 0;
-        st = sp_halves(L, N, M) == 2 ? sp_launch_h<2>(at, p, m, n, s) : sp_launch_h<1>(at, p, m, n, s);
+
+        const int H = sp_halves(L, N, M), nt = sp_tokens(H, m, n);
+        switch (H * 1000 + nt) {
+            case 2192: st = sp_launch_h<2, 192>(at, p, m, n, s); break;
+            case 2128: st = sp_launch_h<2, 128>(at, p, m, n, s); break;
+            case 2160: st = sp_launch_h<2, 160>(at, p, m, n, s); break;
+            case 2224: st = sp_launch_h<2, 224>(at, p, m, n, s); break;
+            case 1256: st = sp_launch_h<1, 256>(at, p, m, n, s); break;
+            case 1128: st = sp_launch_h<1, 128>(at, p, m, n, s); break;
+            case 1192: st = sp_launch_h<1, 192>(at, p, m, n, s); break;
+            default: st = fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: unsupported (H, NT)");
+        }
     }
     e = cudaFreeAsync(at, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;
+}
+
+void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int* tokens) {
+    *halves = tcs::sp_halves(L, N, M);
+    *tokens = tcs::sp_tokens(*halves, m, n);
 }
 
 size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L) {

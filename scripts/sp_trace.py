@@ -9,20 +9,20 @@ A = torch.from_numpy(synth.uniform((m, k), 1, 1)).cuda().bfloat16()
 B = torch.from_numpy(synth.uniform((k, n), 2, 2)).cuda().bfloat16()
 W = nmspmm.nm_compress(B, N, M, L)
 PW = nmspmm.nm_prepack(W)
-for mask in [0, 27]:
+for mask in [int(x) for x in os.environ.get("SP_MASKS", "0 27").split()]:
     os.environ["NM_SP_DBG"] = str(64 | mask)
     C = torch.zeros(m, n, device="cuda", dtype=torch.bfloat16)
     for _ in range(2):
         nmspmm.nm_spmm_prepacked(A, PW, out=C)
     torch.cuda.synchronize()
-    ts = C.view(-1).view(torch.int64)[: 8 * 80].view(80, 8).cpu().tolist()
+    ts = C.view(-1).view(torch.int64)[: 8 * 100].view(100, 8).cpu().tolist()
     base = ts[0][0]
     print(f"mask {mask}")
     prev = None
     for st, r in enumerate(ts):
-        if r[0] == 0 and st > 0:
+        if r[0] == 0 and r[6] == 0 and st > 0:
             break
-        rel = [x - base if x else -1 for x in r[:6]]
+        rel = [x - base if x else -1 for x in r[:8]]
         d = (r[4] - prev) if prev else 0
         prev = r[4]
         print(st, rel, "mma-step", d)
