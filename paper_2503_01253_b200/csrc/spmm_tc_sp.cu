@@ -22,6 +22,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <cstring>
 
 #include "tcgen05.cuh"
 
@@ -97,6 +98,7 @@ struct Params {
     const int* nstages;    // [ntiles]
     void* C;
     int m, n, k, mp, smax, max_stages, c_bf16;
+    int tma_c;  // 1: C tile staged in shared memory and written by TMA stores (tmC valid)
     int dbg;  // NM_SP_DBG (timing studies only): 1 skip gathers, 2 skip MMAs, 8 skip C stores, 16 skip weights
 };
 
@@ -114,6 +116,17 @@ __device__ __forceinline__ void cp_async16_pred(uint32_t dst, const void* src, u
 }
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
 __device__ __forceinline__ void mma_sp(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc,
@@ -150,7 +163,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 template <int H, int NT_>
 __global__ void __launch_bounds__(THREADS, 1)
-    spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const Params p) {
+    spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const __grid_constant__ CUtensorMap tmC, const Params p) {
     using CF = Cfg<H, NT_>;
     constexpr int NT = CF::NT, MC = CF::MC, B_BYTES = CF::B_BYTES, W_BYTES = CF::W_BYTES, STAGES = CF::ST;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -290,9 +303,44 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(acc_full, 0);
         tc_fence_after();
         if (warp == 0) SP_TS(nst, 7);
+        const int qw = warp & 3;
+        if (p.tma_c) {
+            // staged: each 32-token chunk of the [NT][MC] C tile is assembled in the (now idle)
+            // stage ring, then one TMA tensor store writes it (clipped at m, n).  Warps 0-3 take
+            // the even chunks, 4-7 the odd ones; lane = column, so a warp's 32 stores per token row
+            // are 64 / 128 contiguous bytes.
+            const int eb = p.c_bf16 ? 2 : 4;
+            const int rowb = MC * eb;
+            const uint32_t tbase = tmem + (static_cast<uint32_t>(qw * 32) << 16);
+#pragma unroll 1
+            for (int t0 = (warp >> 2) * 32; t0 < NT; t0 += 64) {
+                uint8_t* buf = smem + (t0 / 32) * 32 * rowb;
+#pragma unroll 1
+                for (int h = 0; h < H; ++h) {
+                    uint32_t v[32];
+                    tmem_ld32(tbase + h * NT + t0, v);
+                    tmem_wait_ld();
+                    uint8_t* cb = buf + (h * 128 + qw * 32 + lane) * eb;
+                    if (p.c_bf16) {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            *reinterpret_cast<__nv_bfloat16*>(cb + i * rowb) = __float2bfloat16_rn(__uint_as_float(v[i]));
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) *reinterpret_cast<uint32_t*>(cb + i * rowb) = v[i];
+                    }
+                }
+                fence_proxy_async_smem();
+                named_bar_sync(1 + (warp >> 2), 128);
+                if (qw == 0 && lane == 0 && !(p.dbg & (8 | 64))) {
+                    tma_store_2d(&tmC, buf, tile * MC, m0 + t0);
+                    bulk_commit();
+                }
+            }
+            if (qw == 0 && lane == 0) bulk_wait_read0();
+        } else {
 #pragma unroll 1
         for (int h = 0; h < H; ++h) {
-            const int qw = warp & 3;
             const int col = tile * MC + h * 128 + qw * 32 + lane;        // this lane's output column
             const int pc = tile * MC + h * 128 + qw * 32 + (lane & ~1);  // column pair base
 #pragma unroll 1
@@ -329,6 +377,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     }
                 }
             }
+        }
         }
         tc_fence_before();
         if (warp == 0) SP_TS(nst, 0);
@@ -577,7 +626,7 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
 }
 
 template <int H, int NT>
-static nm_status sp_launch_h(const __nv_bfloat16* at, const tcs::Params& p, int64_t m, int64_t n, cudaStream_t s) {
+static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, int64_t n, cudaStream_t s) {
     using namespace tcs;
     using CF = Cfg<H, NT>;
     static bool attr = false;
@@ -586,9 +635,22 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, const tcs::Params& p, int6
                                          CF::SMEM_BYTES));
         attr = true;
     }
+    // C through TMA stores when its rows are 16-B aligned (the staged tile, NT/32 chunks of
+    // 32 x MC elements, must fit in the stage ring it reuses)
+    CUtensorMap tmC;
+    const int eb = p.c_bf16 ? 2 : 4;
+    p.tma_c = 0;
+    const char* te = std::getenv("NM_SP_TMA_C");
+    if (!(te && te[0] == '0') && (n * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
+        NT * CF::MC * eb <= CF::ST * (CF::B_BYTES + CF::W_BYTES)) {
+        if (make_tma_2d(&tmC, p.C, p.c_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, eb, m,
+                        n, 32, CF::MC, 0) == NM_OK)
+            p.tma_c = 1;
+    }
+    if (!p.tma_c) memset(&tmC, 0, sizeof(tmC));
     const dim3 grid(static_cast<unsigned>(ceil_div(m, CF::NT)), static_cast<unsigned>(ceil_div(n, CF::MC)));
     prof_begin(s);
-    spmm_tc_sp_kernel<H, NT><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, p);
+    spmm_tc_sp_kernel<H, NT><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, p);
     prof_end(s);
     note_launch();
     NM_LAUNCH_CHECK("spmm_tc_sp_kernel");
