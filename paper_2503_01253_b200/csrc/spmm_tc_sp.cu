@@ -63,9 +63,10 @@ struct Cfg {
 };
 
 // Tokens per CTA (MMA N); NM_SP_NT overrides (ablation).  H = 1: 256 (a full 512-B row per
-// warp-wide cp.async).  H = 2: the candidate minimising waves x stage time, with the stage times
-// measured on B200 at k = 4096: 160 / 192 / 224 tokens -> 1.03 / 1.00 / 1.07
-// (TMEM caps N at 224 with two accumulators), i.e. the fewest waves, 192 on ties.
+// warp-wide cp.async).  H = 2: the fewest waves of CTAs over the SMs, ties in the order
+// 192, 208, 176, 224, 160 -- measured on B200 (profiles/r01f_sp_nt_sweep.txt): at equal wave
+// counts the kernel time is flat within +-4 % in NT, 192 lowest (TMEM caps N at 224 with two
+// accumulators and the metadata ring).
 static int sp_tokens(int H, int64_t m, int64_t n) {
     const char* e = std::getenv("NM_SP_NT");
     if (e) return std::atoi(e);
@@ -73,9 +74,9 @@ static int sp_tokens(int H, int64_t m, int64_t n) {
     const int64_t sms = num_sms(), col_tiles = (n + 255) / 256;
     int best = 192;
     int64_t best_cost = -1;
-    for (const int nt : {192, 160, 224}) {
+    for (const int nt : {192, 208, 176, 224, 160}) {
         const int64_t tiles = col_tiles * ((m + nt - 1) / nt);
-        const int64_t cost = ((tiles + sms - 1) / sms) * (nt == 192 ? 100 : nt == 160 ? 103 : 107);
+        const int64_t cost = (tiles + sms - 1) / sms;
         if (best_cost < 0 || cost < best_cost) best_cost = cost, best = nt;
     }
     return best;
@@ -422,53 +423,45 @@ __global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ A, __nv_
 }
 
 // ------------------------------------------------------------------------- offline prepack
-// Slot packing for one column tile (one thread per tile; the paper's offline PreProcessing slot,
-// Listing 3).  Item = k row kept by at least one of the tile's G groups, type = G-bit
-// membership mask.  Greedy: fill each quad with the heaviest type that still fits (no group above
-// two rows per quad), ties to the type with the most items left.  Every quad takes >= 2 items,
-// so a tile needs at most 2 |U| + 4 slots.
-__global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ slots, uint8_t* __restrict__ stype,
-                               int* __restrict__ nstages, int* __restrict__ qbuf, int n, int k, int N, int M, int L,
-                               int smax, int H) {
-    const int tile = blockIdx.x * blockDim.x + threadIdx.x;
+// Slot packing (the paper's offline PreProcessing slot, Listing 3), one thread per
+// (column tile, k chunk of KC rows, KC a multiple of M): item = k row of the chunk kept by at
+// least one of the tile's G groups, type = G-bit membership mask.  Greedy: fill each quad with
+// the heaviest type that still fits (no group above two rows per quad), ties to the type with
+// the most items left.  Every quad takes >= 2 items, so a chunk needs at most 2 |U_c| + 4 slots.
+// Chunks pack independently (each ends with at most one partial quad) so the prepack runs on
+// tiles x chunks threads; sp_compact_kernel concatenates them.
+__host__ __device__ inline int sp_chunk_rows(int M) { return (512 + M - 1) / M * M; }
+
+__global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ tmp_slots,
+                               uint8_t* __restrict__ tmp_type, int* __restrict__ chunk_cnt, int* __restrict__ qbuf,
+                               int n, int k, int N, int M, int L, int H, int nchunks) {
+    const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int MC = 128 * H;
     const int ntiles = (n + MC - 1) / MC;
-    if (tile >= ntiles) return;
+    if (gid >= ntiles * nchunks) return;
+    const int tile = gid / nchunks, c = gid % nchunks;
+    const int KC = sp_chunk_rows(M);
+    const int r0 = c * KC, r1 = min(k, r0 + KC), rows = r1 - r0;
     const int q = n / L, G = MC / L, g0 = tile * G;
     const int gcount = min(G, q - g0);
     const int T = 1 << G;
-    int* qk = qbuf + static_cast<int64_t>(tile) * (k + 256 + 1);  // per-type queues of k rows ([k]) + counts
-    int* cnt = qk + k;                                             // [T <= 256]
-    // membership per k row, accumulated in the queue area first (as masks), then bucketed
-    for (int i = 0; i < k; ++i) qk[i] = 0;
-    const int windows = k / M;
+    int* qk = qbuf + static_cast<int64_t>(gid) * KC;                         // chunk rows, bucketed by type
+    int* sl = tmp_slots + static_cast<int64_t>(gid) * (2 * KC + 4);           // this chunk's slots
+    uint8_t* ty = tmp_type + static_cast<int64_t>(gid) * (2 * KC + 4);
+    // membership masks of the chunk's rows (kept in sl[] while bucketing)
+    for (int i = 0; i < rows; ++i) sl[i] = 0;
     for (int gi = 0; gi < gcount; ++gi)
-        for (int t = 0; t < windows; ++t)
-            for (int s = 0; s < N; ++s) {
-                const int off = D[static_cast<int64_t>(t * N + s) * q + g0 + gi];
-                qk[t * M + off] |= 1 << gi;
-            }
-    for (int t = 0; t < T; ++t) cnt[t] = 0;
-    for (int i = 0; i < k; ++i) cnt[qk[i]]++;
-    // bucket in place: start offsets per type, then a second array would be needed -- use the
-    // slot array of this tile as temporary storage for the masks
-    int* sl = slots + static_cast<int64_t>(tile) * smax;
-    uint8_t* ty = stype + static_cast<int64_t>(tile) * smax;
-    for (int i = 0; i < k; ++i) sl[i] = qk[i];
-    int start[257];
-    int acc = 0;
-    for (int t = 0; t < T; ++t) {
-        start[t] = acc;
-        acc += cnt[t];
-    }
-    start[T] = acc;
-    int fillp[256];
-    for (int t = 0; t < T; ++t) fillp[t] = start[t];
-    for (int i = 0; i < k; ++i) qk[fillp[sl[i]]++] = i;
-    int head[256];
+        for (int t = r0 / M; t < r1 / M; ++t)
+            for (int s = 0; s < N; ++s) sl[t * M + D[static_cast<int64_t>(t * N + s) * q + g0 + gi] - r0] |= 1 << gi;
+    int start[257], head[256];
+    for (int t = 0; t <= T; ++t) start[t] = 0;
+    for (int i = 0; i < rows; ++i) start[sl[i] + 1]++;
+    for (int t = 0; t < T; ++t) start[t + 1] += start[t];
     for (int t = 0; t < T; ++t) head[t] = start[t];
-    int remaining = k - cnt[0];
-    int ns = 0;  // slots written
+    for (int i = 0; i < rows; ++i) qk[head[sl[i]]++] = r0 + i;
+    for (int t = 0; t < T; ++t) head[t] = start[t];
+    int remaining = rows - (start[1] - start[0]);
+    int ns = 0;
     while (remaining > 0) {
         uint32_t once = 0, twice = 0;
         int placed = 0;
@@ -490,17 +483,38 @@ __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ 
             ++placed;
         }
         for (; placed < 4; ++placed) {
-            sl[ns] = k;  // padding slot: out-of-range row, TMA zero fill
+            sl[ns] = k;  // padding slot: the zero row k of A^T
             ty[ns] = 0;
             ++ns;
         }
     }
-    const int padded = (ns + SLOTS - 1) / SLOTS * SLOTS;
-    for (; ns < padded; ++ns) {
-        sl[ns] = k;
-        ty[ns] = 0;
+    chunk_cnt[gid] = ns;
+}
+
+// Concatenate a tile's chunk slot lists (one block per tile), pad to whole 64-slot stages.
+__global__ void sp_compact_kernel(const int* __restrict__ tmp_slots, const uint8_t* __restrict__ tmp_type,
+                                  const int* __restrict__ chunk_cnt, int* __restrict__ slots, uint8_t* __restrict__ stype,
+                                  int* __restrict__ nstages, int k, int M, int nchunks, int smax) {
+    const int tile = blockIdx.x;
+    const int KC = sp_chunk_rows(M);
+    int* sl = slots + static_cast<int64_t>(tile) * smax;
+    uint8_t* ty = stype + static_cast<int64_t>(tile) * smax;
+    int off = 0;
+    for (int c = 0; c < nchunks; ++c) {
+        const int gid = tile * nchunks + c;
+        const int cnt = chunk_cnt[gid];
+        for (int i = threadIdx.x; i < cnt; i += blockDim.x) {
+            sl[off + i] = tmp_slots[static_cast<int64_t>(gid) * (2 * KC + 4) + i];
+            ty[off + i] = tmp_type[static_cast<int64_t>(gid) * (2 * KC + 4) + i];
+        }
+        off += cnt;
     }
-    nstages[tile] = padded / SLOTS;
+    const int padded = (off + SLOTS - 1) / SLOTS * SLOTS;
+    for (int i = off + threadIdx.x; i < padded; i += blockDim.x) {
+        sl[i] = k;
+        ty[i] = 0;
+    }
+    if (threadIdx.x == 0) nstages[tile] = padded / SLOTS;
 }
 
 // Weight images: one thread per (tile, stage, output row r of the tile).  Per quad: the (<= 2)
@@ -577,12 +591,13 @@ bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     return (L == 16 || L == 32 || L == 64 || L == 128) && n % 2 == 0 && k > 0 && k < (1 << 30) && M <= 256;
 }
 
-void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, size_t* off_slots, size_t* off_stype, size_t* off_nst, size_t* off_q,
-                 size_t* off_img, size_t* total, int* smax, int* max_stages) {
+void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, size_t* off_slots, size_t* off_stype, size_t* off_nst,
+                 size_t* off_q, size_t* off_img, size_t* total, int* smax, int* max_stages) {
     using namespace tcs;
     const int H = sp_halves(L, N, M);
     const int64_t ntiles = (n + 128 * H - 1) / (128 * H);
-    const int64_t sm = ((2 * k + 4) + SLOTS - 1) / SLOTS * SLOTS;
+    const int64_t KC = sp_chunk_rows(M), nchunks = (k + KC - 1) / KC;
+    const int64_t sm = ((2 * k + 4 * nchunks) + SLOTS - 1) / SLOTS * SLOTS;  // >= sum of chunk bounds
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     size_t o = 0;
     *off_slots = o;
@@ -591,8 +606,10 @@ void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, size_t* off_slots, s
     o += al(static_cast<size_t>(ntiles * sm));
     *off_nst = o;
     o += al(static_cast<size_t>(ntiles) * 4);
-    *off_q = o;
-    o += al(static_cast<size_t>(ntiles * (k + 257)) * 4);
+    *off_q = o;  // pack scratch: bucketed rows, chunk slot lists + types, chunk counts
+    const int64_t units = ntiles * nchunks;
+    o += al(static_cast<size_t>(units * KC) * 4) + al(static_cast<size_t>(units * (2 * KC + 4)) * 5) +
+         al(static_cast<size_t>(units) * 4);
     *off_img = o;
     o += static_cast<size_t>(ntiles * (sm / SLOTS) * H) * WH_BYTES;
     *total = o;
@@ -610,11 +627,25 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
     const int mc = 128 * sp_halves(L, N, M);
     const int ntiles = static_cast<int>((n + mc - 1) / mc);
     NM_CUDA_TRY(cudaMemsetAsync(b + oi, 0, tot - oi, s));
-    sp_pack_kernel<<<static_cast<unsigned>(ceil_div(ntiles, 32)), 32, 0, s>>>(
-        D, reinterpret_cast<int*>(b + os), b + ot, reinterpret_cast<int*>(b + on), reinterpret_cast<int*>(b + oq),
-        static_cast<int>(n), static_cast<int>(k), N, M, L, smax, sp_halves(L, N, M));
+    const int KC = sp_chunk_rows(M), nchunks = static_cast<int>((k + KC - 1) / KC);
+    const int64_t units = static_cast<int64_t>(ntiles) * nchunks;
+    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
+    int* qk = reinterpret_cast<int*>(b + oq);
+    uint8_t* tsl = b + oq + al(static_cast<size_t>(units * KC) * 4);
+    uint8_t* tty = tsl + static_cast<size_t>(units * (2 * KC + 4)) * 4;
+    int* ccnt = reinterpret_cast<int*>(b + oq + al(static_cast<size_t>(units * KC) * 4) +
+                                       al(static_cast<size_t>(units * (2 * KC + 4)) * 5));
+    sp_pack_kernel<<<static_cast<unsigned>(ceil_div(units, 32)), 32, 0, s>>>(
+        D, reinterpret_cast<int*>(tsl), tty, ccnt, qk, static_cast<int>(n), static_cast<int>(k), N, M, L,
+        sp_halves(L, N, M), nchunks);
     note_launch();
     NM_LAUNCH_CHECK("sp_pack_kernel");
+    sp_compact_kernel<<<static_cast<unsigned>(ntiles), 256, 0, s>>>(reinterpret_cast<const int*>(tsl), tty, ccnt,
+                                                                   reinterpret_cast<int*>(b + os), b + ot,
+                                                                   reinterpret_cast<int*>(b + on),
+                                                                   static_cast<int>(k), M, nchunks, smax);
+    note_launch();
+    NM_LAUNCH_CHECK("sp_compact_kernel");
     const int64_t threads = static_cast<int64_t>(ntiles) * mst * mc;
     sp_image_kernel<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, s>>>(
         static_cast<const __nv_bfloat16*>(Bv), D, reinterpret_cast<const int*>(b + os), b + ot,
@@ -702,6 +733,8 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
             case 2128: st = sp_launch_h<2, 128>(at, p, m, n, s); break;
             case 2160: st = sp_launch_h<2, 160>(at, p, m, n, s); break;
             case 2224: st = sp_launch_h<2, 224>(at, p, m, n, s); break;
+            case 2176: st = sp_launch_h<2, 176>(at, p, m, n, s); break;
+            case 2208: st = sp_launch_h<2, 208>(at, p, m, n, s); break;
             case 1256: st = sp_launch_h<1, 256>(at, p, m, n, s); break;
             case 1128: st = sp_launch_h<1, 128>(at, p, m, n, s); break;
             case 1192: st = sp_launch_h<1, 192>(at, p, m, n, s); break;
