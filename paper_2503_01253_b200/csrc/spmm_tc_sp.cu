@@ -164,7 +164,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 template <int H, int NT_>
 __global__ void __launch_bounds__(THREADS, 1)
-    spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const __grid_constant__ CUtensorMap tmC, const Params p) {
+    spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const __grid_constant__ CUtensorMap tmC,
+                      const __grid_constant__ CUtensorMap tmC16, const Params p) {
     using CF = Cfg<H, NT_>;
     constexpr int NT = CF::NT, MC = CF::MC, B_BYTES = CF::B_BYTES, W_BYTES = CF::W_BYTES, STAGES = CF::ST;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -322,19 +323,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                     tmem_ld32(tbase + h * NT + t0, v);
                     tmem_wait_ld();
                     uint8_t* cb = buf + (h * 128 + qw * 32 + lane) * eb;
+                    // NT % 32 == 16 (176, 208 tokens): the last chunk holds 16 tokens of this tile
+                    const int rows = NT - t0 < 32 ? NT - t0 : 32;
                     if (p.c_bf16) {
 #pragma unroll
                         for (int i = 0; i < 32; ++i)
-                            *reinterpret_cast<__nv_bfloat16*>(cb + i * rowb) = __float2bfloat16_rn(__uint_as_float(v[i]));
+                            if (i < rows)
+                                *reinterpret_cast<__nv_bfloat16*>(cb + i * rowb) = __float2bfloat16_rn(__uint_as_float(v[i]));
                     } else {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) *reinterpret_cast<uint32_t*>(cb + i * rowb) = v[i];
+                        for (int i = 0; i < 32; ++i)
+                            if (i < rows) *reinterpret_cast<uint32_t*>(cb + i * rowb) = v[i];
                     }
                 }
                 fence_proxy_async_smem();
                 named_bar_sync(1 + (warp >> 2), 128);
                 if (qw == 0 && lane == 0 && !(p.dbg & (8 | 64))) {
-                    tma_store_2d(&tmC, buf, tile * MC, m0 + t0);
+                    tma_store_2d(NT - t0 < 32 ? &tmC16 : &tmC, buf, tile * MC, m0 + t0);
                     bulk_commit();
                 }
             }
@@ -362,8 +367,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const uint32_t y = __shfl_xor_sync(0xffffffffu, x, 1);
                         const float lo = __uint_as_float(odd ? y : v[i]);
                         const float hi = __uint_as_float(odd ? v[i + 1] : y);
-                        const int t = m0 + t0 + i + (odd ? 1 : 0);
-                        if (t < p.m && pc < p.n && !(p.dbg & (8 | 64))) {
+                        const int tl = t0 + i + (odd ? 1 : 0), t = m0 + tl;  // tl < NT: stay inside the tile
+                        if (tl < NT && t < p.m && pc < p.n && !(p.dbg & (8 | 64))) {
                             __nv_bfloat162 hh = __floats2bfloat162_rn(lo, hi);
                             *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.C) +
                                                                static_cast<int64_t>(t) * p.n + pc) = hh;
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int t = m0 + t0 + i;
-                        if (t < p.m && col < p.n && !(p.dbg & (8 | 64)))
+                        if (t0 + i < NT && t < p.m && col < p.n && !(p.dbg & (8 | 64)))
                             static_cast<float*>(p.C)[static_cast<int64_t>(t) * p.n + col] = __uint_as_float(v[i]);
                     }
                 }
@@ -668,20 +673,24 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
     }
     // C through TMA stores when its rows are 16-B aligned (the staged tile, NT/32 chunks of
     // 32 x MC elements, must fit in the stage ring it reuses)
-    CUtensorMap tmC;
+    CUtensorMap tmC, tmC16;
     const int eb = p.c_bf16 ? 2 : 4;
     p.tma_c = 0;
     const char* te = std::getenv("NM_SP_TMA_C");
     if (!(te && te[0] == '0') && (n * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
-        NT * CF::MC * eb <= CF::ST * (CF::B_BYTES + CF::W_BYTES)) {
-        if (make_tma_2d(&tmC, p.C, p.c_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, eb, m,
-                        n, 32, CF::MC, 0) == NM_OK)
+        (NT + 31) / 32 * 32 * CF::MC * eb <= CF::ST * (CF::B_BYTES + CF::W_BYTES)) {
+        const CUtensorMapDataType dt = p.c_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        if (make_tma_2d(&tmC, p.C, dt, eb, m, n, 32, CF::MC, 0) == NM_OK &&
+            make_tma_2d(&tmC16, p.C, dt, eb, m, n, 16, CF::MC, 0) == NM_OK)
             p.tma_c = 1;
     }
-    if (!p.tma_c) memset(&tmC, 0, sizeof(tmC));
+    if (!p.tma_c) {
+        memset(&tmC, 0, sizeof(tmC));
+        memset(&tmC16, 0, sizeof(tmC16));
+    }
     const dim3 grid(static_cast<unsigned>(ceil_div(m, CF::NT)), static_cast<unsigned>(ceil_div(n, CF::MC)));
     prof_begin(s);
-    spmm_tc_sp_kernel<H, NT><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, p);
+    spmm_tc_sp_kernel<H, NT><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
     prof_end(s);
     note_launch();
     NM_LAUNCH_CHECK("spmm_tc_sp_kernel");

@@ -420,3 +420,25 @@ def test_spmm_tc_sp_edges_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, 
     assert np.array_equal(C.astype(np.float64), ref)
     Cb = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.bfloat16).float().cpu().numpy()
     assert oracle.rel_frobenius(Cb, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("nt", ["160", "176", "192", "208", "224"])
+@pytest.mark.parametrize("cdt", [torch.bfloat16, torch.float32])
+def test_spmm_tc_sp_token_tiles_all_rows(nm, oracle, monkeypatch, nt, cdt):
+    """Every token-tile size the selector may pick, several token tiles deep, every row and column
+    checked: integer inputs make fp32 C exact and bf16 C its RNE (catches epilogue chunks that
+    spill into the next tile's rows)."""
+    use_tc_path(monkeypatch, "sp")
+    monkeypatch.setenv("NM_SP_NT", nt)
+    m, n, k, N, M, L = 650, 512, 256, 16, 32, 32
+    A = synth.integer((m, k), 111, synth.TID_A)
+    B = synth.integer((k, n), 112, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=cdt).float().cpu().numpy()
+    if cdt == torch.float32:
+        assert np.array_equal(C.astype(np.float64), ref)
+    else:
+        want = torch.from_numpy(ref.astype(np.float32)).bfloat16().float().numpy()
+        assert np.array_equal(C, want)
