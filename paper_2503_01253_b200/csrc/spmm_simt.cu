@@ -67,8 +67,8 @@ __device__ __forceinline__ int a_col_offset(int kk) {
 //      eight LDS.32 of column kabs.
 // PK:  (with AT) the paper's packing for high sparsity (Listing 3): only
 //      the dense columns some group of the tile selects (col_info) are
-//      fetched -- one 512-B bulk copy per needed A^T row, issued by warp 0's lanes --
-//      into consecutive panel rows, and the indices are remapped to packed
+//      fetched -- one 512-B A^T row per warp-wide cp.async, the rows spread over all
+//      warps -- into consecutive panel rows, and the indices are remapped to packed
 //      positions (reorderingIdx) by a popcount over the col_info mask.
 template <bool TWO, bool AT, bool PK>
 __global__ void __launch_bounds__(THREADS, 2)
@@ -101,7 +101,8 @@ __global__ void __launch_bounds__(THREADS, 2)
     if (tid == 0) {
         if (!PK) tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
-        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+        // packed mode: + one cp.async.mbarrier.arrive.noinc per thread (the gathered A^T rows)
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], PK ? 1 + THREADS : 1);
         fence_mbar_init();
     }
     if (PK)
@@ -115,21 +116,27 @@ __global__ void __launch_bounds__(THREADS, 2)
         const int s = (panel - p_begin) % STAGES;
         const int k0 = panel * p.bk, u0 = panel * p.bkw;
         if (PK) {
+            // every warp: the needed rows among dense columns [8 warp, 8 warp + 8) of the panel,
+            // one 512-B A^T row per warp-wide 16-B cp.async (the TMA bulk copy per row was the
+            // cost that made packing lose); thread 0 also fetches the B' panel
             const uint64_t mk = smask[panel];
-            if (lane == 0) {
-                mbar_arrive_expect_tx(&bars[s], static_cast<uint32_t>(__popcll(mk) * (BM * 4) + p.bkw * BN * 4));
+            if (tid == 0) {
+                mbar_arrive_expect_tx(&bars[s], static_cast<uint32_t>(p.bkw * BN * 4));
                 tma_load_2d(sB + s * B_STAGE_BYTES, &tmB, &bars[s], n0, u0);
             }
-            __syncwarp();
+            const uint32_t sa = smem_u32(sA + s * A_STAGE_BYTES) + 16u * static_cast<uint32_t>(lane);
+            const float* src = p.AT + static_cast<int64_t>(k0) * p.at_ld + m0 + 4 * lane;
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int b = lane + 32 * h;
+            for (int i = 0; i < 8; ++i) {
+                const int b = 8 * warp + i;
                 if ((mk >> b) & 1ull) {
                     const int pos = __popcll(mk & ((1ull << b) - 1ull));
-                    bulk_load(sA + s * A_STAGE_BYTES + pos * (BM * 4), p.AT + static_cast<int64_t>(k0 + b) * p.at_ld + m0,
-                              BM * 4, &bars[s]);
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa + pos * (BM * 4)),
+                                 "l"(src + static_cast<int64_t>(b) * p.at_ld)
+                                 : "memory");
                 }
             }
+            asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&bars[s])) : "memory");
             return;
         }
         mbar_arrive_expect_tx(&bars[s], stage_tx);
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         }
     };
 
-    if (PK ? warp == 0 : tid == 0) issue(p_begin);
+    if (PK || tid == 0) issue(p_begin);
     load_d(p_begin);
     store_d(p_begin);
     __syncthreads();
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 
     for (int panel = p_begin; panel < p_end; ++panel) {
         const int rel = panel - p_begin, s = rel % STAGES;
-        if ((PK ? warp == 0 : tid == 0) && panel + 1 < p_end) issue(panel + 1);  // freed by the last sync
+        if ((PK || tid == 0) && panel + 1 < p_end) issue(panel + 1);  // freed by the last sync
         if (panel + 1 < p_end) load_d(panel + 1);
         mbar_wait(&bars[s], (rel / STAGES) & 1);
 

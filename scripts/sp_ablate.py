@@ -14,7 +14,8 @@ C = torch.empty(m, n, device="cuda", dtype=torch.bfloat16)
 flops = 2.0 * m * n * (k // M * N)
 names = {0: "full", 1: "no gather", 2: "no MMA", 3: "no gather, no MMA", 8: "no C stores",
          11: "no gather/MMA/stores", 16: "no weights", 27: "sync skeleton", 155: "skeleton, arrive not commit",
-         131: "no gather/MMA, arrive"}
+         131: "no gather/MMA, arrive", 19: "no gather/MMA/weights", 147: "no g/MMA/w, arrive",
+         283: "skeleton, warp arrivals", 411: "skel, warp arr, plain empty"}
 lib = nmspmm.lib()
 import ctypes
 for dbg in [int(x) for x in os.environ.get('SP_DBGS', '0 1 2 3 8 11 16 27 155 131').split()]:
@@ -29,4 +30,4 @@ for dbg in [int(x) for x in os.environ.get('SP_DBGS', '0 1 2 3 8 11 16 27 155 13
     ms, cnt, la = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64()
     lib.nm_profile_end(ctypes.byref(ms), ctypes.byref(cnt), ctypes.byref(la))
     kms = ms.value / max(cnt.value, 1)
-    print(f"dbg={dbg} {names[dbg]:28s} kernel {kms*1e3:8.1f} us  {flops/kms/1e9:8.1f} TFLOP/s-equiv", flush=True)
+    print(f"dbg={dbg} {names.get(dbg, str(dbg)):28s} kernel {kms*1e3:8.1f} us  {flops/kms/1e9:8.1f} TFLOP/s-equiv", flush=True)
