@@ -75,8 +75,9 @@ static int sp_tokens(int H, int64_t m, int64_t n) {
     int best = 192;
     int64_t best_cost = -1;
     for (const int nt : {192, 208, 176, 224, 160}) {
-        const int64_t tiles = col_tiles * ((m + nt - 1) / nt);
-        const int64_t cost = (tiles + sms - 1) / sms;
+        const int64_t tiles = col_tiles * ((m + nt - 1) / nt), tail = tiles % sms;
+        // waves x 2; a tail that at most half fills the SMs is split in two (half a wave)
+        const int64_t cost = 2 * (tiles / sms) + (tail == 0 ? 0 : 2 * tail <= sms ? 1 : 2);
         if (best_cost < 0 || cost < best_cost) best_cost = cost, best = nt;
     }
     return best;
@@ -100,6 +101,10 @@ struct Params {
     void* C;
     int m, n, k, mp, smax, max_stages, c_bf16;
     int tma_c;  // 1: C tile staged in shared memory and written by TMA stores (tmC valid)
+    int n_tok;       // token tiles (1-D grid: token tile fastest)
+    int full_ctas;   // CTAs [0, full_ctas) do one whole tile; the rest split the tail tiles in two
+    float* ws;       // tail split: fp32 partial of part 1 per tail tile, [tail][NT][MC]
+    int* flags;      // tail split: flags[tail] = 1 once part 1's partial is in ws (zeroed per launch)
     int dbg;  // NM_SP_DBG (timing studies only): 1 skip gathers, 2 skip MMAs, 8 skip C stores, 16 skip weights
 };
 
@@ -155,6 +160,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
         : "memory");
 }
 
+__device__ __forceinline__ int ld_acquire(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
 // NM_SP_DBG & 64: CTA (0,0) records clock64 per stage into C (timing study only)
 #define SP_TS(st, slot)                                                                                \
     do {                                                                                               \
@@ -180,9 +194,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // token tiles vary fastest: the CTAs that share a column tile's weight stream run together,
     // so it is read from DRAM once and served from L2 to the others
-    const int tile = blockIdx.y;
-    const int m0 = blockIdx.x * NT;
-    const int nst = p.nstages[tile];
+    // 1-D grid, token tiles fastest (the CTAs that share a column tile's weight stream run
+    // together, so it is read from DRAM once and served from L2 to the others).  The last,
+    // partial wave's tiles are split in two stage ranges ("tail split"): part 1 leaves an fp32
+    // partial in ws, part 0 adds it in its epilogue (a + b: order-independent, deterministic).
+    int tid_lin = blockIdx.x, part = -1;
+    if (tid_lin >= p.full_ctas) {
+        part = (tid_lin - p.full_ctas) & 1;
+        tid_lin = p.full_ctas + ((tid_lin - p.full_ctas) >> 1);
+    }
+    const int tile = tid_lin / p.n_tok;
+    const int m0 = (tid_lin % p.n_tok) * NT;
+    const int nst_all = p.nstages[tile];
+    const int smid = (nst_all + 1) >> 1;
+    const int sa = part == 1 ? smid : 0, sb = part == 0 ? smid : nst_all;
+    const int nst = sb - sa;  // stages this CTA runs (ring index = st - sa)
+    const int tail_idx = tid_lin - p.full_ctas;
 
     if (warp == MMA_WARP) {
         if (lane == 0) {
@@ -229,15 +256,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         constexpr int PF = 16;
         int kq[PF];
 #pragma unroll
-        for (int u = 0; u < PF; ++u) kq[u] = u < nst ? ssrc[u * SLOTS] : 0;
+        for (int u = 0; u < PF; ++u) kq[u] = u < nst ? ssrc[(sa + u) * SLOTS] : 0;
         for (int st0 = 0; st0 < nst; st0 += PF) {
 #pragma unroll
             for (int u = 0; u < PF; ++u) {
-                const int st = st0 + u;
+                const int st = st0 + u;  // local stage (global stage sa + st)
                 if (st >= nst) break;
                 const int s = st % STAGES;
                 const uint32_t off = static_cast<uint32_t>(kq[u]) * pitch;  // byte offset of this lane's row
-                if (st + PF < nst) kq[u] = ssrc[(st + PF) * SLOTS];
+                if (st + PF < nst) kq[u] = ssrc[(sa + st + PF) * SLOTS];
                 if (warp == 0) SP_TS(st, 0);
                 if (st >= STAGES) mbar_wait(&empty[s], ((st / STAGES) - 1) & 1);
                 if (warp == 0) SP_TS(st, 1);
@@ -246,7 +273,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         mbar_arrive(&full[s]);
                     } else {
                         mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(W_BYTES));
-                        bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(st) * W_BYTES, W_BYTES, &full[s]);
+                        bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(sa + st) * W_BYTES, W_BYTES, &full[s]);
                     }
                 }
                 if (!(p.dbg & 1)) {
@@ -306,7 +333,44 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         if (warp == 0) SP_TS(nst, 7);
         const int qw = warp & 3;
-        if (p.tma_c) {
+        if (part == 1) {
+            // tail split, part 1: fp32 partial to ws[tail_idx] ([MC][NT], lane = column), then flag
+            float* w = p.ws + static_cast<int64_t>(tail_idx) * MC * NT;
+#pragma unroll 1
+            for (int h = 0; h < H; ++h)
+#pragma unroll 1
+                for (int t0 = (warp >> 2) * 32; t0 < NT; t0 += 64) {
+                    uint32_t v[32];
+                    if (nst > 0) {
+                        tmem_ld32(tmem + (static_cast<uint32_t>(qw * 32) << 16) + h * NT + t0, v);
+                        tmem_wait_ld();
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = 0u;
+                    }
+                    // ws is [NT][MC] (token-major): for each token the warp's 32 lanes write 128
+                    // contiguous bytes (a column-major layout scattered every store over 32 rows)
+                    const int nv = NT - t0 < 32 ? NT - t0 : 32;
+                    float* dst = w + static_cast<int64_t>(t0) * MC + h * 128 + qw * 32 + lane;
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < nv) dst[static_cast<int64_t>(i) * MC] = __uint_as_float(v[i]);
+                }
+            __threadfence();
+            named_bar_sync(1, 32 * GATHER_WARPS);
+            if (warp == 0 && lane == 0) st_release(p.flags + tail_idx, 1);
+        } else if (p.tma_c) {
+            if (part == 0) {  // tail split, part 0: part 1's partial must be in ws before it is added
+                if (warp == 0 && lane == 0)  // one poller with back-off (256 spinning threads per CTA
+                                             // measured 50 % slower: they load the L2 the others need)
+                    for (long long spin = 0; ld_acquire(p.flags + tail_idx) == 0; ++spin) {
+                        __nanosleep(256);
+                        if (spin > (1ll << 24)) __trap();  // a missing partial is a bug: fail, do not hang
+                    }
+                named_bar_sync(1, 32 * GATHER_WARPS);
+                __threadfence();
+            }
+            const float* wpart = part == 0 ? p.ws + static_cast<int64_t>(tail_idx) * MC * NT : nullptr;
             // staged: each 32-token chunk of the [NT][MC] C tile is assembled in the (now idle)
             // stage ring, then one TMA tensor store writes it (clipped at m, n).  Warps 0-3 take
             // the even chunks, 4-7 the odd ones; lane = column, so a warp's 32 stores per token row
@@ -320,8 +384,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
                 for (int h = 0; h < H; ++h) {
                     uint32_t v[32];
-                    tmem_ld32(tbase + h * NT + t0, v);
-                    tmem_wait_ld();
+                    if (nst > 0) {
+                        tmem_ld32(tbase + h * NT + t0, v);
+                        tmem_wait_ld();
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = 0u;
+                    }
+                    if (wpart) {
+                        const float* src = wpart + static_cast<int64_t>(t0) * MC + h * 128 + qw * 32 + lane;
+                        const int nv = NT - t0 < 32 ? NT - t0 : 32;
+#pragma unroll
+                        for (int i = 0; i < 32; ++i)
+                            if (i < nv) v[i] = __float_as_uint(__uint_as_float(v[i]) + src[static_cast<int64_t>(i) * MC]);
+                    }
                     uint8_t* cb = buf + (h * 128 + qw * 32 + lane) * eb;
                     // NT % 32 == 16 (176, 208 tokens): the last chunk holds 16 tokens of this tile
                     const int rows = NT - t0 < 32 ? NT - t0 : 32;
@@ -950,12 +1026,32 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
         memset(&tmC, 0, sizeof(tmC));
         memset(&tmC16, 0, sizeof(tmC16));
     }
-    const dim3 grid(static_cast<unsigned>(ceil_div(m, CF::NT)), static_cast<unsigned>(ceil_div(n, CF::MC)));
+    // tail split (NM_SP_TAIL=0 disables): the tiles of a partial last wave that at most half
+    // fills the SMs run as two half-range CTAs each
+    p.n_tok = static_cast<int>(ceil_div(m, CF::NT));
+    const int64_t tiles = ceil_div(n, CF::MC) * p.n_tok;
+    const int64_t sms = num_sms();
+    const int64_t tail = tiles % sms;
+    const char* te2 = std::getenv("NM_SP_TAIL");
+    const bool split = p.tma_c && !(te2 && te2[0] == '0') && tail > 0 && 2 * tail <= sms;
+    p.full_ctas = static_cast<int>(split ? tiles - tail : tiles);
+    p.ws = nullptr;
+    p.flags = nullptr;
+    if (split) {
+        nm_status st = scratch_alloc(reinterpret_cast<void**>(&p.ws), static_cast<size_t>(tail) * CF::MC * NT * 4, s);
+        if (!st) st = scratch_alloc(reinterpret_cast<void**>(&p.flags), static_cast<size_t>(tail) * 4, s);
+        if (st) return st;
+        NM_CUDA_TRY(cudaMemsetAsync(p.flags, 0, static_cast<size_t>(tail) * 4, s));
+    }
+    const unsigned grid = static_cast<unsigned>(split ? tiles + tail : tiles);
     prof_begin(s);
     spmm_tc_sp_kernel<H, NT><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
     prof_end(s);
     note_launch();
-    NM_LAUNCH_CHECK("spmm_tc_sp_kernel");
+    const cudaError_t e = cudaGetLastError();
+    if (p.ws) cudaFreeAsync(p.ws, s);
+    if (p.flags) cudaFreeAsync(p.flags, s);
+    if (e != cudaSuccess) return cuda_fail(e, "spmm_tc_sp_kernel");
     return NM_OK;
 }
 
