@@ -455,3 +455,18 @@ def test_spmm_tc_sp_pair_kernel_integer_exact(nm, oracle, monkeypatch, m, n, k, 
     W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
     C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
+
+
+@pytest.mark.parametrize("tail", ["0", "1"])
+@pytest.mark.parametrize("m,n,k,N,M,L", [(700, 768, 512, 16, 32, 32), (300, 640, 1024, 4, 32, 32)])
+def test_spmm_tc_sp_tail_split_on_off(nm, oracle, monkeypatch, tail, m, n, k, N, M, L):
+    """Small grids take the tail split (two half-range CTAs per tile, part 0 adds part 1's
+    partial); NM_SP_TAIL=0 runs one CTA per tile.  Both bit-exact on integer inputs."""
+    use_tc_path(monkeypatch, "sp")
+    monkeypatch.setenv("NM_SP_TAIL", tail)
+    A = synth.integer((m, k), 131, synth.TID_A)
+    B = synth.integer((k, n), 132, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
