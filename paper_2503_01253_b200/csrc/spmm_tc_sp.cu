@@ -192,8 +192,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // token tiles vary fastest: the CTAs that share a column tile's weight stream run together,
-    // so it is read from DRAM once and served from L2 to the others
+    unsigned long long t_start = 0;
+    if ((p.dbg & 256) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     // 1-D grid, token tiles fastest (the CTAs that share a column tile's weight stream run
     // together, so it is read from DRAM once and served from L2 to the others).  The last,
     // partial wave's tiles are split in two stage ranges ("tail split"): part 1 leaves an fp32
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
                 fence_proxy_async_smem();
                 named_bar_sync(1 + (warp >> 2), 128);
-                if (qw == 0 && lane == 0 && !(p.dbg & (8 | 64))) {
+                if (qw == 0 && lane == 0 && !(p.dbg & (8 | 64 | 256))) {
                     tma_store_2d(NT - t0 < 32 ? &tmC16 : &tmC, buf, tile * MC, m0 + t0);
                     bulk_commit();
                 }
@@ -468,6 +468,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == MMA_WARP) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
+    }
+    if ((p.dbg & 256) && threadIdx.x == 0) {  // timeline study: [start ns, end ns, smid, stages]
+        unsigned long long t_end;
+        uint32_t smid;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        long long* o = static_cast<long long*>(p.C) + 4 * static_cast<int64_t>(blockIdx.x);
+        o[0] = static_cast<long long>(t_start);
+        o[1] = static_cast<long long>(t_end);
+        o[2] = smid;
+        o[3] = nst;
     }
 }
 
