@@ -169,6 +169,29 @@ __device__ __forceinline__ void st_release(int* p, int v) {
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // NM_SP_DBG & 64: CTA (0,0) records clock64 per stage into C (timing study only)
 #define SP_TS(st, slot)                                                                                \
     do {                                                                                               \
@@ -176,7 +199,11 @@ __device__ __forceinline__ void st_release(int* p, int v) {
             static_cast<long long*>(p.C)[(st) * 8 + (slot)] = clock64();                               \
     } while (0)
 
-template <int H, int NT_>
+// MCAST: launched as clusters of 2 CTAs (adjacent token tiles of one column tile, identical stage
+// ranges); each CTA bulk-copies half of every weight image with .multicast::cluster into both,
+// and every MMA commit releases the stage in both CTAs (empty count 2): the weight stream's L2
+// traffic per SM halves.
+template <int H, int NT_, bool MCAST>
 __global__ void __launch_bounds__(THREADS, 1)
     spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const __grid_constant__ CUtensorMap tmC,
                       const __grid_constant__ CUtensorMap tmC16, const Params p) {
@@ -215,7 +242,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(&full[s], 1 + 32 * GATHER_WARPS);
-                mbar_init(&empty[s], 1);
+                mbar_init(&empty[s], MCAST ? 2 : 1);
             }
             mbar_init(acc_full, 1);
             fence_mbar_init();
@@ -224,9 +251,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_alloc(tmem_slot, TMEM_COLS);
     }
     tc_fence_before();
-    __syncthreads();
+    if (MCAST) cluster_sync_all();  // the peer's multicast copies / commits target these barriers
+    else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const uint32_t crank = MCAST ? cluster_rank() : 0u;
 
     if (warp < GATHER_WARPS) {
         // ============ gather: one slot row (NT tokens) per warp instruction ============
@@ -271,6 +300,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (warp == 0 && lane == 0) {
                     if (p.dbg & 16) {
                         mbar_arrive(&full[s]);
+                    } else if (MCAST) {
+                        // both halves land in both CTAs: expect all W_BYTES, copy (and multicast) ours
+                        constexpr uint32_t HALF_W = W_BYTES / 2;
+                        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(W_BYTES));
+                        bulk_load_mc(sW + s * W_BYTES + crank * HALF_W,
+                                     wsrc + static_cast<int64_t>(sa + st) * W_BYTES + crank * HALF_W, HALF_W, &full[s],
+                                     0x3);
                     } else {
                         mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(W_BYTES));
                         bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(sa + st) * W_BYTES, W_BYTES, &full[s]);
@@ -316,6 +352,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             if (elect_one()) {
                 if (p.dbg & 128) mbar_arrive(&empty[s]);  // timing study: plain arrive instead of commit
+                else if (MCAST) tc_commit_mc(&empty[s], 0x3);  // the stage is free once both CTAs are done
                 else tc_commit(&empty[s]);
             }
             __syncwarp();
@@ -464,7 +501,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_before();
         if (warp == 0) SP_TS(nst, 0);
     }
-    __syncthreads();
+    if (MCAST) cluster_sync_all();  // no multicast copy / commit may still target this CTA
+    else __syncthreads();
     if (warp == MMA_WARP) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
@@ -498,14 +536,6 @@ constexpr int P2_SMEM = P2_ST * (P2_B_BYTES + WH_BYTES) + 1024 + 256;
 static_assert(P2_SMEM <= 232448, "shared memory budget");
 static_assert(P2_NT * 128 * 4 <= P2_ST * (P2_B_BYTES + WH_BYTES), "fp32 C staging fits the ring");
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
     asm volatile(
         "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
@@ -1047,7 +1077,9 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
     using CF = Cfg<H, NT>;
     static bool attr = false;
     if (!attr) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         CF::SMEM_BYTES));
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          CF::SMEM_BYTES));
         attr = true;
     }
@@ -1070,12 +1102,17 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
     }
     // tail split (NM_SP_TAIL=0 disables): the tiles of a partial last wave that at most half
     // fills the SMs run as two half-range CTAs each
+    // weight multicast (NM_SP_MC=1): clusters of two adjacent token tiles (n_tok padded to even;
+    // a padding tile gathers zeros and stores nothing); no tail split
+    const char* mce = std::getenv("NM_SP_MC");
+    const bool mc = mce && mce[0] == '1';
     p.n_tok = static_cast<int>(ceil_div(m, CF::NT));
+    if (mc) p.n_tok += p.n_tok & 1;
     const int64_t tiles = ceil_div(n, CF::MC) * p.n_tok;
     const int64_t sms = num_sms();
     const int64_t tail = tiles % sms;
     const char* te2 = std::getenv("NM_SP_TAIL");
-    const bool split = p.tma_c && !(te2 && te2[0] == '0') && tail > 0 && 2 * tail <= sms;
+    const bool split = !mc && p.tma_c && !(te2 && te2[0] == '0') && tail > 0 && 2 * tail <= sms;
     p.full_ctas = static_cast<int>(split ? tiles - tail : tiles);
     p.ws = nullptr;
     p.flags = nullptr;
@@ -1087,7 +1124,23 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
     }
     const unsigned grid = static_cast<unsigned>(split ? tiles + tail : tiles);
     prof_begin(s);
-    spmm_tc_sp_kernel<H, NT><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
+    if (mc) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(THREADS);
+        lc.dynamicSmemBytes = CF::SMEM_BYTES;
+        lc.stream = s;
+        cudaLaunchAttribute la[1];
+        la[0].id = cudaLaunchAttributeClusterDimension;
+        la[0].val.clusterDim.x = 2;
+        la[0].val.clusterDim.y = 1;
+        la[0].val.clusterDim.z = 1;
+        lc.attrs = la;
+        lc.numAttrs = 1;
+        cudaLaunchKernelEx(&lc, spmm_tc_sp_kernel<H, NT, true>, at, tmC, tmC16, p);
+    } else {
+        spmm_tc_sp_kernel<H, NT, false><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
+    }
     prof_end(s);
     note_launch();
     const cudaError_t e = cudaGetLastError();
