@@ -41,7 +41,11 @@ class ShardedNmLinear:
     """y = x . B~ with B~'s column groups sharded over a process group (NCCL)."""
 
     def __init__(self, local_weight, n: int, group=None):
+        from . import nmspmm
         self.W = local_weight  # nmspmm.NmWeight of this rank's padded shard
+        # the offline weight prepack (P:470-475) once per layer: the bf16 sparse-tensor-core
+        # kernel's slot packing and images; plain values/idx for the fp32 path
+        self.PW = nmspmm.nm_prepack(local_weight) if local_weight.values.is_cuda else None
         self.group = group
         self.G = dist.get_world_size(group)
         self.n = n
@@ -65,6 +69,8 @@ class ShardedNmLinear:
 
     def local(self, A: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         from . import nmspmm
+        if self.PW is not None:
+            return nmspmm.nm_spmm_prepacked(A, self.PW, out=out)
         return nmspmm.nm_spmm(A, self.W, out=out)
 
     def __call__(self, A: torch.Tensor) -> torch.Tensor:
