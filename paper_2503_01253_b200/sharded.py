@@ -77,6 +77,8 @@ class ShardedNmLinear:
         from . import nmspmm
         m = A.shape[0]
         c_local = self.local(A)
+        if self.G == 1 and self.nr == self.n:  # a single shard is already C (no exchange step)
+            return c_local
         gathered = torch.empty((self.G, m, self.nr), dtype=c_local.dtype, device=A.device)
         dist.all_gather_into_tensor(gathered, c_local, group=self.group)
         C = torch.empty((m, self.n), dtype=c_local.dtype, device=A.device)
