@@ -445,15 +445,17 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     const int ntiles = ntiles_n * static_cast<int>(ceil_div(m, BM));
     const int resident = 2 * num_sms();  // 2 CTAs per SM (launch bounds, ~105 KB smem)
     const int rem = ntiles % resident;
-    // Measured on B200 (cfg2-cfg4): splitting the partial wave gains nothing -- CTAs do
-    // not retire in lock-step waves -- so it is off unless NM_SIMT_SPLIT asks for it.
+    // Measured on B200 (cfg2-cfg4): splitting the partial wave of a multi-wave grid gains
+    // nothing -- CTAs do not retire in lock-step waves -- so it is off there unless
+    // NM_SIMT_SPLIT asks for it.  A grid below one wave (e.g. a column shard of a multi-GPU
+    // layer) is split so that it fills the resident CTA slots (up to 4 parts per tile).
     int split = 1;
     const char* env_split = getenv("NM_SIMT_SPLIT");
     if (env_split) split = atoi(env_split);
+    else if (ntiles < resident) split = resident / ntiles;
     split = split > 4 ? 4 : split;
     if (split > p.npanels / 2) split = p.npanels / 2;
-    (void)rem;
-    if (split < 2 || ntiles < resident) split = 1;
+    if (split < 2) split = 1;
     p.split = split;
     p.full_tiles = split > 1 ? ntiles - rem : ntiles;
     float* ws = nullptr;
