@@ -123,11 +123,19 @@ nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, in
  *   idx    : w x q uint8 (must be valid; not re-checked on the hot path);
  *   C      : m x n, dtype c_dt, device, overwritten.
  *   ab_dt / c_dt / math:  NM_F32 + NM_MATH_F32_SIMT   -> fp32 FFMA, c_dt NM_F32
- *                         NM_F32 + NM_MATH_TF32_TC    -> tcgen05 tf32, c_dt NM_F32
- *                         NM_BF16 + NM_MATH_BF16_TC   -> tcgen05 bf16, c_dt NM_BF16 (RNE) or NM_F32
+ *                         NM_F32 + NM_MATH_TF32_TC    -> NM_ERR_UNSUPPORTED (not built)
+ *                         NM_BF16 + NM_MATH_BF16_TC   -> bf16 on the tensor cores, fp32 accumulate,
+ *                                                        c_dt NM_BF16 (RNE) or NM_F32: the sparse-
+ *                                                        tensor-core kernel (tcgen05.mma.sp over the
+ *                                                        offline slot packing) when L is 16/32/64/128,
+ *                                                        k % 8 == 0, A 16-B and C 4-B aligned; else
+ *                                                        the dense-MMA tcgen05 kernels or the generic one
  *                         NM_MATH_AUTO                -> selector (nm_plan_query)
- * Each C element is accumulated inside one CTA in a fixed order (no split-K,
- * no atomics): results are bit-reproducible run to run (R13).
+ * bf16 without nm_prepack re-packs the weight on every call (ms); use
+ * nm_prepack / nm_spmm_prepacked for repeated products with one weight.
+ * No atomics on data: where a tile's k range is split over CTAs (fp32: grids below
+ * one wave; bf16: the partial last wave) the partials are added in a fixed order,
+ * so results are bit-reproducible run to run (R13).
  * m == 0 or n == 0 is a no-op returning NM_OK.  Asynchronous.
  */
 nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
