@@ -772,37 +772,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 }
 
 // A (m x k bf16, row-major) -> At (k x mp, mp = m rounded up to 8): 64 x 64 tiles through shared memory.
-__global__ void transpose_bf16_kernel(const __nv_bfloat16* __restrict__ A, __nv_bfloat16* __restrict__ At, int m,
-                                      int k, int mp) {
-    __shared__ __nv_bfloat16 t[64][66];
+__global__ void __launch_bounds__(256) transpose_bf16_kernel(const __nv_bfloat16* __restrict__ A,
+                                                            __nv_bfloat16* __restrict__ At, int m, int k, int mp) {
+    // 64 tokens x 64 k per block.  Token pairs (2p, 2p+1) travel as one 32-bit word: a thread
+    // loads 8 k of rows 2p and 2p+1 (two 16-B loads; a warp covers 4 pairs x 128 B: coalesced),
+    // PRMT builds the 8 (row 2p, row 2p+1) words, 8 smem stores (columns XOR-swizzled by 4 (k/8)
+    // words: conflict-free); the output side reads 16 B (8 tokens) of a k row per LDS.128 and
+    // writes it with one 16-B store.
+    __shared__ __align__(16) uint32_t t2[64][36];  // [k][token pair], rows padded to 144 B
     const int k0 = blockIdx.x * 64, r0 = blockIdx.y * 64;
-    const int tid = threadIdx.x;  // 256 threads
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (blockIdx.x == 0 && blockIdx.y == 0)  // row k: the zero row the padding slots read
         for (int c = tid * 8; c < mp; c += 256 * 8)
             *reinterpret_cast<uint4*>(At + static_cast<int64_t>(k) * mp + c) = make_uint4(0, 0, 0, 0);
-    // load: 64 rows x 8 chunks of 8 k (16 B)
+    {
+        const int c = lane & 7, p = 4 * warp + (lane >> 3);  // 8-k chunk, token pair
+        const int r = r0 + 2 * p, kc = k0 + 8 * c;
+        uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
+        if (kc < k) {
+            if (r < m) x = *reinterpret_cast<const uint4*>(A + static_cast<int64_t>(r) * k + kc);
+            if (r + 1 < m) y = *reinterpret_cast<const uint4*>(A + static_cast<int64_t>(r + 1) * k + kc);
+        }
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w}, ys[4] = {y.x, y.y, y.z, y.w};
+        const int col = p ^ (4 * c);
 #pragma unroll
-    for (int it = 0; it < 2; ++it) {
-        const int e = tid + it * 256;
-        const int r = e >> 3, c = (e & 7) * 8;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (r0 + r < m && k0 + c < k) v = *reinterpret_cast<const uint4*>(A + static_cast<int64_t>(r0 + r) * k + k0 + c);
-        const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&v);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) t[r][c + j] = h[j];
+        for (int i = 0; i < 4; ++i) {
+            uint32_t lo, hi;
+            asm("prmt.b32 %0, %1, %2, 0x5410;" : "=r"(lo) : "r"(xs[i]), "r"(ys[i]));
+            asm("prmt.b32 %0, %1, %2, 0x7632;" : "=r"(hi) : "r"(xs[i]), "r"(ys[i]));
+            t2[8 * c + 2 * i][col] = lo;
+            t2[8 * c + 2 * i + 1][col] = hi;
+        }
     }
     __syncthreads();
-    // store: 64 k rows x 8 chunks of 8 tokens
 #pragma unroll
     for (int it = 0; it < 2; ++it) {
         const int e = tid + it * 256;
-        const int kr = e >> 3, c = (e & 7) * 8;
-        if (k0 + kr < k && r0 + c < mp) {
-            __align__(16) __nv_bfloat16 h[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) h[j] = t[c + j][kr];
-            *reinterpret_cast<uint4*>(At + static_cast<int64_t>(k0 + kr) * mp + r0 + c) = *reinterpret_cast<uint4*>(h);
-        }
+        const int kr = e >> 3, q = e & 7;  // k row, 8-token chunk
+        if (k0 + kr < k && r0 + 8 * q < mp)
+            *reinterpret_cast<uint4*>(At + static_cast<int64_t>(k0 + kr) * mp + r0 + 8 * q) =
+                *reinterpret_cast<const uint4*>(&t2[kr][(4 * q) ^ (4 * ((kr >> 3) & 7))]);
     }
 }
 
