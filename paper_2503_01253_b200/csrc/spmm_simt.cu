@@ -332,17 +332,33 @@ void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw) {
 }
 
 // A (m x k) -> A^T (k x m): 32x32 tiles through padded shared memory, coalesced both ways.
-__global__ void transpose_kernel(const float* __restrict__ A, float* __restrict__ AT, int m, int k, int ld) {
-    __shared__ float t[32][33];
-    const int k0 = blockIdx.x * 32, m0 = blockIdx.y * 32;
-    for (int r = threadIdx.y; r < 32; r += 8) {
-        const int i = m0 + r, j = k0 + threadIdx.x;
-        if (i < m && j < k) t[r][threadIdx.x] = A[static_cast<int64_t>(i) * k + j];
+__global__ void __launch_bounds__(256) transpose_kernel(const float* __restrict__ A, float* __restrict__ AT, int m,
+                                                       int k, int ld) {
+    // 64 x 64 tile, 16-B global accesses on both sides (a warp moves 2 x 256 contiguous bytes);
+    // smem rows padded to 65 floats: the 4-token column reads are conflict-free.  k % 4 == 0
+    // (SIMT applicability); tokens >= m are written as zeros (never read back into C).
+    __shared__ float t[64][65];
+    const int k0 = blockIdx.x * 64, m0 = blockIdx.y * 64;
+    const int tid = threadIdx.x;
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int e = tid + it * 256;
+        const int r = e >> 4, c4 = (e & 15) * 4;
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (m0 + r < m && k0 + c4 < k) v = *reinterpret_cast<const float4*>(A + static_cast<int64_t>(m0 + r) * k + k0 + c4);
+        t[r][c4] = v.x;
+        t[r][c4 + 1] = v.y;
+        t[r][c4 + 2] = v.z;
+        t[r][c4 + 3] = v.w;
     }
     __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += 8) {
-        const int j = k0 + r, i = m0 + threadIdx.x;
-        if (i < m && j < k) AT[static_cast<int64_t>(j) * ld + i] = t[threadIdx.x][r];
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+        const int e = tid + it * 256;
+        const int kr = e >> 4, q4 = (e & 15) * 4;
+        if (k0 + kr < k && m0 + q4 < ld)
+            *reinterpret_cast<float4*>(AT + static_cast<int64_t>(k0 + kr) * ld + m0 + q4) =
+                make_float4(t[q4][kr], t[q4 + 1][kr], t[q4 + 2][kr], t[q4 + 3][kr]);
     }
 }
 
@@ -420,8 +436,8 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     if (use_at) {
         st = scratch_alloc(reinterpret_cast<void**>(&AT), static_cast<size_t>(k) * p.at_ld * sizeof(float), s);
         if (st) return st;
-        const dim3 tg(static_cast<unsigned>(ceil_div(k, 32)), static_cast<unsigned>(ceil_div(m, 32)));
-        transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, AT, static_cast<int>(m), static_cast<int>(k), p.at_ld);
+        const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(p.at_ld, 64)));
+        transpose_kernel<<<tg, 256, 0, s>>>(A, AT, static_cast<int>(m), static_cast<int>(k), p.at_ld);
         note_launch();
         NM_LAUNCH_CHECK("transpose_kernel");
         p.AT = AT;

@@ -233,8 +233,8 @@ nm_status simt_pipe_launch(const float* A, const float* Bv, const uint8_t* D, fl
     if (st) return st;
     st = scratch_alloc(reinterpret_cast<void**>(&tbl), static_cast<size_t>(ntiles_n) * p.npanels * p.tbl_bytes, s);
     if (st) return st;
-    const dim3 tg(static_cast<unsigned>(ceil_div(k, 32)), static_cast<unsigned>(ceil_div(m, 32)));
-    transpose_kernel<<<tg, dim3(32, 8), 0, s>>>(A, AT, static_cast<int>(m), static_cast<int>(k), at_ld);
+    const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(at_ld, 64)));
+    transpose_kernel<<<tg, 256, 0, s>>>(A, AT, static_cast<int>(m), static_cast<int>(k), at_ld);
     note_launch();
     NM_LAUNCH_CHECK("transpose_kernel");
     build_simt_table_kernel<<<dim3(p.npanels, ntiles_n), 256, 0, s>>>(D, tbl, p.q, N, M, L, p.bkw, p.npanels, p.slots,
