@@ -553,13 +553,6 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
             : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
 }
-__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint64_t* bar, uint32_t cta) {
-    asm volatile(
-        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
-        "mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
-        "r"(cta)
-        : "memory");
-}
 __device__ __forceinline__ void mma_sp2(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc,
                                         uint32_t emeta) {
     asm volatile(
@@ -608,7 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (warp == MMA_WARP) {
         if (lane == 0) {
             for (int s = 0; s < STAGES; ++s) {
-                mbar_init(&full[s], 1 + ((p.dbg & 256) ? GATHER_WARPS : 32 * GATHER_WARPS) + (leader ? 1 : 0));
+                mbar_init(&full[s], 1 + 32 * GATHER_WARPS + (leader ? 1 : 0));  // + the peer's relay
                 mbar_init(&empty[s], 1);
             }
             mbar_init(acc_full, 1);
@@ -673,12 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         cp_async16(bstage + dl[i], src_base + o, srcsz);
                     }
                 }
-                if (p.dbg & 256) {  // timing study (no gathers): one plain arrive per warp
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&full[s]);
-                } else {
-                    cp_async_arrive_noinc(&full[s]);
-                }
+                cp_async_arrive_noinc(&full[s]);
                 if (warp == 0) TS2(st, 2);
             }
         }
@@ -688,8 +676,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                    (static_cast<uint32_t>(P2_NT >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
         for (int st = 0; st < nst; ++st) {
             const int s = st % STAGES;
-            if (p.dbg & 1024) mbar_wait(&full[s], (st / STAGES) & 1);
-            else mbar_wait_cluster(&full[s], (st / STAGES) & 1);
+            mbar_wait_cluster(&full[s], (st / STAGES) & 1);
             TS2(st, 3);
             tc_fence_after();
             if (elect_one() && !(p.dbg & 2)) {
@@ -722,9 +709,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             mbar_wait(&full[s], (st / STAGES) & 1);
             TS2(st, 5);
             if (lane == 0) {
-                if (p.dbg & 32) fence_proxy_async_smem();  // ablation: the proxy fence is not needed
-                if (p.dbg & 512) mbar_arrive_remote_relaxed(&full[s], 0);
-                else mbar_arrive_remote(&full[s], 0);
+                mbar_arrive_remote(&full[s], 0);
             }
             __syncwarp();
         }
