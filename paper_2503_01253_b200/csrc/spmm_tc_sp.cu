@@ -105,7 +105,8 @@ struct Params {
     int full_ctas;   // CTAs [0, full_ctas) do one whole tile; the rest split the tail tiles in two
     float* ws;       // tail split: fp32 partial of part 1 per tail tile, [tail][NT][MC]
     int* flags;      // tail split: flags[tail] = 1 once part 1's partial is in ws (zeroed per launch)
-    int dbg;  // NM_SP_DBG (timing studies only): 1 skip gathers, 2 skip MMAs, 8 skip C stores, 16 skip weights
+    int dbg;  // NM_SP_DBG (timing studies only): 1 skip gathers, 2 skip MMAs, 8 skip C stores, 16 skip weights,
+              // 64 per-stage clock64 trace, 128 plain arrive for commits (no MMA), 256 per-CTA timeline
 };
 
 // 16-B global -> shared copy (L2 only); src_bytes = 0 zero-fills the destination
