@@ -521,242 +521,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-// ====================================================================================================
-// spmm_tc_sp2_kernel: the same slot-packed sparse contraction on a CTA pair (cluster of 2,
-// tcgen05.mma.sp.cta_group::2, M = 256 output columns = the two 128-column halves of an H = 2 tile,
-// N = 256 tokens).  Each CTA stages its own weight half and gathers its own 128 tokens of every slot
-// row (two rows per warp instruction); the pair's MMA reads both CTAs' operands, so every SM moves
-// half the shared-memory bytes per MAC of the one-CTA, two-accumulator kernel.  The leader (rank 0)
-// issues the MMAs; the peer's stage readiness reaches the leader's full barrier through a relay
-// arrive (cp.async completions can only arrive on a CTA-local barrier).
-// ====================================================================================================
-constexpr int P2_NT = 256;                         // tokens per pair (128 per CTA)
-constexpr int P2_B_BYTES = SLOTS * 2 * 128;        // 2 token atoms x 64 slot rows x 128 B = 16 KB
-constexpr int P2_ST = 8;
-constexpr int P2_SMEM = P2_ST * (P2_B_BYTES + WH_BYTES) + 1024 + 256;
-static_assert(P2_SMEM <= 232448, "shared memory budget");
-static_assert(P2_NT * 128 * 4 <= P2_ST * (P2_B_BYTES + WH_BYTES), "fp32 C staging fits the ring");
-
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
-    asm volatile(
-        "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
-        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
-        "r"(cta)
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok)
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-}
-__device__ __forceinline__ void mma_sp2(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc,
-                                        uint32_t emeta) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.sp.cta_group::2.kind::f16 [%0], %1, %2, [%5], %3, {%6, %6, %6, %6, %6, %6, %6, %6}, p;\n\t}" ::"r"(d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(emeta), "r"(0u)
-        : "memory");
-}
-__device__ __forceinline__ void tmem_cp2_128x128b(uint32_t taddr, uint64_t sdesc) {
-    asm volatile("tcgen05.cp.cta_group::2.128x128b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
-}
-__device__ __forceinline__ void tc_commit2_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"(mask)
-        : "memory");
-}
-
-// NM_SP_DBG & 64: cluster (0,0) records clock64 per stage (leader slots 0-5, peer 8-13) into C
-#define TS2(st, slot)                                                                                  \
-    do {                                                                                               \
-        if ((p.dbg & 64) && blockIdx.x < 2 && blockIdx.y == 0 && lane == 0)                            \
-            static_cast<long long*>(p.C)[(st) * 16 + (slot) + 8 * blockIdx.x] = clock64();             \
-    } while (0)
-
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    spmm_tc_sp2_kernel(const __nv_bfloat16* __restrict__ At, const __grid_constant__ CUtensorMap tmC, const Params p) {
-    constexpr int STAGES = P2_ST, B_BYTES = P2_B_BYTES, W_BYTES = WH_BYTES;
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* sB = smem;
-    uint8_t* sW = smem + STAGES * B_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sW + STAGES * W_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* acc_full = empty + STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_rank();
-    const bool leader = rank == 0;
-    const int tile = blockIdx.y;                              // 256-column tile (H = 2 prepack)
-    const int m0 = (blockIdx.x >> 1) * P2_NT;                 // the pair's token tile
-    const int nst = p.nstages[tile];
-
-    if (warp == MMA_WARP) {
-        if (lane == 0) {
-            for (int s = 0; s < STAGES; ++s) {
-                mbar_init(&full[s], 1 + 32 * GATHER_WARPS + (leader ? 1 : 0));  // + the peer's relay
-                mbar_init(&empty[s], 1);
-            }
-            mbar_init(acc_full, 1);
-            fence_mbar_init();
-        }
-        __syncwarp();
-        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                     "r"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp < GATHER_WARPS) {
-        // ============ gather: this CTA's 128 tokens of each slot row; two rows per warp instruction ============
-        const int half = lane >> 4, l16 = lane & 15;
-        const int tok = m0 + 128 * static_cast<int>(rank) + 8 * l16;
-        const bool tok_ok = tok < p.mp;
-        const uint32_t srcsz = tok_ok ? 16u : 0u;
-        const char* src_base = reinterpret_cast<const char*>(At) + 2 * static_cast<int64_t>(tok_ok ? tok : 0);
-        const uint32_t pitch = static_cast<uint32_t>(p.mp) * 2u;
-        uint32_t dl[ROWS_PER_WARP / 2];
-#pragma unroll
-        for (int i = 0; i < ROWS_PER_WARP / 2; ++i) {
-            const int r = warp * ROWS_PER_WARP + 2 * i + half;
-            dl[i] = static_cast<uint32_t>((l16 >> 3) * (SLOTS * 128) + r * 128) +
-                    ((static_cast<uint32_t>(l16 & 7) ^ static_cast<uint32_t>(r & 7)) << 4);
-        }
-        const uint8_t* wsrc = p.wimg + static_cast<int64_t>(tile) * p.max_stages * 2 * WH_BYTES + rank * WH_BYTES;
-        const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * ROWS_PER_WARP + (lane % ROWS_PER_WARP);
-        constexpr int PF = 16;
-        int kq[PF];
-#pragma unroll
-        for (int v = 0; v < PF; ++v) kq[v] = v < nst ? ssrc[v * SLOTS] : 0;
-        for (int st0 = 0; st0 < nst; st0 += PF) {
-#pragma unroll
-            for (int v = 0; v < PF; ++v) {
-                const int st = st0 + v;
-                if (st >= nst) break;
-                const int s = st % STAGES;
-                const uint32_t off = static_cast<uint32_t>(kq[v]) * pitch;
-                if (st + PF < nst) kq[v] = ssrc[(st + PF) * SLOTS];
-                if (warp == 0) TS2(st, 0);
-                if (st >= STAGES) mbar_wait(&empty[s], ((st / STAGES) - 1) & 1);
-                if (warp == 0) TS2(st, 1);
-                if (warp == 0 && lane == 0) {
-                    if (p.dbg & 16) {
-                        mbar_arrive(&full[s]);
-                    } else {
-                        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(W_BYTES));
-                        bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(st) * 2 * WH_BYTES, W_BYTES, &full[s]);
-                    }
-                }
-                if (!(p.dbg & 1)) {
-                    const uint32_t bstage = smem_u32(sB + s * B_BYTES);
-#pragma unroll
-                    for (int i = 0; i < ROWS_PER_WARP / 2; ++i) {
-                        const uint32_t o = __shfl_sync(0xffffffffu, off, 2 * i + half);
-                        cp_async16(bstage + dl[i], src_base + o, srcsz);
-                    }
-                }
-                cp_async_arrive_noinc(&full[s]);
-                if (warp == 0) TS2(st, 2);
-            }
-        }
-    } else if (leader) {
-        // ============ leader MMA issuer: full[s] covers both CTAs (local arrivals + the peer's relay) ============
-        constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
-                                   (static_cast<uint32_t>(P2_NT >> 3) << 17) | (static_cast<uint32_t>(256 >> 4) << 24);
-        for (int st = 0; st < nst; ++st) {
-            const int s = st % STAGES;
-            mbar_wait_cluster(&full[s], (st / STAGES) & 1);
-            TS2(st, 3);
-            tc_fence_after();
-            if (elect_one() && !(p.dbg & 2)) {
-                const uint32_t wa = smem_u32(sW + s * W_BYTES);
-                const uint32_t ba = smem_u32(sB + s * B_BYTES);
-                const uint32_t ecol = tmem + P2_NT + 4 * s;
-                tmem_cp2_128x128b(ecol, smem_desc(wa + A_BYTES, 2048, 128, 0));
-#pragma unroll
-                for (int j = 0; j < 2; ++j)
-                    mma_sp2(tmem, smem_desc(wa + 32 * j, 16, 512, 4), smem_desc(ba + 4096 * j, SLOTS * 128, 1024, 2),
-                            idesc | static_cast<uint32_t>(j), (st | j) ? 1u : 0u, ecol);
-            }
-            if (elect_one()) {
-                if (p.dbg & 128) {  // timing study (no MMA in flight): plain arrives instead of the commit
-                    mbar_arrive(&empty[s]);
-                    mbar_arrive_remote(&empty[s], 1);
-                } else {
-                    tc_commit2_mc(&empty[s], 0x3);
-                }
-            }
-            __syncwarp();
-            TS2(st, 4);
-        }
-        if (elect_one()) tc_commit2_mc(acc_full, 0x3);
-        __syncwarp();
-    } else {
-        // ============ peer relay: this CTA's stage s is complete -> arrive on the leader's full[s] ============
-        for (int st = 0; st < nst; ++st) {
-            const int s = st % STAGES;
-            mbar_wait(&full[s], (st / STAGES) & 1);
-            TS2(st, 5);
-            if (lane == 0) {
-                mbar_arrive_remote(&full[s], 0);
-            }
-            __syncwarp();
-        }
-    }
-
-    if (warp < GATHER_WARPS) {
-        // ============ epilogue: this CTA's 128 columns x the pair's 256 tokens, staged, TMA stores ============
-        mbar_wait(acc_full, 0);
-        tc_fence_after();
-        const int qw = warp & 3;
-        const int eb = p.c_bf16 ? 2 : 4;
-        const int rowb = 128 * eb;
-        const uint32_t tbase = tmem + (static_cast<uint32_t>(qw * 32) << 16);
-        const int col0 = tile * 256 + 128 * static_cast<int>(rank);
-#pragma unroll 1
-        for (int t0 = (warp >> 2) * 32; t0 < P2_NT; t0 += 64) {
-            uint8_t* buf = smem + (t0 / 32) * 32 * rowb;
-            uint32_t v[32];
-            tmem_ld32(tbase + t0, v);
-            tmem_wait_ld();
-            uint8_t* cb = buf + (qw * 32 + lane) * eb;
-            if (p.c_bf16) {
-#pragma unroll
-                for (int i = 0; i < 32; ++i)
-                    *reinterpret_cast<__nv_bfloat16*>(cb + i * rowb) = __float2bfloat16_rn(__uint_as_float(v[i]));
-            } else {
-#pragma unroll
-                for (int i = 0; i < 32; ++i) *reinterpret_cast<uint32_t*>(cb + i * rowb) = v[i];
-            }
-            fence_proxy_async_smem();
-            named_bar_sync(1 + (warp >> 2), 128);
-            if (qw == 0 && lane == 0 && !(p.dbg & (8 | 64))) {
-                tma_store_2d(&tmC, buf, col0, m0 + t0);
-                bulk_commit();
-            }
-        }
-        if (qw == 0 && lane == 0) bulk_wait_read0();
-        tc_fence_before();
-    }
-    cluster_sync_all();  // the leader's MMAs / commits touching this CTA are complete in both CTAs
-    if (warp == MMA_WARP) {
-        tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS) : "memory");
-    }
-}
-
 // A (m x k bf16, row-major) -> At (k x mp, mp = m rounded up to 8): 64 x 64 tiles through shared memory.
 __global__ void __launch_bounds__(256) transpose_bf16_kernel(const __nv_bfloat16* __restrict__ A,
                                                             __nv_bfloat16* __restrict__ At, int m, int k, int mp) {
@@ -1145,31 +909,6 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
     return NM_OK;
 }
 
-// CTA-pair kernel: needs the TMA-store epilogue (C rows 16-B aligned).
-static nm_status sp2_launch(const __nv_bfloat16* at, tcs::Params p, int64_t m, int64_t n, cudaStream_t s, bool* ran) {
-    using namespace tcs;
-    *ran = false;
-    const int eb = p.c_bf16 ? 2 : 4;
-    if ((n * eb) % 16 != 0 || (reinterpret_cast<uintptr_t>(p.C) & 15) != 0) return NM_OK;
-    CUtensorMap tmC;
-    const CUtensorMapDataType dt = p.c_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
-    if (make_tma_2d(&tmC, p.C, dt, eb, m, n, 32, 128, 0) != NM_OK) return NM_OK;
-    static bool attr = false;
-    if (!attr) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P2_SMEM));
-        attr = true;
-    }
-    p.tma_c = 1;
-    const dim3 grid(static_cast<unsigned>(2 * ceil_div(m, P2_NT)), static_cast<unsigned>(ceil_div(n, 256)));
-    prof_begin(s);
-    spmm_tc_sp2_kernel<<<grid, THREADS, P2_SMEM, s>>>(at, tmC, p);
-    prof_end(s);
-    note_launch();
-    NM_LAUNCH_CHECK("spmm_tc_sp2_kernel");
-    *ran = true;
-    return NM_OK;
-}
-
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M, int L,
                     cudaStream_t s) {
     using namespace tcs;
@@ -1209,10 +948,7 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
         p.dbg = dbg ? std::atoi(dbg) : 0;
 
         const int H = sp_halves(L, N, M), nt = sp_tokens(H, m, n);
-        const char* pe = std::getenv("NM_SP_PAIR");
-        bool ran = false;
-        if (H == 2 && pe && pe[0] == '1') st = sp2_launch(at, p, m, n, s, &ran);
-        if (!st && !ran) switch (H * 1000 + nt) {
+        switch (H * 1000 + nt) {
             case 2192: st = sp_launch_h<2, 192>(at, p, m, n, s); break;
             case 2128: st = sp_launch_h<2, 128>(at, p, m, n, s); break;
             case 2160: st = sp_launch_h<2, 160>(at, p, m, n, s); break;

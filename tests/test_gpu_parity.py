@@ -444,19 +444,6 @@ def test_spmm_tc_sp_token_tiles_all_rows(nm, oracle, monkeypatch, nt, cdt):
         assert np.array_equal(C, want)
 
 
-@pytest.mark.parametrize("m,n,k,N,M,L", [(300, 512, 512, 16, 32, 32), (513, 384, 1024, 8, 32, 64)])
-def test_spmm_tc_sp_pair_kernel_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L):
-    """The CTA-pair (cta_group::2) variant, opt-in via NM_SP_PAIR=1 (measured slower, DESIGN.md 5.2)."""
-    use_tc_path(monkeypatch, "sp")
-    monkeypatch.setenv("NM_SP_PAIR", "1")
-    A = synth.integer((m, k), 121, synth.TID_A)
-    B = synth.integer((k, n), 122, synth.TID_B)
-    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
-    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
-    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
-    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
-
-
 @pytest.mark.parametrize("tail", ["0", "1"])
 @pytest.mark.parametrize("m,n,k,N,M,L", [(700, 768, 512, 16, 32, 32), (300, 640, 1024, 4, 32, 32)])
 def test_spmm_tc_sp_tail_split_on_off(nm, oracle, monkeypatch, tail, m, n, k, N, M, L):
