@@ -38,8 +38,12 @@ using namespace nm::tc;
 // groups): 128 columns x 256 tokens.
 constexpr int SLOTS = 64;                  // logical k slots per stage (2 MMAs of K = 32)
 constexpr int A_BYTES = 128 * SLOTS;       // per half: 128 rows x 32 compressed bf16 (64 B rows, 64-B swizzle)
-constexpr int E_BYTES = 128 * 16;          // per half: metadata, 128 TMEM lanes x 16 B (columns 0, 1 used)
+constexpr int E_BYTES = 128 * 16;          // per half: metadata of a stage PAIR, 128 TMEM lanes x 16 B
+                                           // (words 0, 1: the even stage's two MMAs; 2, 3: the odd stage's)
 constexpr int WH_BYTES = A_BYTES + E_BYTES;
+// Weight image of one (column tile, stage): [A_0 .. A_{H-1} | E_0 .. E_{H-1}]; the E blocks are
+// present (and copied) only for even stages and carry the metadata of the stage pair, so an odd
+// stage moves H x A_BYTES and the metadata costs 1 KB per half and stage instead of 2.
 constexpr int GATHER_WARPS = 8;            // also the epilogue warps (TMEM lane quarter = warp % 4)
 constexpr int ROWS_PER_WARP = SLOTS / GATHER_WARPS;
 constexpr int MMA_WARP = GATHER_WARPS;
@@ -56,9 +60,12 @@ struct Cfg {
     static constexpr int ST0 = (232448 - 1024 - 256) / (W_BYTES + B_BYTES);
     static constexpr int ST = ST0 > 8 ? 8 : ST0;          // pipeline stages (shared-memory bound)
     static constexpr int SMEM_BYTES = ST * (W_BYTES + B_BYTES) + 1024 + 256;
-    static constexpr int META_COL = H * NT;               // metadata ring: 4 H columns per stage
+    static constexpr int META_COL = H * NT;               // metadata ring: 4 H columns per stage pair
+    // a pair's TMEM columns are rewritten NPAIR pairs later; by then the producer has refilled the
+    // smem slot of a stage >= STAGES later, so the MMAs that read them have completed
+    static constexpr int NPAIR = (ST + 2) / 2;
     static_assert(NT % 16 == 0 && NT <= 256, "MMA N");
-    static_assert(META_COL + 4 * H * ST <= TMEM_COLS, "TMEM budget");
+    static_assert(META_COL + 4 * H * NPAIR <= TMEM_COLS, "TMEM budget");
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
@@ -95,7 +102,7 @@ static int sp_halves(int L, int N, int M) {
 }
 
 struct Params {
-    const uint8_t* wimg;   // [ntiles][max_stages][H][WH_BYTES]
+    const uint8_t* wimg;   // [ntiles][max_stages][H x A_BYTES | H x E_BYTES (even stages)]
     const int* slots;      // [ntiles][smax] row of A^T per slot (k = padding, TMA zero fill)
     const int* nstages;    // [ntiles]
     void* C;
@@ -234,7 +241,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tile = tid_lin / p.n_tok;
     const int m0 = (tid_lin % p.n_tok) * NT;
     const int nst_all = p.nstages[tile];
-    const int smid = (nst_all + 1) >> 1;
+    const int smid = min(nst_all, ((nst_all + 3) >> 2) << 1);  // even: a stage pair's metadata stays in one part
     const int sa = part == 1 ? smid : 0, sb = part == 0 ? smid : nst_all;
     const int nst = sb - sa;  // stages this CTA runs (ring index = st - sa)
     const int tail_idx = tid_lin - p.full_ctas;
@@ -301,16 +308,16 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (warp == 0 && lane == 0) {
                     if (p.dbg & 16) {
                         mbar_arrive(&full[s]);
-                    } else if (MCAST) {
-                        // both halves land in both CTAs: expect all W_BYTES, copy (and multicast) ours
-                        constexpr uint32_t HALF_W = W_BYTES / 2;
-                        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(W_BYTES));
-                        bulk_load_mc(sW + s * W_BYTES + crank * HALF_W,
-                                     wsrc + static_cast<int64_t>(sa + st) * W_BYTES + crank * HALF_W, HALF_W, &full[s],
-                                     0x3);
                     } else {
-                        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(W_BYTES));
-                        bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(sa + st) * W_BYTES, W_BYTES, &full[s]);
+                        // even stages bring the pair's metadata blocks, odd ones only the A images
+                        const uint32_t wb = ((sa + st) & 1) ? static_cast<uint32_t>(H * A_BYTES) : W_BYTES;
+                        mbar_arrive_expect_tx(&full[s], wb);
+                        if (MCAST)  // both halves land in both CTAs: copy (and multicast) ours
+                            bulk_load_mc(sW + s * W_BYTES + crank * (wb / 2),
+                                         wsrc + static_cast<int64_t>(sa + st) * W_BYTES + crank * (wb / 2), wb / 2,
+                                         &full[s], 0x3);
+                        else
+                            bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(sa + st) * W_BYTES, wb, &full[s]);
                     }
                 }
                 if (!(p.dbg & 1)) {
@@ -339,16 +346,20 @@ __global__ void __launch_bounds__(THREADS, 1)
             tc_fence_after();
             if (elect_one() && !(p.dbg & 2)) {
                 const uint32_t ba = smem_u32(sB + s * B_BYTES);
+                const int gs = sa + st;  // stage index in the tile (pairs: 2i, 2i+1)
+                const uint32_t pcol = tmem + CF::META_COL + 4 * H * ((gs >> 1) % CF::NPAIR);
 #pragma unroll
                 for (int h = 0; h < H; ++h) {
-                    const uint32_t wa = smem_u32(sW + s * W_BYTES + h * WH_BYTES);
-                    const uint32_t ecol = tmem + CF::META_COL + 4 * (H * s + h);
-                    tmem_cp_128x128b(ecol, smem_desc(wa + A_BYTES, 2048, 128, 0));
+                    const uint32_t wa = smem_u32(sW + s * W_BYTES + h * A_BYTES);
+                    const uint32_t ecol = pcol + 4 * h;
+                    if (!(gs & 1))  // the pair's metadata arrives with its even stage (sa is even)
+                        tmem_cp_128x128b(ecol, smem_desc(smem_u32(sW + s * W_BYTES) + H * A_BYTES + h * E_BYTES, 2048,
+                                                         128, 0));
 #pragma unroll
                     for (int j = 0; j < 2; ++j)
                         mma_sp(tmem + h * NT, smem_desc(wa + 32 * j, 16, 512, 4),
                                smem_desc(ba + 4096 * j, SLOTS * 128, 1024, 2), idesc | static_cast<uint32_t>(j),
-                               (st | j) ? 1u : 0u, ecol);
+                               (st | j) ? 1u : 0u, ecol + 2 * (gs & 1));
                 }
             }
             if (elect_one()) {
@@ -713,8 +724,10 @@ __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint
     const int g = j / L, gi = r / L;
     const bool live = j < n;
     const int hf = r / 128;
-    uint8_t* img = wimg + ((static_cast<int64_t>(tile) * max_stages + st) * H + hf) * WH_BYTES;
-    uint32_t* meta = reinterpret_cast<uint32_t*>(img + A_BYTES);
+    uint8_t* img = wimg + (static_cast<int64_t>(tile) * max_stages + st) * H * WH_BYTES + hf * A_BYTES;
+    // metadata of the pair (st & ~1, st | 1) lives in the even stage's E block of this half
+    uint32_t* meta = reinterpret_cast<uint32_t*>(wimg + (static_cast<int64_t>(tile) * max_stages + (st & ~1)) * H * WH_BYTES +
+                                                 H * A_BYTES + hf * E_BYTES);
     const int* sl = slots + static_cast<int64_t>(tile) * smax + st * SLOTS;
     const uint8_t* ty = stype + static_cast<int64_t>(tile) * smax + st * SLOTS;
     for (int qd = 0; qd < SLOTS / 4; ++qd) {
@@ -753,7 +766,7 @@ __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint
         const int mma = qd / 8, c = qd % 8;
         const int ln = (rr % 8) + 8 * (c / 4) + 16 * (rr / 16);
         const int bit = 16 * ((rr / 8) % 2) + 4 * (c % 4);
-        atomicOr(&meta[ln * 4 + mma], static_cast<uint32_t>(pos[0] | (pos[1] << 2)) << bit);
+        atomicOr(&meta[ln * 4 + 2 * (st & 1) + mma], static_cast<uint32_t>(pos[0] | (pos[1] << 2)) << bit);
     }
 }
 
