@@ -40,8 +40,8 @@ CONFIGS = {
     "cfg4_65b": (2048, 22016, 8192, 4, 32, 32),
 }
 HEADLINE = "cfg2"
-VARIANTS = ["cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_65b:f32", "cfg3_62:bf16", "cfg3_75:bf16",
-            "cfg4_65b:bf16"]
+VARIANTS = ["cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_13b:f32", "cfg4_65b:f32", "cfg3_62:bf16",
+            "cfg3_75:bf16", "cfg4_13b:bf16", "cfg4_65b:bf16"]
 
 
 def load_peaks():
