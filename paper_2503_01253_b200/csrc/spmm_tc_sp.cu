@@ -1,7 +1,8 @@
 // spmm_tc_sp.cu -- bf16 vector-wise N:M SpMM on the sparse tensor cores (tcgen05.mma.sp, sm_100a).
 //
 // Eq. 1 computed as C^T = B~^T . A^T with the weight as the MMA's sparse A operand:
-//   * MMA M = 128 output columns (128 / L column groups), MMA N = 256 tokens, MMA K = 32 "slots".
+//   * MMA M = 128 output columns per column half (128 / L groups; H = 1 or 2 halves share a
+//     token tile), MMA N = NT tokens (160-256), MMA K = 32 "slots".
 //   * Per column tile, the union of the k rows its groups keep (the paper's col_info)
 //     is arranged offline into a slot sequence kappa(s) in which every aligned quad of slots holds
 //     at most two rows kept by any one group (sp_pack_kernel: the paper's offline index
@@ -9,16 +10,17 @@
 //     exactly what the sparse tensor core contracts at twice the dense rate: per quad, two
 //     values of B' plus a 4-bit metadata nibble naming their slots.
 //   * The dense operand is the token tile of A gathered by slot: rows kappa(s) of A^T (A
-//     transposed once per call), one 512-B row (256 tokens) per warp-wide 16-B cp.async,
+//     transposed once per call), one row segment (NT tokens) per warp-wide 16-B cp.async,
 //     written straight into the 128-B-swizzled MN-major layout the MMA reads.  (TMA
 //     tile::gather4 does the same with no SM instructions but measured ~80 clk per 4 rows
-//     per SM on B200 -- 6x slower than this kernel needs; giving it a quarter or half of the
-//     rows beside the cp.async warps was slower too.)
+//     per SM on B200 -- 6x slower than this kernel needs.)
 //   * Compressed weights + metadata are prepacked per (column tile, 64-slot stage) as the exact
-//     shared-memory images (one bulk copy each); metadata goes to TMEM by tcgen05.cp.
-// Roles: warps 0-3 gather (16 slot rows each per stage; warp 0 also bulk-copies the weight
-// image) and then the epilogue (TMEM -> registers -> C); warp 4 MMA issuer (tcgen05.cp + 2
-// tcgen05.mma.sp per stage).
+//     shared-memory images (one bulk copy each; a stage pair's metadata rides with its even
+//     stage); metadata goes to TMEM by tcgen05.cp.
+// Roles: warps 0-7 gather (8 slot rows each per stage; warp 0 also bulk-copies the weight
+// image) and then the epilogue (TMEM -> registers -> smem -> TMA store); warp 8 issues the
+// tcgen05.cp + 2 H tcgen05.mma.sp per stage.  Optional: tail split of the last partial wave,
+// weight multicast over 2-CTA clusters (NM_SP_MC=1).
 #include <cuda_bf16.h>
 
 #include <cstdlib>
