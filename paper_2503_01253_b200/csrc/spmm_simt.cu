@@ -159,6 +159,9 @@ __global__ void __launch_bounds__(THREADS, 2)
         d_us[r] = (u < p.bkw && sl < nslots) ? (u << 8 | sl) : -1;
         d_wb[r] = (u / p.N) * p.M;
     }
+    // the valid entries are a prefix r < nd (e grows with r): the per-panel index loops stop
+    // there -- at L >= 32 a panel has only BKW x (BN/L + 1) entries, most threads 0 or 1
+    const int nd = min(D_PER_THREAD, max(0, (p.bkw * nslots - tid + THREADS - 1) / THREADS));
     const int wtot = (p.k / p.M) * p.N;
     auto load_d = [&](int panel) {
         const int u0 = panel * p.bkw;
@@ -166,8 +169,9 @@ __global__ void __launch_bounds__(THREADS, 2)
         const int ulim = wtot - u0;  // rows of D left (last panel may be partial)
 #pragma unroll
         for (int r = 0; r < D_PER_THREAD; ++r) {
+            if (r >= nd) break;
             const int u = d_us[r] >> 8, sl = d_us[r] & 255;
-            dreg[r] = (d_us[r] >= 0 && u < ulim) ? Dp[u * p.q + sl] : 0;
+            dreg[r] = (u < ulim) ? Dp[u * p.q + sl] : 0;
         }
     };
     auto store_d = [&](int panel) {
@@ -175,7 +179,8 @@ __global__ void __launch_bounds__(THREADS, 2)
         const uint64_t mk = PK ? smask[panel] : 0ull;
 #pragma unroll
         for (int r = 0; r < D_PER_THREAD; ++r) {
-            if (d_us[r] >= 0) {
+            if (r >= nd) break;
+            {
                 const int kk = d_wb[r] + dreg[r];  // dense column inside the panel
                 const int row = PK ? __popcll(mk & ((1ull << kk) - 1ull)) : kk;  // packed position
                 kb[(d_us[r] >> 8) * MAX_SLOTS + (d_us[r] & 255)] = AT ? row * (BM * 4) : a_col_offset(kk);
