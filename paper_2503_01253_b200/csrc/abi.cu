@@ -211,14 +211,15 @@ void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_
 nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                          int64_t k, int N, int M, int L, cudaStream_t s);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
-size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L);
+// tf: fp32 operands on the tf32 sparse tensor cores (1:2 slot pairs), else bf16 (2:4 slot quads)
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf);
 void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int* tokens);
-nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, void* buf,
+nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, void* buf,
                         cudaStream_t s);
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
-                    int M, int L, cudaStream_t s);
+                    int M, int L, bool tf, cudaStream_t s);
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                       int64_t k, int N, int M, int L, cudaStream_t s);
+                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s);
 
 // Sparse-tensor-core slot path (spmm_tc_sp.cu): bf16, L in {16, 32, 64, 128}, A 16-B aligned with
 // k % 8 == 0 (the per-call transpose reads 16-B chunks), C 4-B aligned.  NM_TC_SP=0 disables it.
@@ -329,7 +330,15 @@ static nm_status select(const void* A, const void* Bv, const void* C, int64_t m,
             *kernel = simt_f32_applicable(A, Bv, C, m, n, k, N, M, L) ? K_SIMT_F32 : K_GENERIC;
             return NM_OK;
         }
-        if (math == NM_MATH_TF32_TC) return fail(NM_ERR_UNSUPPORTED, "tf32 tensor-core path not built yet");
+        if (math == NM_MATH_TF32_TC) {
+            // explicit opt-in only (tf32 rounds the operands; AUTO keeps the paper's fp32 semantics)
+            if (!tc_sp_ok(A, C, m, n, k, N, M, L))
+                return fail(NM_ERR_UNSUPPORTED, "tf32 sparse-tensor-core path needs L in {16,32,64,128}, k % 8 == 0, "
+                                                "A 16-B and C 4-B aligned");
+            *used = NM_MATH_TF32_TC;
+            *kernel = K_TC_TF32;
+            return NM_OK;
+        }
         return fail(NM_ERR_UNSUPPORTED, "bf16 math requested on fp32 operands");
     }
     if (math == NM_MATH_AUTO || math == NM_MATH_BF16_TC) {
@@ -421,7 +430,8 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
         return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
                                static_cast<float*>(C), m, n, k, N, M, L, mode, s);
     }
-    if (kernel == K_TC_SP) return tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
+    if (kernel == K_TC_SP) return tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, false, s);
+    if (kernel == K_TC_TF32) return tc_sp_launch(A, values, idx, C, false, m, n, k, N, M, L, true, s);
     if (kernel == K_TC_BF16) return tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
     if (ab_dt == NM_F32) return generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
     if (c_dt == NM_BF16) return generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);
@@ -491,14 +501,15 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->threads = 256;
         out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
         out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
-    } else if (kernel == K_TC_SP) {
-        // tokens x output columns per CTA (MMA N x M per column half), 64 slots per stage
+    } else if (kernel == K_TC_SP || kernel == K_TC_TF32) {
+        // tokens x output columns per CTA (MMA N x M per column half), 64 (bf16) / 32 (tf32) slots
+        // per stage, the same bytes per stage
         int hh = 1, nt = 256;
         tc_sp_geometry(m, n, N, M, L, &hh, &nt);
         out->bm = nt;
         out->bn = 128 * hh;
-        out->bk = 64;
-        out->bkw = 32;
+        out->bk = kernel == K_TC_SP ? 64 : 32;
+        out->bkw = out->bk / 2;
         out->threads = 288;
         out->grid = static_cast<int32_t>(ceil_div(m, out->bm) * ceil_div(n, out->bn));
         {
@@ -524,8 +535,10 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->threads = 256;
         out->grid = static_cast<int32_t>(ceil_div(m, 8) * ceil_div(n, 32));
     }
-    // nominal peaks when none are given: FP32 FFMA = SMs * 128 lanes * 2 * 1.965 GHz; bf16 TC 2.25 PF; HBM 7.7 TB/s
-    if (peak_flops <= 0) peak_flops = used == NM_MATH_F32_SIMT ? double(sms) * 128 * 2 * 1.965e9 : 2.25e15;
+    // nominal peaks when none are given: FP32 FFMA = SMs * 128 lanes * 2 * 1.965 GHz; bf16 TC 2.25 PF, tf32 half
+    // of it; HBM 7.7 TB/s
+    if (peak_flops <= 0)
+        peak_flops = used == NM_MATH_F32_SIMT ? double(sms) * 128 * 2 * 1.965e9 : used == NM_MATH_TF32_TC ? 1.125e15 : 2.25e15;
     if (peak_hbm <= 0) peak_hbm = 7.7e12;
     out->t_compute_us = out->flops / peak_flops * 1e6;
     out->t_memory_us = out->bytes / peak_hbm * 1e6;
@@ -568,7 +581,7 @@ extern "C" {
 
 int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
     if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16) return -1;
-    if (prepack_kind2(n, k, N, M, L, dt)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L));
+    if (prepack_kind2(n, k, N, M, L, dt)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, false));
     int g[5];
     if (!prepack_kind1(n, k, N, M, L, dt, g)) return 0;
     size_t pb, tb, bb;
@@ -598,7 +611,7 @@ nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t 
         if ((st = require_device())) return st;
         out->kind = 2;
         out->bperm = buf;
-        st = tc_sp_prepack(values, idx, n, k, N, M, L, buf, static_cast<cudaStream_t>(stream));
+        st = tc_sp_prepack(values, idx, n, k, N, M, L, false, buf, static_cast<cudaStream_t>(stream));
         if (st) return st;
     } else if (prepack_kind1(n, k, N, M, L, dt, g)) {
         const int64_t need = nm_prepack_bytes(n, k, N, M, L, dt);
@@ -634,7 +647,7 @@ nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64
         if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
         if ((st = require_device())) return st;
         if (tc_sp_ok(A, C, m, w->n, w->k, w->N, w->M, w->L))
-            return tc_sp_run(A, w->bperm, C, c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L,
+            return tc_sp_run(A, w->bperm, C, c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, false,
                              static_cast<cudaStream_t>(stream));
     }
     if (w->kind == 1) {

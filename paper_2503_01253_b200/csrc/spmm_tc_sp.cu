@@ -29,6 +29,9 @@
 #include "tcgen05.cuh"
 
 namespace nm {
+
+__global__ void transpose_kernel(const float* __restrict__ A, float* __restrict__ AT, int m, int k, int ld);
+
 namespace tcs {
 
 using namespace nm::tc;
@@ -38,8 +41,24 @@ using namespace nm::tc;
 // is packed over all 128 H / L groups), so the gathered bytes per MAC halve at H = 2.
 // H = 2 (L >= 32): 256 columns x 192 tokens; H = 1 (L = 16, where 256 columns would be 16
 // groups): 128 columns x 256 tokens.
-constexpr int SLOTS = 64;                  // logical k slots per stage (2 MMAs of K = 32)
-constexpr int A_BYTES = 128 * SLOTS;       // per half: 128 rows x 32 compressed bf16 (64 B rows, 64-B swizzle)
+// Element types.  bf16 (kind::f16): 2:4 along the slots, 64 slots per stage (2 MMAs of K = 32),
+// quads of slots share a metadata nibble.  tf32 (kind::tf32, fp32 operands): 1:2 along the
+// slots, 32 slots per stage (2 MMAs of K = 16), pairs of slots share a nibble (0x4: the pair's
+// first slot, 0xE: its second -- established on the GPU by scripts/ubench_sp_tf32.cu).  Both
+// give 64-B weight-image rows and the same bytes per stage; the tf32 token tile is MN-major with
+// the 32-B-atom 128-B swizzle (descriptor layout 1: 32-B chunks XOR k % 4, 4-row groups).
+template <bool TF>
+struct El {
+    static constexpr int E = TF ? 4 : 2;                // operand bytes
+    static constexpr int SLOTS = TF ? 32 : 64;          // slots per stage
+    static constexpr int PG = TF ? 2 : 4;               // slots per metadata group
+    static constexpr int TOK_ATOM = 128 / E;            // tokens per 128-B swizzled row
+    static constexpr uint32_t B_SBO = TF ? 512 : 1024;  // k-direction stride of the swizzle groups
+    static constexpr uint32_t B_LAYOUT = TF ? 1 : 2;    // 128B_BASE32B / 128B
+    static constexpr uint32_t B_STEP = (SLOTS / 2) * 128;  // one MMA's K slots of the token tile
+    static constexpr uint32_t FMT = TF ? 2 : 1;         // instruction-descriptor a/b format
+};
+constexpr int A_BYTES = 8192;              // per half: 128 rows x 64 B (32 bf16 / 16 tf32), 64-B swizzle
 constexpr int E_BYTES = 128 * 16;          // per half: metadata of a stage PAIR, 128 TMEM lanes x 16 B
                                            // (words 0, 1: the even stage's two MMAs; 2, 3: the odd stage's)
 constexpr int WH_BYTES = A_BYTES + E_BYTES;
@@ -47,17 +66,16 @@ constexpr int WH_BYTES = A_BYTES + E_BYTES;
 // present (and copied) only for even stages and carry the metadata of the stage pair, so an odd
 // stage moves H x A_BYTES and the metadata costs 1 KB per half and stage instead of 2.
 constexpr int GATHER_WARPS = 8;            // also the epilogue warps (TMEM lane quarter = warp % 4)
-constexpr int ROWS_PER_WARP = SLOTS / GATHER_WARPS;
 constexpr int MMA_WARP = GATHER_WARPS;
 constexpr int THREADS = (GATHER_WARPS + 1) * 32;
 constexpr int TMEM_COLS = 512;
 
-template <int H, int NT_>
+template <int H, int NT_, bool TF = false>
 struct Cfg {
     static constexpr int MC = 128 * H;                    // output columns per CTA
     static constexpr int NT = NT_;                        // tokens per CTA (MMA N)
-    static constexpr int ATOMS = (NT + 63) / 64;
-    static constexpr int B_BYTES = SLOTS * ATOMS * 128;   // token atoms x 64 slot rows x 128 B
+    static constexpr int ATOMS = (NT + El<TF>::TOK_ATOM - 1) / El<TF>::TOK_ATOM;
+    static constexpr int B_BYTES = El<TF>::SLOTS * ATOMS * 128;  // token atoms x slot rows x 128 B
     static constexpr int W_BYTES = H * WH_BYTES;          // per (column tile, stage) weight image
     static constexpr int ST0 = (232448 - 1024 - 256) / (W_BYTES + B_BYTES);
     static constexpr int ST = ST0 > 8 ? 8 : ST0;          // pipeline stages (shared-memory bound)
@@ -145,13 +163,21 @@ __device__ __forceinline__ void named_bar_sync(int id, int threads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+template <bool TF>
 __device__ __forceinline__ void mma_sp(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc,
                                        uint32_t emeta) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t}" ::"r"(d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(emeta)
-        : "memory");
+    if (TF)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.sp.cta_group::1.kind::tf32 [%0], %1, %2, [%5], %3, p;\n\t}" ::"r"(d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(emeta)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.sp.cta_group::1.kind::f16 [%0], %1, %2, [%5], %3, p;\n\t}" ::"r"(d),
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(emeta)
+            : "memory");
 }
 
 __device__ __forceinline__ void tmem_cp_128x128b(uint32_t taddr, uint64_t sdesc) {
@@ -213,12 +239,15 @@ __device__ __forceinline__ void cluster_sync_all() {
 // ranges); each CTA bulk-copies half of every weight image with .multicast::cluster into both,
 // and every MMA commit releases the stage in both CTAs (empty count 2): the weight stream's L2
 // traffic per SM halves.
-template <int H, int NT_, bool MCAST>
+// TF: fp32 operands on kind::tf32 (El<true>), else bf16 on kind::f16.
+template <int H, int NT_, bool MCAST, bool TF>
 __global__ void __launch_bounds__(THREADS, 1)
-    spmm_tc_sp_kernel(const __nv_bfloat16* __restrict__ At, const __grid_constant__ CUtensorMap tmC,
+    spmm_tc_sp_kernel(const void* __restrict__ At, const __grid_constant__ CUtensorMap tmC,
                       const __grid_constant__ CUtensorMap tmC16, const Params p) {
-    using CF = Cfg<H, NT_>;
+    using CF = Cfg<H, NT_, TF>;
+    using EL = El<TF>;
     constexpr int NT = CF::NT, MC = CF::MC, B_BYTES = CF::B_BYTES, W_BYTES = CF::W_BYTES, STAGES = CF::ST;
+    constexpr int SLOTS = EL::SLOTS, RPW = SLOTS / GATHER_WARPS;  // slot rows per gather warp and stage
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sB = smem;                               // STAGES x B_BYTES (1024-aligned: 128-B swizzle atoms)
@@ -270,25 +299,45 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp < GATHER_WARPS) {
         // ============ gather: one slot row (NT tokens) per warp instruction ============
         // lane l copies tokens [8l, 8l+8) of the row: token atom l/8, 16-B chunk l%8 of the
-        // 128-B swizzled row (chunk ^= row % 8).  Warp wg owns ROWS_PER_WARP consecutive rows of a stage.
+        // 128-B swizzled row (chunk ^= row % 8).  Warp wg owns RPW consecutive rows of a stage.
         // Completion: cp.async.mbarrier.arrive.noinc per thread (no wait in the loop).
         const uint8_t* wsrc = p.wimg + static_cast<int64_t>(tile) * p.max_stages * W_BYTES;
-        const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * ROWS_PER_WARP + (lane % ROWS_PER_WARP);
-        // per-lane constants: source = A^T row base + 2 (m0 + 8 lane) bytes (row k of A^T is a zero
+        const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * RPW + (lane % RPW);
+        // per-lane constants: source = A^T row base + E (m0 + token) bytes (row k of A^T is a zero
         // row, the padding slots' source); destination = stage + this lane's (atom, swizzled chunk)
-        // of each of the warp's rows -- row r % 8 = i because ROWS_PER_WARP = 8, so the XOR is static
-        static_assert(ROWS_PER_WARP == 8, "rows per warp = swizzle period");
-        const int tok = m0 + 8 * lane;
-        const bool lane_on = lane < NT / 8;
-        const bool tok_ok = lane_on && tok < p.mp;
-        const uint32_t srcsz = tok_ok ? 16u : 0u;
-        const char* src_base = reinterpret_cast<const char*>(At) + 2 * static_cast<int64_t>(tok_ok ? tok : 0);
-        const uint32_t pitch = static_cast<uint32_t>(p.mp) * 2u;
-        uint32_t dl[ROWS_PER_WARP];
+        // of each of the warp's rows.  Eight 512-B copies per warp and stage:
+        //   bf16: copy i = slot row i (NT <= 256 tokens), lane -> tokens [8 lane, +8): atom lane / 8,
+        //         16-B chunk lane % 8 ^ (row % 8 = i);
+        //   tf32: copy i = slot row i / 2, token half i % 2 (NT <= 256 tokens = 2 x 512 B), lane ->
+        //         tokens 128 (i % 2) + [4 lane, +4): atom 4 (i % 2) + lane / 8, 32-B chunk
+        //         (lane % 8) / 2 ^ (row % 4 = i / 2), 16-B half lane % 2.
+        // The row's swizzle phase equals its index inside the warp's rows, so every XOR is static.
+        static_assert(SLOTS * EL::E == 128, "eight 512-B copies per warp and stage");
+        constexpr int NCOPY = 8, CPR = NCOPY / RPW;  // copies per slot row
+        const char* src_c[CPR];
+        uint32_t srcsz_c[CPR];
+        bool on_c[CPR];
 #pragma unroll
-        for (int i = 0; i < ROWS_PER_WARP; ++i)
-            dl[i] = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128) + (warp * ROWS_PER_WARP + i) * 128) +
-                    ((static_cast<uint32_t>(lane & 7) ^ static_cast<uint32_t>(i)) << 4);
+        for (int h2 = 0; h2 < CPR; ++h2) {
+            const int tl = TF ? 128 * h2 + 4 * lane : 8 * lane;  // first token of this lane's 16 B
+            on_c[h2] = tl < NT;
+            const bool ok = on_c[h2] && m0 + tl < p.mp;
+            srcsz_c[h2] = ok ? 16u : 0u;
+            src_c[h2] = static_cast<const char*>(At) + EL::E * static_cast<int64_t>(ok ? m0 + tl : 0);
+        }
+        const uint32_t pitch = static_cast<uint32_t>(p.mp) * EL::E;
+        uint32_t dl[NCOPY];
+#pragma unroll
+        for (int i = 0; i < NCOPY; ++i) {
+            if (TF) {
+                const uint32_t j = i / CPR, h2 = i % CPR;
+                dl[i] = static_cast<uint32_t>((4 * h2 + (lane >> 3)) * (SLOTS * 128) + (warp * RPW + j) * 128) +
+                        (((static_cast<uint32_t>(lane & 7) >> 1) ^ j) << 5) + ((static_cast<uint32_t>(lane) & 1u) << 4);
+            } else {
+                dl[i] = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128) + (warp * RPW + i) * 128) +
+                        ((static_cast<uint32_t>(lane & 7) ^ static_cast<uint32_t>(i)) << 4);
+            }
+        }
         // slot rows are prefetched PF stages ahead in rotating registers (loop unrolled by PF): a
         // register is reloaded only after PF iterations, so the load latency (~1-2k clk under load)
         // is not paid per stage -- at PF = 4 it was, and it paced the whole pipeline
@@ -325,9 +374,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 if (!(p.dbg & 1)) {
                     const uint32_t bstage = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-                    for (int i = 0; i < ROWS_PER_WARP; ++i) {
-                        const uint32_t o = __shfl_sync(0xffffffffu, off, i);
-                        cp_async16_pred(bstage + dl[i], src_base + o, srcsz, lane_on);
+                    for (int i = 0; i < NCOPY; ++i) {
+                        const uint32_t o = __shfl_sync(0xffffffffu, off, i / CPR);
+                        cp_async16_pred(bstage + dl[i], src_c[i % CPR] + o, srcsz_c[i % CPR], on_c[i % CPR]);
                     }
                 }
                 // arrives on full[s] once this thread's copies have landed (counts as one of the
@@ -338,7 +387,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp == MMA_WARP) {
         // ============ MMA issuer: per stage and half, metadata -> TMEM and two sparse MMAs ============
-        constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
+        constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (EL::FMT << 7) | (EL::FMT << 10) | (1u << 16) |
                                    (static_cast<uint32_t>(NT >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
         for (int st = 0; st < nst; ++st) {
             const int s = st % STAGES;
@@ -359,9 +408,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                                                          128, 0));
 #pragma unroll
                     for (int j = 0; j < 2; ++j)
-                        mma_sp(tmem + h * NT, smem_desc(wa + 32 * j, 16, 512, 4),
-                               smem_desc(ba + 4096 * j, SLOTS * 128, 1024, 2), idesc | static_cast<uint32_t>(j),
-                               (st | j) ? 1u : 0u, ecol + 2 * (gs & 1));
+                        mma_sp<TF>(tmem + h * NT, smem_desc(wa + 32 * j, 16, 512, 4),
+                                   smem_desc(ba + EL::B_STEP * j, SLOTS * 128, EL::B_SBO, EL::B_LAYOUT),
+                                   idesc | static_cast<uint32_t>(j), (st | j) ? 1u : 0u, ecol + 2 * (gs & 1));
                 }
             }
             if (elect_one()) {
@@ -581,17 +630,18 @@ __global__ void __launch_bounds__(256) transpose_bf16_kernel(const __nv_bfloat16
 // ------------------------------------------------------------------------- offline prepack
 // Slot packing (the paper's offline PreProcessing slot, Listing 3), one thread per
 // (column tile, k chunk of KC rows, KC a multiple of M): item = k row of the chunk kept by at
-// least one of the tile's G groups, type = G-bit membership mask.  First complementary pairs
-// (t, ~t), two per quad; then greedy: fill each quad with the heaviest type that still fits (no
-// group above two rows per quad), ties to the type with the most items left.  Every quad takes
-// >= 2 items, so a chunk needs at most 2 |U_c| + 4 slots.
+// least one of the tile's G groups, type = G-bit membership mask.  Packing unit = PG slots with
+// at most PG / 2 rows of any one group: quads (PG = 4, bf16 2:4) or pairs (PG = 2, tf32 1:2).
+// First complementary pairs (t, ~t) (two per quad, one per pair: every group at exactly PG / 2);
+// then greedy: fill each unit with the heaviest type that still fits, ties to the type with the
+// most items left.  Every unit takes >= PG / 2 items, so a chunk needs at most 2 |U_c| + 4 slots.
 // Chunks pack independently (each ends with at most one partial quad) so the prepack runs on
 // tiles x chunks threads; sp_compact_kernel concatenates them.
 __host__ __device__ inline int sp_chunk_rows(int M) { return (1024 + M - 1) / M * M; }
 
 __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ tmp_slots,
                                uint8_t* __restrict__ tmp_type, int* __restrict__ chunk_cnt, int* __restrict__ qbuf,
-                               int n, int k, int N, int M, int L, int H, int nchunks) {
+                               int n, int k, int N, int M, int L, int H, int nchunks, int PG) {
     const int gid = blockIdx.x * blockDim.x + threadIdx.x;
     const int MC = 128 * H;
     const int ntiles = (n + MC - 1) / MC;
@@ -631,7 +681,10 @@ __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ 
         for (; np > 0; --np) {
             const int ra = qk[head[t]++], rb = qk[head[u]++];
             remaining -= 2;
-            if (pend_a < 0) {
+            if (PG == 2) {  // a perfect pair on its own
+                sl[ns] = ra, ty[ns] = static_cast<uint8_t>(t), ++ns;
+                sl[ns] = rb, ty[ns] = static_cast<uint8_t>(u), ++ns;
+            } else if (pend_a < 0) {
                 pend_a = ra, pend_b = rb, pend_ta = t, pend_tb = u;
             } else {
                 sl[ns] = pend_a, ty[ns] = static_cast<uint8_t>(pend_ta), ++ns;
@@ -652,11 +705,12 @@ __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ 
     while (remaining > 0) {
         uint32_t once = 0, twice = 0;
         int placed = 0;
-        for (int sidx = 0; sidx < 4; ++sidx) {
+        for (int sidx = 0; sidx < PG; ++sidx) {
             int best = -1, bkey = -1;
+            const uint32_t full_groups = PG == 4 ? twice : once;  // groups already at PG / 2 rows
             for (int t = 1; t < T; ++t) {
                 const int left = start[t + 1] - head[t];
-                if (left == 0 || (static_cast<uint32_t>(t) & twice)) continue;
+                if (left == 0 || (static_cast<uint32_t>(t) & full_groups)) continue;
                 const int key = (__popc(t) << 20) + left;
                 if (key > bkey) bkey = key, best = t;
             }
@@ -669,7 +723,7 @@ __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ 
             --remaining;
             ++placed;
         }
-        for (; placed < 4; ++placed) {
+        for (; placed < PG; ++placed) {
             sl[ns] = k;  // padding slot: the zero row k of A^T
             ty[ns] = 0;
             ++ns;
@@ -678,10 +732,10 @@ __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ 
     chunk_cnt[gid] = ns;
 }
 
-// Concatenate a tile's chunk slot lists (one block per tile), pad to whole 64-slot stages.
+// Concatenate a tile's chunk slot lists (one block per tile), pad to whole stages of SLOTS slots.
 __global__ void sp_compact_kernel(const int* __restrict__ tmp_slots, const uint8_t* __restrict__ tmp_type,
                                   const int* __restrict__ chunk_cnt, int* __restrict__ slots, uint8_t* __restrict__ stype,
-                                  int* __restrict__ nstages, int k, int M, int nchunks, int smax) {
+                                  int* __restrict__ nstages, int k, int M, int nchunks, int smax, int SLOTS) {
     const int tile = blockIdx.x;
     const int KC = sp_chunk_rows(M);
     int* sl = slots + static_cast<int64_t>(tile) * smax;
@@ -704,12 +758,25 @@ __global__ void sp_compact_kernel(const int* __restrict__ tmp_slots, const uint8
     if (threadIdx.x == 0) nstages[tile] = padded / SLOTS;
 }
 
-// Weight images: one thread per (tile, stage, output row r of the tile).  Per quad: the (<= 2)
-// slots whose row the thread's group keeps -> 2 compressed values (A image, 64-B swizzled
-// K-major) + the metadata nibble (slot index of value 0 | slot index of value 1 << 2) at the
-// TMEM position of (row r, chunk) for tcgen05.mma.sp kind::f16:
-//   lane = r%8 + 8 (chunk/4 of the MMA) + 16 (r/16), bit = 16 ((r/8)%2) + 4 (chunk%4).
-__global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint8_t* __restrict__ D,
+// Weight images: one thread per (tile, stage, output row r of the tile).  Per packing unit (16 per
+// stage: quads for bf16, pairs for tf32): the slots whose row the thread's group keeps -> PG / 2
+// compressed values (A image, 64-B swizzled K-major) + the metadata nibble at the TMEM position of
+// (row r, chunk) for tcgen05.mma.sp (the same for kind::f16 and kind::tf32):
+//   lane = r%8 + 8 (chunk/4 of the MMA) + 16 (r/16), bit = 16 ((r/8)%2) + 4 (chunk%4);
+// nibble: bf16 slot index of value 0 | slot index of value 1 << 2; tf32 0x4 (slot 0) / 0xE (slot 1).
+// tf32 values are rounded to tf32 (RNA) here, offline; the MMA reads the top 19 bits.
+__device__ __forceinline__ void sp_store_val(uint8_t* p, float v, bool tf) {
+    if (tf) {
+        uint32_t r;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+        *reinterpret_cast<uint32_t*>(p) = r;
+    } else {
+        *reinterpret_cast<__nv_bfloat16*>(p) = __float2bfloat16_rn(v);
+    }
+}
+
+template <bool TF>
+__global__ void sp_image_kernel(const void* __restrict__ Bv_, const uint8_t* __restrict__ D,
                                 const int* __restrict__ slots, const uint8_t* __restrict__ stype,
                                 const int* __restrict__ nstages, uint8_t* __restrict__ wimg, int n, int k, int N, int M,
                                 int L, int smax, int max_stages, int H) {
@@ -730,25 +797,26 @@ __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint
     // metadata of the pair (st & ~1, st | 1) lives in the even stage's E block of this half
     uint32_t* meta = reinterpret_cast<uint32_t*>(wimg + (static_cast<int64_t>(tile) * max_stages + (st & ~1)) * H * WH_BYTES +
                                                  H * A_BYTES + hf * E_BYTES);
+    constexpr int SLOTS = El<TF>::SLOTS, PG = El<TF>::PG, NV = PG / 2, E = El<TF>::E;
     const int* sl = slots + static_cast<int64_t>(tile) * smax + st * SLOTS;
     const uint8_t* ty = stype + static_cast<int64_t>(tile) * smax + st * SLOTS;
-    for (int qd = 0; qd < SLOTS / 4; ++qd) {
+    for (int qd = 0; qd < SLOTS / PG; ++qd) {
         int pos[2] = {-1, -1};
         int npos = 0;
-        for (int i = 0; i < 4; ++i)
-            if (live && ((ty[4 * qd + i] >> gi) & 1)) pos[npos++] = i;
+        for (int i = 0; i < PG; ++i)
+            if (live && npos < NV && ((ty[PG * qd + i] >> gi) & 1)) pos[npos++] = i;
         // fill unused value positions with distinct unused slots (value 0)
-        for (int i = 0; npos < 2 && i < 4; ++i)
+        for (int i = 0; npos < NV && i < PG; ++i)
             if (i != pos[0]) pos[npos++] = i;
-        if (pos[0] > pos[1]) {
+        if (NV == 2 && pos[0] > pos[1]) {
             const int t = pos[0];
             pos[0] = pos[1];
             pos[1] = t;
         }
-        for (int e = 0; e < 2; ++e) {
-            __nv_bfloat16 v = __float2bfloat16(0.f);
-            const int kk = sl[4 * qd + pos[e]];
-            if (live && kk < k && ((ty[4 * qd + pos[e]] >> gi) & 1)) {
+        for (int e = 0; e < NV; ++e) {
+            float v = 0.f;
+            const int kk = sl[PG * qd + pos[e]];
+            if (live && kk < k && ((ty[PG * qd + pos[e]] >> gi) & 1)) {
                 const int t = kk / M, off = kk % M;
                 int lo = 0, hi = N - 1;  // D ascending within the window (R7)
                 while (lo < hi) {
@@ -756,19 +824,21 @@ __global__ void sp_image_kernel(const __nv_bfloat16* __restrict__ Bv, const uint
                     if (D[static_cast<int64_t>(t * N + mid) * q + g] < off) lo = mid + 1;
                     else hi = mid;
                 }
-                v = Bv[static_cast<int64_t>(t * N + lo) * n + j];
+                const int64_t vi = static_cast<int64_t>(t * N + lo) * n + j;
+                v = TF ? static_cast<const float*>(Bv_)[vi] : __bfloat162float(static_cast<const __nv_bfloat16*>(Bv_)[vi]);
             }
-            const int pidx = 2 * qd + e;  // compressed element of the row (0..31)
-            const int b = 2 * pidx;
+            const int pidx = NV * qd + e;  // compressed element of the row (32 bf16 / 16 tf32)
+            const int b = E * pidx;
             const int rr = r % 128;
             const int off = (rr / 8) * 512 + (rr % 8) * 64 + ((((b >> 4) ^ ((rr % 8) >> 1)) & 3) << 4) + (b & 15);
-            *reinterpret_cast<__nv_bfloat16*>(img + off) = v;
+            sp_store_val(img + off, v, TF);
         }
         const int rr = r % 128;
         const int mma = qd / 8, c = qd % 8;
         const int ln = (rr % 8) + 8 * (c / 4) + 16 * (rr / 16);
         const int bit = 16 * ((rr / 8) % 2) + 4 * (c % 4);
-        atomicOr(&meta[ln * 4 + 2 * (st & 1) + mma], static_cast<uint32_t>(pos[0] | (pos[1] << 2)) << bit);
+        const uint32_t nib = TF ? (pos[0] ? 0xEu : 0x4u) : static_cast<uint32_t>(pos[0] | (pos[1] << 2));
+        atomicOr(&meta[ln * 4 + 2 * (st & 1) + mma], nib << bit);
     }
 }
 
@@ -780,10 +850,11 @@ bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     return (L == 16 || L == 32 || L == 64 || L == 128) && n % 2 == 0 && k > 0 && k < (1 << 30) && M <= 256;
 }
 
-void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, size_t* off_slots, size_t* off_stype, size_t* off_nst,
-                 size_t* off_q, size_t* off_img, size_t* total, int* smax, int* max_stages) {
+void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, bool tf, size_t* off_slots, size_t* off_stype,
+                 size_t* off_nst, size_t* off_q, size_t* off_img, size_t* total, int* smax, int* max_stages) {
     using namespace tcs;
     const int H = sp_halves(L, N, M);
+    const int SLOTS = tf ? El<true>::SLOTS : El<false>::SLOTS;
     const int64_t ntiles = (n + 128 * H - 1) / (128 * H);
     const int64_t KC = sp_chunk_rows(M), nchunks = (k + KC - 1) / KC;
     const int64_t sm = ((2 * k + 4 * nchunks) + SLOTS - 1) / SLOTS * SLOTS;  // >= sum of chunk bounds
@@ -806,12 +877,12 @@ void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, size_t* off_slots, s
     *max_stages = static_cast<int>(sm / SLOTS);
 }
 
-nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, void* buf,
+nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, void* buf,
                         cudaStream_t s) {
     using namespace tcs;
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
-    tc_sp_sizes(n, k, N, M, L, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    tc_sp_sizes(n, k, N, M, L, tf, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
     uint8_t* b = static_cast<uint8_t*>(buf);
     const int mc = 128 * sp_halves(L, N, M);
     const int ntiles = static_cast<int>((n + mc - 1) / mc);
@@ -826,35 +897,36 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
                                        al(static_cast<size_t>(units * (2 * KC + 4)) * 5));
     sp_pack_kernel<<<static_cast<unsigned>(ceil_div(units, 32)), 32, 0, s>>>(
         D, reinterpret_cast<int*>(tsl), tty, ccnt, qk, static_cast<int>(n), static_cast<int>(k), N, M, L,
-        sp_halves(L, N, M), nchunks);
+        sp_halves(L, N, M), nchunks, tf ? El<true>::PG : El<false>::PG);
     note_launch();
     NM_LAUNCH_CHECK("sp_pack_kernel");
     sp_compact_kernel<<<static_cast<unsigned>(ntiles), 256, 0, s>>>(reinterpret_cast<const int*>(tsl), tty, ccnt,
                                                                    reinterpret_cast<int*>(b + os), b + ot,
                                                                    reinterpret_cast<int*>(b + on),
-                                                                   static_cast<int>(k), M, nchunks, smax);
+                                                                   static_cast<int>(k), M, nchunks, smax,
+                                                                   tf ? El<true>::SLOTS : El<false>::SLOTS);
     note_launch();
     NM_LAUNCH_CHECK("sp_compact_kernel");
     const int64_t threads = static_cast<int64_t>(ntiles) * mst * mc;
-    sp_image_kernel<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, s>>>(
-        static_cast<const __nv_bfloat16*>(Bv), D, reinterpret_cast<const int*>(b + os), b + ot,
-        reinterpret_cast<const int*>(b + on), b + oi, static_cast<int>(n), static_cast<int>(k), N, M, L, smax, mst,
-        sp_halves(L, N, M));
+    auto img = tf ? sp_image_kernel<true> : sp_image_kernel<false>;
+    img<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, s>>>(
+        Bv, D, reinterpret_cast<const int*>(b + os), b + ot, reinterpret_cast<const int*>(b + on), b + oi,
+        static_cast<int>(n), static_cast<int>(k), N, M, L, smax, mst, sp_halves(L, N, M));
     note_launch();
     NM_LAUNCH_CHECK("sp_image_kernel");
     return NM_OK;
 }
 
-template <int H, int NT>
-static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, int64_t n, cudaStream_t s) {
+template <int H, int NT, bool TF>
+static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n, cudaStream_t s) {
     using namespace tcs;
-    using CF = Cfg<H, NT>;
+    using CF = Cfg<H, NT, TF>;
     static bool attr = false;
     if (!attr) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         CF::SMEM_BYTES));
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         CF::SMEM_BYTES));
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false, TF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, true, TF>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         attr = true;
     }
     // C through TMA stores when its rows are 16-B aligned (the staged tile, NT/32 chunks of
@@ -911,9 +983,9 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
         la[0].val.clusterDim.z = 1;
         lc.attrs = la;
         lc.numAttrs = 1;
-        cudaLaunchKernelEx(&lc, spmm_tc_sp_kernel<H, NT, true>, at, tmC, tmC16, p);
+        cudaLaunchKernelEx(&lc, spmm_tc_sp_kernel<H, NT, true, TF>, at, tmC, tmC16, p);
     } else {
-        spmm_tc_sp_kernel<H, NT, false><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
+        spmm_tc_sp_kernel<H, NT, false, TF><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
     }
     prof_end(s);
     note_launch();
@@ -924,28 +996,56 @@ static nm_status sp_launch_h(const __nv_bfloat16* at, tcs::Params p, int64_t m, 
     return NM_OK;
 }
 
+template <bool TF>
+static nm_status sp_dispatch(int H, int nt, const void* at, const tcs::Params& p, int64_t m, int64_t n, cudaStream_t s) {
+    switch (H * 1000 + nt) {
+        case 2192: return sp_launch_h<2, 192, TF>(at, p, m, n, s);
+        case 2128: return sp_launch_h<2, 128, TF>(at, p, m, n, s);
+        case 2160: return sp_launch_h<2, 160, TF>(at, p, m, n, s);
+        case 2224: return sp_launch_h<2, 224, TF>(at, p, m, n, s);
+        case 2176: return sp_launch_h<2, 176, TF>(at, p, m, n, s);
+        case 2208: return sp_launch_h<2, 208, TF>(at, p, m, n, s);
+        case 1256: return sp_launch_h<1, 256, TF>(at, p, m, n, s);
+        case 1128: return sp_launch_h<1, 128, TF>(at, p, m, n, s);
+        case 1192: return sp_launch_h<1, 192, TF>(at, p, m, n, s);
+        default: return fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: unsupported (H, NT)");
+    }
+}
+
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M, int L,
-                    cudaStream_t s) {
+                    bool tf, cudaStream_t s) {
     using namespace tcs;
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
-    tc_sp_sizes(n, k, N, M, L, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    tc_sp_sizes(n, k, N, M, L, tf, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
     const uint8_t* b = static_cast<const uint8_t*>(buf);
     const int64_t mp = (m + 7) / 8 * 8;
-    __nv_bfloat16* at = nullptr;
+    const int eb = tf ? 4 : 2;
+    void* at = nullptr;
     // k + 1 rows: row k is zero, the source of the padding slots (kappa = k)
-    nm_status st = scratch_alloc(reinterpret_cast<void**>(&at), static_cast<size_t>((k + 1) * mp) * 2, s);
+    nm_status st = scratch_alloc(&at, static_cast<size_t>((k + 1) * mp) * eb, s);
     if (st) return st;
-    if (static_cast<uint64_t>(k + 1) * static_cast<uint64_t>(mp) * 2u >= (1ull << 32)) {
+    if (static_cast<uint64_t>(k + 1) * static_cast<uint64_t>(mp) * static_cast<uint64_t>(eb) >= (1ull << 32)) {
         cudaFreeAsync(at, s);
         return fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: A^T larger than 4 GiB (32-bit row offsets)");
     }
     const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(mp, 64)));
-    transpose_bf16_kernel<<<tg, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(A), at, static_cast<int>(m),
-                                             static_cast<int>(k), static_cast<int>(mp));
-    note_launch();
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) st = cuda_fail(e, "transpose_bf16_kernel");
+    cudaError_t e = cudaSuccess;
+    if (tf) {
+        // fp32 A^T by the SIMT path's transpose (tokens >= m written as zeros), then the zero row k
+        transpose_kernel<<<tg, 256, 0, s>>>(static_cast<const float*>(A), static_cast<float*>(at), static_cast<int>(m),
+                                            static_cast<int>(k), static_cast<int>(mp));
+        note_launch();
+        e = cudaGetLastError();
+        if (e == cudaSuccess)
+            e = cudaMemsetAsync(static_cast<float*>(at) + k * mp, 0, static_cast<size_t>(mp) * 4, s);
+    } else {
+        transpose_bf16_kernel<<<tg, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(A), static_cast<__nv_bfloat16*>(at),
+                                                 static_cast<int>(m), static_cast<int>(k), static_cast<int>(mp));
+        note_launch();
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) st = cuda_fail(e, "spmm_tc_sp transpose");
     if (!st) {
         Params p{};
         p.wimg = b + oi;
@@ -963,18 +1063,7 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
         p.dbg = dbg ? std::atoi(dbg) : 0;
 
         const int H = sp_halves(L, N, M), nt = sp_tokens(H, m, n);
-        switch (H * 1000 + nt) {
-            case 2192: st = sp_launch_h<2, 192>(at, p, m, n, s); break;
-            case 2128: st = sp_launch_h<2, 128>(at, p, m, n, s); break;
-            case 2160: st = sp_launch_h<2, 160>(at, p, m, n, s); break;
-            case 2224: st = sp_launch_h<2, 224>(at, p, m, n, s); break;
-            case 2176: st = sp_launch_h<2, 176>(at, p, m, n, s); break;
-            case 2208: st = sp_launch_h<2, 208>(at, p, m, n, s); break;
-            case 1256: st = sp_launch_h<1, 256>(at, p, m, n, s); break;
-            case 1128: st = sp_launch_h<1, 128>(at, p, m, n, s); break;
-            case 1192: st = sp_launch_h<1, 192>(at, p, m, n, s); break;
-            default: st = fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: unsupported (H, NT)");
-        }
+        st = tf ? sp_dispatch<true>(H, nt, at, p, m, n, s) : sp_dispatch<false>(H, nt, at, p, m, n, s);
     }
     e = cudaFreeAsync(at, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
@@ -986,21 +1075,21 @@ void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int*
     *tokens = tcs::sp_tokens(*halves, m, n);
 }
 
-size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L) {
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf) {
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
-    tc_sp_sizes(n, k, N, M, L, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    tc_sp_sizes(n, k, N, M, L, tf, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
     return tot;
 }
 
 // nm_spmm without a prepacked weight: prepack into pooled scratch, run, release.
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                       int64_t k, int N, int M, int L, cudaStream_t s) {
+                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s) {
     void* buf = nullptr;
-    nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k, N, M, L), s);
+    nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k, N, M, L, tf), s);
     if (st) return st;
-    st = tc_sp_prepack(Bv, D, n, k, N, M, L, buf, s);
-    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, s);
+    st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, buf, s);
+    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, tf, s);
     const cudaError_t e = cudaFreeAsync(buf, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;

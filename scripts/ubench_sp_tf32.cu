@@ -138,14 +138,14 @@ __global__ void __launch_bounds__(128, 1) sp_kernel(const __grid_constant__ CUte
                                (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
         for (int j = 0; j < 4; ++j) {
             const uint64_t ad = sdesc(su32(sA) + 32 * j, 16, 1024, 2);
-            const uint64_t bd = sdesc(su32(sB) + 2048 * j, K * 128, 1024, 2);
+            const uint64_t bd = sdesc(su32(sB) + 2048 * j, K * 128, 512, 1);
             const uint32_t acc = j ? 1u : 0u;
             if (a.mode & 4) {
                 // dense: A = first 8 physical columns (32 B) of each row = logical K 0..7 only; B rows 0..7
                 asm volatile(
                     "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-                    "l"(sdesc(su32(sA), 16, 1024, 2)), "l"(sdesc(su32(sB), K * 128, 1024, 2)), "r"(idesc), "r"(0u)
+                    "l"(sdesc(su32(sA), 16, 1024, 2)), "l"(sdesc(su32(sB), K * 128, 512, 1)), "r"(idesc), "r"(0u)
                     : "memory");
                 break;
             }
@@ -230,8 +230,10 @@ int run(int N, int mode, int probe, int box_rows, unsigned seed) {
     std::vector<uint8_t> bimg(K * N * 4, 0);
     for (int k = 0; k < K; ++k)
         for (int t = 0; t < N; ++t) {
+            // 32-bit MN-major operands take SWIZZLE_128B_BASE32B (descriptor layout 1): 32-B
+            // chunks of a 128-B row XOR (k % 4), 4-row groups (SBO 512), token atoms LBO apart
             const int b = (t % 32) * 4;
-            const int off = (t / 32) * (K * 128) + k * 128 + (((b >> 4) ^ (k % 8)) << 4) + (b & 15);
+            const int off = (t / 32) * (K * 128) + k * 128 + (((b >> 5) ^ (k % 4)) << 5) + (b & 31);
             memcpy(&bimg[off], &Xg[perm[k] * N + t], 4);
         }
     // metadata smem image for tcgen05.cp: lane-major rows of 16 B: word j of lane l = meta[j][l]

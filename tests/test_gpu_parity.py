@@ -457,3 +457,73 @@ def test_spmm_tc_sp_tail_split_on_off(nm, oracle, monkeypatch, tail, m, n, k, N,
     W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
     C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
+
+
+# --------------------------------------------------------------- tf32 sparse tensor cores (opt-in math)
+# Tolerance: A is read by the tensor core at tf32 precision (10 explicit mantissa bits, relative
+# error < 2^-10 per element), B' is rounded to tf32 offline (< 2^-11); the fp32 accumulation adds
+# the fp32 path's error.  The north star's 5e-3 relative Frobenius bound for tf32
+# holds with margin; integer inputs in {-2..2} are exact in tf32 and every partial sum is exact in
+# fp32, so they must match the oracle bit for bit.
+TF32_CASES = TC_CASES + SP_EDGE
+
+
+def run_tf32(nm, oracle, m, n, k, N, M, L, kind, seed):
+    A = synth.make(kind, (m, k), 141 + seed, synth.TID_A)
+    B = synth.make(kind, (k, n), 142 + seed, synth.TID_B)
+    vals, D = oracle.compress(B, N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A), W, math="tf32_tc").cpu().numpy()
+    return C, oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", TF32_CASES)
+def test_spmm_tc_tf32_vs_oracle(nm, oracle, m, n, k, N, M, L):
+    assert nm.nm_plan_query(m, n, k, N, M, L, torch.float32, "tf32_tc")["kernel"] == 3
+    C, ref = run_tf32(nm, oracle, m, n, k, N, M, L, "uniform", 0)
+    assert oracle.rel_frobenius(C, ref) <= TOL_BF16
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", TF32_CASES)
+def test_spmm_tc_tf32_integer_exact(nm, oracle, m, n, k, N, M, L):
+    C, ref = run_tf32(nm, oracle, m, n, k, N, M, L, "integer", 1)
+    assert np.array_equal(C.astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("nt", ["160", "176", "192", "208", "224"])
+def test_spmm_tc_tf32_token_tiles_all_rows(nm, oracle, monkeypatch, nt):
+    monkeypatch.setenv("NM_SP_NT", nt)
+    C, ref = run_tf32(nm, oracle, 650, 512, 256, 16, 32, 32, "integer", 2)
+    assert np.array_equal(C.astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("tail", ["0", "1"])
+@pytest.mark.parametrize("m,n,k,N,M,L", [(700, 768, 512, 16, 32, 32), (300, 640, 1024, 4, 32, 32)])
+def test_spmm_tc_tf32_tail_split_on_off(nm, oracle, monkeypatch, tail, m, n, k, N, M, L):
+    monkeypatch.setenv("NM_SP_TAIL", tail)
+    C, ref = run_tf32(nm, oracle, m, n, k, N, M, L, "integer", 3)
+    assert np.array_equal(C.astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3_75", "cfg4_65b"])
+def test_spmm_tc_tf32_full_size_sampled(nm, oracle, cfg):
+    m, n, k, N, M, L = {"cfg2": (4096, 4096, 4096, 16, 32, 32), "cfg3_75": (2048, 11008, 4096, 8, 32, 32),
+                        "cfg4_65b": (2048, 22016, 8192, 4, 32, 32)}[cfg]
+    A = synth.uniform((m, k), 151, synth.TID_A)
+    W = nm.nm_compress(dev(synth.uniform((k, n), 152, synth.TID_B)), N, M, L)
+    C = nm.nm_spmm(dev(A), W, math="tf32_tc")
+    rows = np.array([0, 3, 127, 128, m // 2 + 5, m - 1])
+    ref = oracle.spmm_sparse_f64(A, W.values.cpu().numpy(), W.idx.cpu().numpy(), k, N, M, L, rows=rows)
+    assert oracle.rel_frobenius(C[torch.from_numpy(rows).cuda()].cpu().numpy(), ref) <= TOL_BF16
+
+
+def test_spmm_tc_tf32_deterministic_and_opt_in(nm):
+    m, n, k, N, M, L = 512, 512, 1024, 8, 32, 32
+    A = dev(synth.uniform((m, k), 5, 1))
+    W = nm.nm_compress(dev(synth.uniform((k, n), 6, 2)), N, M, L)
+    assert torch.equal(nm.nm_spmm(A, W, math="tf32_tc"), nm.nm_spmm(A, W, math="tf32_tc"))
+    # AUTO keeps the paper's fp32 semantics (SIMT kernel); tf32 needs a slot-path geometry
+    assert nm.nm_plan_query(m, n, k, N, M, L, torch.float32)["kernel"] == 1
+    W8 = nm.nm_compress(dev(synth.uniform((64, 64), 7, 2)), 2, 4, 8)
+    with pytest.raises(nm.NmError):
+        nm.nm_spmm(dev(synth.uniform((16, 64), 8, 1)), W8, math="tf32_tc")
