@@ -41,7 +41,8 @@ CONFIGS = {
 }
 HEADLINE = "cfg2"
 VARIANTS = ["cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_13b:f32", "cfg4_65b:f32", "cfg3_62:bf16",
-            "cfg3_75:bf16", "cfg4_13b:bf16", "cfg4_65b:bf16"]
+            "cfg3_75:bf16", "cfg4_13b:bf16", "cfg4_65b:bf16", "cfg2:tf32", "cfg3_62:tf32", "cfg3_75:tf32",
+            "cfg4_65b:tf32"]  # tf32 = fp32 operands on the tf32 sparse tensor cores (opt-in math)
 
 
 def load_peaks():
@@ -124,12 +125,15 @@ def make_inputs(cfg, dtype, device, seed=0):
     return A, Bd, W
 
 
-def make_step(A, W, C, dtype):
-    '''One hot-path step.  fp32: nm_spmm (CUDA-core path).  bf16: the weight is prepacked
-    once, outside the timed region (the paper's offline PreProcessing), and
-    the step is nm_spmm_prepacked.'''
+def make_step(A, W, C, dtype, math=None):
+    '''One hot-path step.  fp32: nm_spmm (CUDA-core path).  bf16 and tf32 (fp32 operands,
+    math="tf32_tc"): the weight is prepacked once, outside the timed region (the paper's
+    offline PreProcessing), and the step is nm_spmm_prepacked.'''
     import torch
     from paper_2503_01253_b200 import nmspmm
+    if math == "tf32_tc":
+        PWt = nmspmm.nm_prepack(W, math="tf32_tc")
+        return lambda: nmspmm.nm_spmm_prepacked(A, PWt, out=C)
     if dtype == torch.float32:
         return lambda: nmspmm.nm_spmm(A, W, out=C, math="f32_simt")
     PW = nmspmm.nm_prepack(W)
@@ -166,13 +170,13 @@ def alg_bytes(cfg, e):
     return e * m * k + e * w * n + w * q + e * m * n
 
 
-def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True):
+def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True, math=None):
     import torch
     from paper_2503_01253_b200 import nmspmm
     stream = torch.cuda.current_stream()
     A, Bd, W = make_inputs(cfg, dtype, "cuda")
     C = torch.empty(cfg[0], cfg[1], dtype=dtype, device="cuda")
-    step = make_step(A, W, C, dtype)
+    step = make_step(A, W, C, dtype, math)
     for _ in range(warmup):
         step()
     nmspmm.nm_profile_begin()
@@ -182,7 +186,8 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True):
     kms = k_ms / max(1, k_cnt)
     res = {"ms": t, "tflops": flop_count(cfg) / (t * 1e-3) / 1e12, "kernel_ms": kms,
            "kernel_tflops": flop_count(cfg) / (kms * 1e-3) / 1e12, "launches_per_step": launches / steps,
-           "plan": nmspmm.nm_plan_query(*cfg, dtype=dtype, math="f32_simt" if dtype == torch.float32 else "auto")}
+           "plan": nmspmm.nm_plan_query(*cfg, dtype=dtype,
+                                        math=math or ("f32_simt" if dtype == torch.float32 else "auto"))}
     if with_cublas:
         torch.backends.cuda.matmul.allow_tf32 = False
         Cd = torch.empty_like(C)
@@ -191,6 +196,13 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True):
         m, n, k = cfg[:3]
         res.update({"cublas_ms": td, "cublas_dense_tflops": 2.0 * m * n * k / (td * 1e-3) / 1e12,
                     "speedup_vs_cublas": td / t, "target_speedup": 0.7 * cfg[4] / cfg[3]})
+        if math == "tf32_tc":  # the like-for-like dense comparator: cuBLAS with TF32 tensor cores
+            torch.backends.cuda.matmul.allow_tf32 = True
+            mst = time_steps(lambda: torch.mm(A, Bd, out=Cd), steps, warmup, stream, flush)
+            torch.backends.cuda.matmul.allow_tf32 = False
+            tt = statistics.fmean(mst)
+            res.update({"cublas_tf32_dense_tflops": 2.0 * m * n * k / (tt * 1e-3) / 1e12,
+                        "speedup_vs_cublas_tf32": tt / t})
     del A, Bd, W, C
     return res, ms
 
@@ -396,9 +408,12 @@ def run_ours(args):
             name, _, vdt = item.partition(":")
             vdt = vdt or args.dtype
             vcfg = CONFIGS[name]
-            tdt = torch.float32 if vdt == "f32" else torch.bfloat16
-            r, _ = measure_config(vcfg, tdt, max(5, args.steps // 2), args.warmup, flush)
-            peak_v = fp32_alu_peak_tflops(sm_mhz) if vdt == "f32" else peaks.get("bf16_tflops", 1590.0)
+            tdt = torch.bfloat16 if vdt == "bf16" else torch.float32
+            r, _ = measure_config(vcfg, tdt, max(5, args.steps // 2), args.warmup, flush,
+                                  math="tf32_tc" if vdt == "tf32" else None)
+            # tf32 dense peak = the measured bf16 peak x the nominal tf32/bf16 ratio 1/2
+            peak_v = (fp32_alu_peak_tflops(sm_mhz) if vdt == "f32" else
+                      peaks.get("bf16_tflops", 1590.0) / (2.0 if vdt == "tf32" else 1.0))
             variants.append({"config": name, "dtype": vdt, "m_n_k": vcfg[:3], "N:M": f"{vcfg[3]}:{vcfg[4]}",
                              "L": vcfg[5], "tflops": round(r["tflops"], 3), "ms": round(r["ms"], 4),
                              "kernel_tflops": round(r["kernel_tflops"], 3),
@@ -406,7 +421,10 @@ def run_ours(args):
                              "roofline_bound": "alu" if vdt == "f32" else "tensor",
                              "cublas_dense_tflops": round(r["cublas_dense_tflops"], 3),
                              "speedup_vs_cublas": round(r["speedup_vs_cublas"], 3),
-                             "target_speedup": round(r["target_speedup"], 3)})
+                             "target_speedup": round(r["target_speedup"], 3)}
+                            | ({"cublas_tf32_dense_tflops": round(r["cublas_tf32_dense_tflops"], 3),
+                                "speedup_vs_cublas_tf32": round(r["speedup_vs_cublas_tf32"], 3)}
+                               if "cublas_tf32_dense_tflops" in r else {}))
             torch.cuda.empty_cache()
         line["variants"] = variants
     print(json.dumps(line), flush=True)

@@ -123,7 +123,13 @@ nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, in
  *   idx    : w x q uint8 (must be valid; not re-checked on the hot path);
  *   C      : m x n, dtype c_dt, device, overwritten.
  *   ab_dt / c_dt / math:  NM_F32 + NM_MATH_F32_SIMT   -> fp32 FFMA, c_dt NM_F32
- *                         NM_F32 + NM_MATH_TF32_TC    -> NM_ERR_UNSUPPORTED (not built)
+ *                         NM_F32 + NM_MATH_TF32_TC    -> opt-in: fp32 operands on the tf32 sparse tensor
+ *                                                        cores (A read at tf32 precision, B' rounded to
+ *                                                        tf32 offline, fp32 accumulate, c_dt NM_F32) by the
+ *                                                        slot kernel with 1:2 slot pairs; needs L in
+ *                                                        {16,32,64,128}, k % 8 == 0, A 16-B and C 4-B
+ *                                                        aligned, else NM_ERR_UNSUPPORTED.  AUTO on fp32
+ *                                                        never picks it (it changes the numerics).
  *                         NM_BF16 + NM_MATH_BF16_TC   -> bf16 on the tensor cores, fp32 accumulate,
  *                                                        c_dt NM_BF16 (RNE) or NM_F32: the sparse-
  *                                                        tensor-core kernel (tcgen05.mma.sp over the
@@ -131,8 +137,8 @@ nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, in
  *                                                        k % 8 == 0, A 16-B and C 4-B aligned; else
  *                                                        the dense-MMA tcgen05 kernels or the generic one
  *                         NM_MATH_AUTO                -> selector (nm_plan_query)
- * bf16 without nm_prepack re-packs the weight on every call (ms); use
- * nm_prepack / nm_spmm_prepacked for repeated products with one weight.
+ * bf16 / tf32 without a prepack re-pack the weight on every call (ms); use
+ * nm_prepack (nm_prepack_ex for tf32) / nm_spmm_prepacked for repeated products with one weight.
  * No atomics on data: where a tile's k range is split over CTAs (fp32: grids below
  * one wave; bf16: the partial last wave) the partials are added in a fixed order,
  * so results are bit-reproducible run to run (R13).
@@ -192,7 +198,8 @@ nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, i
 typedef struct {
     int32_t magic;   /* 0x4B504D4E ("NMPK") once filled */
     int32_t kind;    /* 0 = plain (values/idx used directly), 1 = tcgen05 token-pair prepack,
-                        2 = sparse-tensor-core slot prepack (whole buffer at `bperm`) */
+                        2 = sparse-tensor-core slot prepack, bf16 (whole buffer at `bperm`),
+                        3 = the same for tf32 (fp32 weights, nm_prepack_ex with NM_MATH_TF32_TC) */
     int32_t dtype, N, M, L;
     int64_t n, k;
     int32_t bn, wp, bk, bkw, bkw_pad, npanels;
@@ -207,6 +214,14 @@ int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt)
 nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
                      void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
 nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt, void* stream);
+/* The same with the math the prepacked weight will run with: nm_prepack == nm_prepack_ex(...,
+ * NM_MATH_AUTO, ...).  dt NM_F32 + NM_MATH_TF32_TC gives kind 3 (tf32 slot images, 1:2 slot
+ * pairs, values rounded to tf32) when the tf32 path applies to the weight's shape, else kind 0;
+ * nm_spmm_prepacked on kind 3 runs the tf32 kernel (c_dt must be NM_F32) and reports
+ * NM_ERR_UNSUPPORTED where nm_spmm with NM_MATH_TF32_TC would. */
+int64_t nm_prepack_bytes_ex(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math);
+nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                        nm_math math, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
 
 /*
  * nm_profile_begin / nm_profile_end -- launch accounting for measurement

@@ -571,6 +571,11 @@ static bool prepack_kind1(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt
     tc_bf16_geometry(N, M, L, &g[0], &g[1], &g[2], &g[3], &g[4]);
     return tc_pair_applicable(1, n, k, N, M, L, g[4], g[3]);
 }
+// kind 3 iff the tf32 slot kernel is asked for and applies (aligned operands assumed)
+static bool prepack_kind3(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
+    static const float dummy[4] = {0, 0, 0, 0};
+    return dt == NM_F32 && math == NM_MATH_TF32_TC && k > 0 && tc_sp_ok(dummy, dummy, 1, n, k, N, M, L);
+}
 // kind 2 iff the sparse-tensor-core slot kernel would run (aligned operands assumed)
 static bool prepack_kind2(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
     static const float dummy[4] = {0, 0, 0, 0};
@@ -579,8 +584,9 @@ static bool prepack_kind2(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt
 }  // namespace nm
 extern "C" {
 
-int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
-    if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16) return -1;
+int64_t nm_prepack_bytes_ex(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
+    if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16 || math > NM_MATH_BF16_TC) return -1;
+    if (prepack_kind3(n, k, N, M, L, dt, math)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, true));
     if (prepack_kind2(n, k, N, M, L, dt)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, false));
     int g[5];
     if (!prepack_kind1(n, k, N, M, L, dt, g)) return 0;
@@ -589,12 +595,16 @@ int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt)
     return static_cast<int64_t>(al256(pb) + al256(tb) + al256(bb));
 }
 
-nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
-                     void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream) {
+int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
+    return nm_prepack_bytes_ex(n, k, N, M, L, dt, NM_MATH_AUTO);
+}
+
+nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                        nm_math math, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream) {
     nm_status st = check_common(0, n, k, N, M, L);
     if (st) return st;
     if (!out || (n * k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_prepack: NULL pointer");
-    if (dt > NM_BF16) return fail(NM_ERR_UNSUPPORTED, "dtype");
+    if (dt > NM_BF16 || math > NM_MATH_BF16_TC) return fail(NM_ERR_UNSUPPORTED, "dtype/math");
     *out = nm_prepacked{};
     out->dtype = dt;
     out->N = N;
@@ -605,7 +615,15 @@ nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t 
     out->values = values;
     out->idx = idx;
     int g[5];
-    if (prepack_kind2(n, k, N, M, L, dt)) {
+    if (prepack_kind3(n, k, N, M, L, dt, math)) {
+        const int64_t need = nm_prepack_bytes_ex(n, k, N, M, L, dt, math);
+        if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
+        if ((st = require_device())) return st;
+        out->kind = 3;
+        out->bperm = buf;
+        st = tc_sp_prepack(values, idx, n, k, N, M, L, true, buf, static_cast<cudaStream_t>(stream));
+        if (st) return st;
+    } else if (prepack_kind2(n, k, N, M, L, dt)) {
         const int64_t need = nm_prepack_bytes(n, k, N, M, L, dt);
         if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
         if ((st = require_device())) return st;
@@ -638,8 +656,24 @@ nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t 
     return NM_OK;
 }
 
+nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                     void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream) {
+    return nm_prepack_ex(values, idx, n, k, N, M, L, dt, NM_MATH_AUTO, buf, buf_bytes, out, stream);
+}
+
 nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt, void* stream) {
     if (!w || w->magic != kPrepackMagic) return fail(NM_ERR_NULL, "nm_spmm_prepacked: descriptor not filled by nm_prepack");
+    if (w->kind == 3) {  // tf32 slot images: the tf32 kernel or the same error nm_spmm gives
+        nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
+        if (st) return st;
+        if (c_dt != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
+        if (m == 0 || w->n == 0) return NM_OK;
+        if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
+        if ((st = require_device())) return st;
+        if (!tc_sp_ok(A, C, m, w->n, w->k, w->N, w->M, w->L))
+            return fail(NM_ERR_UNSUPPORTED, "tf32 sparse-tensor-core path needs A 16-B and C 4-B aligned");
+        return tc_sp_run(A, w->bperm, C, false, m, w->n, w->k, w->N, w->M, w->L, true, static_cast<cudaStream_t>(stream));
+    }
     if (w->kind == 2) {
         nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
         if (st) return st;

@@ -26,7 +26,8 @@ MATH = {"auto": 0, "f32_simt": 1, "tf32_tc": 2, "bf16_tc": 3}
 
 EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_decompress", "nm_validate",
            "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
-           "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked"]
+           "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked",
+           "nm_prepack_bytes_ex", "nm_prepack_ex"]
 
 
 class NmError(RuntimeError):
@@ -84,9 +85,12 @@ def lib():
         L.nm_prepack_bytes.restype = I64
         L.nm_prepack.argtypes = [P, P, I64, I64, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
         L.nm_spmm_prepacked.argtypes = [P, ctypes.POINTER(Prepacked), P, I64, I, P]
+        L.nm_prepack_bytes_ex.argtypes = [I64, I64, I, I, I, I, I]
+        L.nm_prepack_bytes_ex.restype = I64
+        L.nm_prepack_ex.argtypes = [P, P, I64, I64, I, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
         L.nm_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         for name in EXPORTS[2:]:
-            if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes"):
+            if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes", "nm_prepack_bytes_ex"):
                 getattr(L, name).restype = I
         _lib = L
     return _lib
@@ -200,16 +204,16 @@ class PrepackedWeight:
     '''A weight after nm_prepack (the paper's offline PreProcessing): keeps the
     original NmWeight (referenced by the descriptor), the device buffer and the descriptor.'''
 
-    def __init__(self, W: NmWeight, stream=None):
+    def __init__(self, W: NmWeight, stream=None, math: str = "auto"):
         self.W = W
         dt = _dt(W.values)
-        nbytes = lib().nm_prepack_bytes(W.n, W.k, W.N, W.M, W.L, dt)
+        nbytes = lib().nm_prepack_bytes_ex(W.n, W.k, W.N, W.M, W.L, dt, MATH[math])
         if nbytes < 0:
             raise NmError(2, "nm_prepack_bytes", "bad shape")
         self.buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=W.values.device)
         self.desc = Prepacked()
-        _check(lib().nm_prepack(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt,
-                                self.buf.data_ptr(), int(nbytes), ctypes.byref(self.desc), _stream(W.values, stream)),
+        _check(lib().nm_prepack_ex(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt, MATH[math],
+                                   self.buf.data_ptr(), int(nbytes), ctypes.byref(self.desc), _stream(W.values, stream)),
                "nm_prepack")
 
     @property
@@ -220,8 +224,9 @@ class PrepackedWeight:
         return getattr(self.W, name)
 
 
-def nm_prepack(W: NmWeight, stream=None) -> PrepackedWeight:
-    return PrepackedWeight(W, stream)
+def nm_prepack(W: NmWeight, stream=None, math: str = "auto") -> PrepackedWeight:
+    """math="tf32_tc" on an fp32 weight prepares the tf32 sparse-tensor-core path (kind 3)."""
+    return PrepackedWeight(W, stream, math)
 
 
 def nm_spmm_prepacked(A: torch.Tensor, PW: PrepackedWeight, out: torch.Tensor | None = None, out_dtype=None,

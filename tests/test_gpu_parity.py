@@ -527,3 +527,19 @@ def test_spmm_tc_tf32_deterministic_and_opt_in(nm):
     W8 = nm.nm_compress(dev(synth.uniform((64, 64), 7, 2)), 2, 4, 8)
     with pytest.raises(nm.NmError):
         nm.nm_spmm(dev(synth.uniform((16, 64), 8, 1)), W8, math="tf32_tc")
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", [(300, 384, 512, 16, 32, 32), (513, 384, 1024, 1, 32, 32),
+                                         (130, 256, 256, 8, 32, 16)])
+def test_spmm_tc_tf32_prepacked(nm, oracle, m, n, k, N, M, L):
+    """nm_prepack_ex(math=tf32_tc): kind 3 images; same bits as nm_spmm(math=tf32_tc)."""
+    A = synth.uniform((m, k), 161, synth.TID_A)
+    vals, D = oracle.compress(synth.uniform((k, n), 162, synth.TID_B), N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    PW = nm.nm_prepack(W, math="tf32_tc")
+    assert PW.kind == 3
+    C = nm.nm_spmm_prepacked(dev(A), PW)
+    assert torch.equal(C, nm.nm_spmm(dev(A), W, math="tf32_tc"))
+    ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)
+    assert oracle.rel_frobenius(C.cpu().numpy(), ref) <= TOL_BF16
+    assert nm.nm_prepack(W).kind == 0  # AUTO on fp32 keeps the SIMT path
