@@ -1,6 +1,6 @@
 #!/bin/bash
 # Full round check: build, smoke, all GPU tests, default bench, sharded path at world 1,
-# launch list, ncu of both SpMM kernels.
+# launch list, ncu of the SIMT, bf16 and tf32 SpMM kernels.
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
@@ -11,3 +11,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --cs
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --csv --log-file gpurun_out/launches_bf16.csv python bench.py --quick --dtype bf16 --steps 10 --warmup 3 > gpurun_out/launches_bf16.out 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_simt -s 3 -c 1 -o gpurun_out/prof_simt -f python bench.py --profile --steps 2 --warmup 3 > gpurun_out/ncu_simt.out 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_tc -s 3 -c 1 -o gpurun_out/prof_tc -f python bench.py --dtype bf16 --profile --steps 2 --warmup 3 > gpurun_out/ncu_tc.out 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_tc_sp -s 3 -c 1 -o gpurun_out/prof_tf32 -f python scripts/tf32_profile.py > gpurun_out/ncu_tf32.out 2>&1
