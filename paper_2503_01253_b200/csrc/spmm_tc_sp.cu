@@ -732,6 +732,146 @@ __global__ void sp_pack_kernel(const uint8_t* __restrict__ D, int* __restrict__ 
     chunk_cnt[gid] = ns;
 }
 
+// The same packing, one warp per (column tile, chunk), producing exactly the slot lists of
+// sp_pack_kernel (same bucket order, same pairs, same greedy choices and tie-breaks), ~40x
+// faster: the chunk's rows live in shared memory, rows are bucketed by a stable warp-wide
+// scatter (__match_any_sync ranks, rows in ascending order), the complementary pairs are
+// emitted lane-parallel, and each greedy pick is a warp max-reduction over the 2^G types
+// (key = popcount << 11 | items left, ties to the smaller type).  sp_pack_kernel stays as the
+// sequential reference (NM_SP_PACK_SEQ=1; the GPU tests compare the two byte for byte).
+constexpr int PACK_KC_MAX = 1280;  // >= sp_chunk_rows(M) for M <= 256
+__global__ void __launch_bounds__(32) sp_pack_warp_kernel(const uint8_t* __restrict__ D, int* __restrict__ tmp_slots,
+                                                          uint8_t* __restrict__ tmp_type, int* __restrict__ chunk_cnt,
+                                                          int n, int k, int N, int M, int L, int H, int nchunks, int PG) {
+    __shared__ int s_type[PACK_KC_MAX], s_qk[PACK_KC_MAX], s_start[257], s_head[256], s_off[257];
+    const int gid = blockIdx.x, lane = threadIdx.x;
+    const int MC = 128 * H;
+    const int tile = gid / nchunks, c = gid % nchunks;
+    const int KC = sp_chunk_rows(M);
+    const int r0 = c * KC, r1 = min(k, r0 + KC), rows = r1 - r0;
+    const int q = n / L, G = MC / L, g0 = tile * G;
+    const int gcount = min(G, q - g0);
+    const int T = 1 << G;
+    const int full = (1 << gcount) - 1;
+    int* sl = tmp_slots + static_cast<int64_t>(gid) * (2 * KC + 4);
+    uint8_t* ty = tmp_type + static_cast<int64_t>(gid) * (2 * KC + 4);
+    const unsigned all = 0xffffffffu;
+    // 1) membership masks (OR is order-independent)
+    for (int i = lane; i < rows; i += 32) s_type[i] = 0;
+    for (int t = lane; t <= T; t += 32) s_start[t] = 0;
+    __syncwarp();
+    const int nwin = rows / M, per_g = nwin * N;
+    for (int e = lane; e < gcount * per_g; e += 32) {
+        const int gi = e / per_g, rem = e - gi * per_g, tw = rem / N, sidx = rem - tw * N;
+        const int t = r0 / M + tw;
+        atomicOr(&s_type[t * M + D[static_cast<int64_t>(t * N + sidx) * q + g0 + gi] - r0], 1 << gi);
+    }
+    __syncwarp();
+    // 2) bucket sizes and starts
+    for (int i = lane; i < rows; i += 32) atomicAdd(&s_start[s_type[i] + 1], 1);
+    __syncwarp();
+    if (lane == 0)
+        for (int t = 0; t < T; ++t) s_start[t + 1] += s_start[t];
+    __syncwarp();
+    for (int t = lane; t < T; t += 32) s_head[t] = s_start[t];
+    __syncwarp();
+    // 3) stable scatter: rows in ascending order within each bucket
+    const unsigned lt = (1u << lane) - 1u;
+    for (int b0 = 0; b0 < rows; b0 += 32) {
+        const int i = b0 + lane;
+        const int tt = i < rows ? s_type[i] : -1;
+        const unsigned peers = __match_any_sync(all, tt);
+        if (tt >= 0) {
+            s_qk[s_head[tt] + __popc(peers & lt)] = r0 + i;
+        }
+        __syncwarp();
+        if (tt >= 0 && (peers & lt) == 0) s_head[tt] += __popc(peers);
+        __syncwarp();
+    }
+    for (int t = lane; t < T; t += 32) s_head[t] = s_start[t];
+    __syncwarp();
+    // 4) complementary pairs (t, ~t), t ascending: offsets by a (short, sequential) scan
+    for (int t = lane; t < T; t += 32) {
+        const int u = full ^ t;
+        int np = 0;
+        if (t >= 1 && u != 0 && t < u && !(t & ~full))
+            np = min(s_start[t + 1] - s_start[t], s_start[u + 1] - s_start[u]);
+        s_off[t] = np;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        int acc = 0;
+        for (int t = 0; t < T; ++t) {
+            const int np = s_off[t];
+            s_off[t] = acc;
+            acc += np;
+        }
+        s_off[T] = acc;
+    }
+    __syncwarp();
+    const int npairs = s_off[T];
+    for (int t = 1; t < T; ++t) {
+        const int np = s_off[t + 1] - s_off[t];  // t's pairs (u = full ^ t), 0 unless t < u
+        if (np == 0) continue;
+        const int u = full ^ t;
+        for (int j = lane; j < np; j += 32) {
+            const int o = 2 * (s_off[t] + j);
+            sl[o] = s_qk[s_start[t] + j], ty[o] = static_cast<uint8_t>(t);
+            sl[o + 1] = s_qk[s_start[u] + j], ty[o + 1] = static_cast<uint8_t>(u);
+        }
+        __syncwarp();
+        if (lane == 0) s_head[t] += np, s_head[u] += np;
+        __syncwarp();
+    }
+    int ns = 2 * npairs;
+    if (PG == 4 && (npairs & 1)) {  // an odd pair: its quad gets two padding slots
+        if (lane == 0) sl[ns] = k, ty[ns] = 0, sl[ns + 1] = k, ty[ns + 1] = 0;
+        ns += 2;
+    }
+    int remaining = rows - (s_start[1] - s_start[0]) - 2 * npairs;
+    // 5) greedy, one warp max-reduction per pick; lane owns types lane + 32 j
+    int left[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int t = lane + 32 * j;
+        left[j] = (t >= 1 && t < T) ? s_start[t + 1] - s_head[t] : 0;
+    }
+    while (remaining > 0) {
+        uint32_t once = 0, twice = 0;
+        int placed = 0;
+        for (int sidx = 0; sidx < PG; ++sidx) {
+            const uint32_t blocked = PG == 4 ? twice : once;
+            uint32_t mine = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t t = static_cast<uint32_t>(lane + 32 * j);
+                if (left[j] > 0 && !(t & blocked)) {
+                    const uint32_t key = ((static_cast<uint32_t>(__popc(t)) << 11 | static_cast<uint32_t>(left[j])) << 8) |
+                                         (255u - t);
+                    mine = key > mine ? key : mine;
+                }
+            }
+            const uint32_t best_key = __reduce_max_sync(all, mine);
+            if (best_key == 0) break;
+            const int best = 255 - static_cast<int>(best_key & 255u);
+            if ((best & 31) == lane) left[best >> 5]--;
+            if (lane == 0) {
+                sl[ns] = s_qk[s_head[best]++];
+                ty[ns] = static_cast<uint8_t>(best);
+            }
+            ++ns;
+            twice |= once & static_cast<uint32_t>(best);
+            once |= static_cast<uint32_t>(best);
+            --remaining;
+            ++placed;
+        }
+        if (lane == 0)
+            for (int pi = placed; pi < PG; ++pi) sl[ns + pi - placed] = k, ty[ns + pi - placed] = 0;
+        ns += PG - placed;
+    }
+    if (lane == 0) chunk_cnt[gid] = ns;
+}
+
 // Concatenate a tile's chunk slot lists (one block per tile), pad to whole stages of SLOTS slots.
 __global__ void sp_compact_kernel(const int* __restrict__ tmp_slots, const uint8_t* __restrict__ tmp_type,
                                   const int* __restrict__ chunk_cnt, int* __restrict__ slots, uint8_t* __restrict__ stype,
@@ -886,7 +1026,7 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
     uint8_t* b = static_cast<uint8_t*>(buf);
     const int mc = 128 * sp_halves(L, N, M);
     const int ntiles = static_cast<int>((n + mc - 1) / mc);
-    NM_CUDA_TRY(cudaMemsetAsync(b + oi, 0, tot - oi, s));
+    NM_CUDA_TRY(cudaMemsetAsync(b, 0, tot, s));  // slot lists past nstages and the images start zeroed
     const int KC = sp_chunk_rows(M), nchunks = static_cast<int>((k + KC - 1) / KC);
     const int64_t units = static_cast<int64_t>(ntiles) * nchunks;
     auto al = [](size_t x) { return (x + 255) / 256 * 256; };
@@ -895,9 +1035,15 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
     uint8_t* tty = tsl + static_cast<size_t>(units * (2 * KC + 4)) * 4;
     int* ccnt = reinterpret_cast<int*>(b + oq + al(static_cast<size_t>(units * KC) * 4) +
                                        al(static_cast<size_t>(units * (2 * KC + 4)) * 5));
-    sp_pack_kernel<<<static_cast<unsigned>(ceil_div(units, 32)), 32, 0, s>>>(
-        D, reinterpret_cast<int*>(tsl), tty, ccnt, qk, static_cast<int>(n), static_cast<int>(k), N, M, L,
-        sp_halves(L, N, M), nchunks, tf ? El<true>::PG : El<false>::PG);
+    const char* seq = std::getenv("NM_SP_PACK_SEQ");
+    if (seq && seq[0] == '1')
+        sp_pack_kernel<<<static_cast<unsigned>(ceil_div(units, 32)), 32, 0, s>>>(
+            D, reinterpret_cast<int*>(tsl), tty, ccnt, qk, static_cast<int>(n), static_cast<int>(k), N, M, L,
+            sp_halves(L, N, M), nchunks, tf ? El<true>::PG : El<false>::PG);
+    else
+        sp_pack_warp_kernel<<<static_cast<unsigned>(units), 32, 0, s>>>(
+            D, reinterpret_cast<int*>(tsl), tty, ccnt, static_cast<int>(n), static_cast<int>(k), N, M, L,
+            sp_halves(L, N, M), nchunks, tf ? El<true>::PG : El<false>::PG);
     note_launch();
     NM_LAUNCH_CHECK("sp_pack_kernel");
     sp_compact_kernel<<<static_cast<unsigned>(ntiles), 256, 0, s>>>(reinterpret_cast<const int*>(tsl), tty, ccnt,
@@ -907,6 +1053,9 @@ nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, 
                                                                    tf ? El<true>::SLOTS : El<false>::SLOTS);
     note_launch();
     NM_LAUNCH_CHECK("sp_compact_kernel");
+    // the pack scratch is dead from here on: clear it so a prepacked buffer is a pure function of
+    // the weight (the tests compare the warp-parallel and the sequential packer byte for byte)
+    NM_CUDA_TRY(cudaMemsetAsync(b + oq, 0, oi - oq, s));
     const int64_t threads = static_cast<int64_t>(ntiles) * mst * mc;
     auto img = tf ? sp_image_kernel<true> : sp_image_kernel<false>;
     img<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, s>>>(

@@ -543,3 +543,22 @@ def test_spmm_tc_tf32_prepacked(nm, oracle, m, n, k, N, M, L):
     ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)
     assert oracle.rel_frobenius(C.cpu().numpy(), ref) <= TOL_BF16
     assert nm.nm_prepack(W).kind == 0  # AUTO on fp32 keeps the SIMT path
+
+
+@pytest.mark.parametrize("dt", ["bf16", "tf32"])
+@pytest.mark.parametrize("k,n,N,M,L", [(4096, 4096, 16, 32, 32), (4096, 1024, 8, 32, 32), (8192, 768, 4, 32, 32),
+                                       (2048, 640, 12, 32, 16), (1536, 512, 3, 8, 64), (2048, 256, 5, 256, 128),
+                                       (1024, 384, 1, 32, 32)])
+def test_sp_pack_warp_matches_sequential(nm, monkeypatch, dt, k, n, N, M, L):
+    """The warp-parallel slot packer reproduces the sequential reference packer exactly (slot
+    lists, types, stage counts, weight and metadata images: the whole prepacked buffer)."""
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    gen = synth.bf16grid if dt == "bf16" else synth.uniform
+    W = nm.nm_compress(dev(gen((k, n), 171, synth.TID_B), tdt), N, M, L)
+    math = "tf32_tc" if dt == "tf32" else "auto"
+    fast = nm.nm_prepack(W, math=math)
+    monkeypatch.setenv("NM_SP_PACK_SEQ", "1")
+    ref = nm.nm_prepack(W, math=math)
+    torch.cuda.synchronize()
+    assert fast.kind == ref.kind == (3 if dt == "tf32" else 2)
+    assert torch.equal(fast.buf, ref.buf)
