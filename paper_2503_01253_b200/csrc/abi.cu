@@ -446,6 +446,27 @@ int64_t nm_spmm_host_ws_bytes(int64_t m, int64_t n, int64_t k, int N, int M, int
     return al(m * k * e) + al(w * n * e) + al(w * q) + al(m * n * ec);
 }
 
+}  // extern "C"
+namespace nm {
+// Row chunks for the host path's copy/compute overlap: fp32 SIMT only (the per-call prepack of
+// the tensor-core paths would be repeated per chunk); 4 chunks of whole 128-row tiles once m >=
+// 1024.  Measured on B200 (profiles/r01p_host_e2e_chunks.txt): 4 chunks beat 2 and 3 at cfg2
+// and cfg4-65B even where a chunk's grid ends in a partial wave -- the overlap gained exceeds
+// the quantization lost.  NM_HOST_CHUNKS=1..4 overrides (ablation).
+static int host_chunks(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab, nm_math math) {
+    const char* e = getenv("NM_HOST_CHUNKS");
+    int force = e ? atoi(e) : 0;
+    if (force < 0 || force > 4) force = 0;
+    static const float dummy[4] = {0, 0, 0, 0};
+    if (ab != NM_F32 || !(math == NM_MATH_AUTO || math == NM_MATH_F32_SIMT) ||
+        !simt_f32_applicable(dummy, dummy, dummy, m, n, k, N, M, L))
+        return 1;
+    if (force) return force;
+    return m >= 1024 ? 4 : 1;
+}
+}  // namespace nm
+extern "C" {
+
 nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_t* idx_host, void* C_host, int64_t m,
                        int64_t n, int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math,
                        void* dev_ws, void* stream) {
@@ -464,12 +485,60 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     uint8_t* dV = dA + al(m * k * e);
     uint8_t* dD = dV + al(w * n * e);
     uint8_t* dC = dD + al(w * q);
-    NM_CUDA_TRY(cudaMemcpyAsync(dA, A_host, static_cast<size_t>(m * k * e), cudaMemcpyHostToDevice, s));
     NM_CUDA_TRY(cudaMemcpyAsync(dV, values_host, static_cast<size_t>(w * n * e), cudaMemcpyHostToDevice, s));
     NM_CUDA_TRY(cudaMemcpyAsync(dD, idx_host, static_cast<size_t>(w * q), cudaMemcpyHostToDevice, s));
-    if ((st = nm_spmm(dA, dV, dD, dC, m, n, k, N, M, L, ab_dt, c_dt, math, stream))) return st;
-    NM_CUDA_TRY(cudaMemcpyAsync(C_host, dC, static_cast<size_t>(m * n * ec), cudaMemcpyDeviceToHost, s));
-    NM_CUDA_TRY(cudaStreamSynchronize(s));
+    const int nch = host_chunks(m, n, k, N, M, L, ab_dt, math);
+    if (nch == 1) {
+        NM_CUDA_TRY(cudaMemcpyAsync(dA, A_host, static_cast<size_t>(m * k * e), cudaMemcpyHostToDevice, s));
+        if ((st = nm_spmm(dA, dV, dD, dC, m, n, k, N, M, L, ab_dt, c_dt, math, stream))) return st;
+        NM_CUDA_TRY(cudaMemcpyAsync(C_host, dC, static_cast<size_t>(m * n * ec), cudaMemcpyDeviceToHost, s));
+        NM_CUDA_TRY(cudaStreamSynchronize(s));
+        return NM_OK;
+    }
+    // Row chunks of A / C, three-stage pipeline: H2D of chunk i+1 (copy stream) and D2H of chunk
+    // i-1 (second copy stream) overlap the SpMM of chunk i (the caller's stream).  Every chunk
+    // is the same product on a row range, so C is unchanged up to the k-split of sub-wave grids
+    // (fixed order).
+    const int64_t rc = ceil_div(ceil_div(m, nch), 128) * 128;
+    cudaStream_t hs = nullptr, ds = nullptr;
+    cudaEvent_t ev[2 * 4 + 1] = {};
+    auto cleanup = [&]() {
+        for (cudaEvent_t x : ev)
+            if (x) cudaEventDestroy(x);
+        if (hs) cudaStreamDestroy(hs);
+        if (ds) cudaStreamDestroy(ds);
+    };
+    cudaError_t ce = cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking);
+    for (int i = 0; ce == cudaSuccess && i < 2 * nch + 1; ++i) ce = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    for (int i = 0; ce == cudaSuccess && i < nch; ++i) {
+        const int64_t r0 = i * rc, r1 = std::min(m, r0 + rc);
+        if (r0 >= r1) break;
+        ce = cudaMemcpyAsync(dA + r0 * k * e, static_cast<const uint8_t*>(A_host) + r0 * k * e,
+                             static_cast<size_t>((r1 - r0) * k * e), cudaMemcpyHostToDevice, hs);
+        if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i], hs);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * i], 0);
+        if (ce != cudaSuccess) break;
+        if ((st = nm_spmm(dA + r0 * k * e, dV, dD, dC + r0 * n * ec, r1 - r0, n, k, N, M, L, ab_dt, c_dt, math, stream))) {
+            cudaStreamSynchronize(s);
+            cudaStreamSynchronize(hs);
+            cleanup();
+            return st;
+        }
+        ce = cudaEventRecord(ev[2 * i + 1], s);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ds, ev[2 * i + 1], 0);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(static_cast<uint8_t*>(C_host) + r0 * n * ec, dC + r0 * n * ec,
+                                 static_cast<size_t>((r1 - r0) * n * ec), cudaMemcpyDeviceToHost, ds);
+    }
+    if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * nch], ds);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * nch], 0);  // the caller's stream sees C_host
+    const cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamSynchronize(hs);
+    cudaStreamSynchronize(ds);
+    cleanup();
+    if (ce != cudaSuccess) return cuda_fail(ce, "nm_spmm_host pipeline");
+    if (se != cudaSuccess) return cuda_fail(se, "nm_spmm_host");
     return NM_OK;
 }
 
