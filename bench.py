@@ -448,7 +448,7 @@ def run_sharded(args):
     dtype = torch.float32 if args.dtype == "f32" else torch.bfloat16
     m, n, k, N, M, L = cfg
     A, Bd, _ = make_inputs(cfg, dtype, "cuda")  # A replicated (column-parallel input), B generated identically
-    layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD)
+    layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD, exchange=args.exchange)
     del Bd
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     flush = (lambda: flush_buf.fill_(1.0)) if not args.no_flush else None
@@ -492,8 +492,9 @@ def run_sharded(args):
                 "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-                "config": config_dict(cfg, args.dtype, {"parallelism": f"col{world} (column groups sharded, "
-                                                                        "NCCL all-gather of C)"}),
+                "config": config_dict(cfg, args.dtype, {"parallelism": f"col{world} (column groups sharded, " + (
+                    "NCCL all-gather of C)" if args.exchange == "nccl" else
+                    "fused peer-store epilogue over CUDA IPC / NVLink + flag barrier)")}),
                 "gpu_launches": int(launches), "clocks": sampler.summary(),
                 "roofline": {"bound": "alu" if dtype == torch.float32 else "tensor", "achieved": round(ach, 3),
                              "peak": round(peak, 2), "unit": "TFLOP/s", "frac": round(ach / peak, 4),
@@ -503,7 +504,7 @@ def run_sharded(args):
                         "unit": "TFLOP/s (effective, kept MACs)", "ms_per_step": round(te.item(), 4),
                         "h2d_bytes_per_step": int(Ah.numel() * Ah.element_size()),
                         "d2h_bytes_per_step": int(Ch.numel() * Ch.element_size()),
-                        "path": "pinned A -> each rank, sharded layer (NCCL all-gather), C -> host on rank 0"},
+                        "path": f"pinned A -> each rank, sharded layer ({args.exchange} exchange), C -> host on rank 0"},
                 "kernel_only_tflops_all_ranks": round(flop_count(cfg) / (t_kernel * 1e-3) / 1e12, 4),
                 "allgather_floor_ms": round((world - 1) / world * m * n * A.element_size() / 770e9 * 1e3, 4)}
         print(json.dumps(line), flush=True)
@@ -526,6 +527,8 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="column-sharded path even at one rank (testing)")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
+                    help="sharded path: NCCL all-gather + unshard, or the fused peer-store epilogue (fp32)")
     args = ap.parse_args()
     if args.warmup < 3 and not args.profile:
         args.warmup = 3

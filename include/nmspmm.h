@@ -227,6 +227,39 @@ nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64
                         nm_math math, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
 
 /*
+ * Fused multi-GPU exchange of the column-sharded layer.  Column j of C
+ * depends only on A, B'[:, j], D[:, j / L] (Eq. 1), so rank r of G computes the columns
+ * of its group shard and, instead of an all-gather + unshard pass, the SpMM epilogue stores
+ * them straight into every rank's C buffer through peer mappings (NVLink); a flag barrier in
+ * peer memory then orders the ranks, stream-ordered, no host synchronisation.
+ *
+ *   nm_ipc_get_handle : CUDA IPC handle (64 bytes, written to `handle`) of the allocation that
+ *                       contains device pointer `dptr`, and dptr's byte offset in it.
+ *   nm_ipc_open_handle: maps another process's handle; *dptr = its base + offset.  (A
+ *                       process cannot open its own handle: use the local pointer.)
+ *   nm_ipc_close      : unmaps (dptr, offset as returned by nm_ipc_open_handle).
+ *   nm_spmm_peers     : C_p[i][col_off + j] = (A . decompress(values, idx))[i][j] for every p <
+ *                       G, i < m, j < n_valid (the shard's unpadded columns; nr = its padded
+ *                       width, values w x nr, idx w x nr/L); C_p are device pointers valid in
+ *                       this process (own buffer or IPC-mapped peers), row pitch ldc floats.
+ *                       fp32 operands on the SIMT kernel (16-B aligned, ldc and col_off
+ *                       multiples of 4), else NM_ERR_UNSUPPORTED.  Asynchronous.
+ *   nm_peer_barrier   : flag_peers[p] = rank p's int[G] flag array (mapped here); publishes
+ *                       `epoch` in every rank's flags[rank] (system-scope release after the
+ *                       stream's earlier work, i.e. after this rank's peer stores) and waits on
+ *                       the stream until every rank has published `epoch` in ours.  Epochs
+ *                       must increase by one per call on all ranks; a rank that never arrives
+ *                       makes the kernel trap after ~2^26 polls instead of hanging.  1 <= G <= 8.
+ */
+nm_status nm_ipc_get_handle(const void* dptr, void* handle, int64_t* offset);
+nm_status nm_ipc_open_handle(const void* handle, int64_t offset, void** dptr);
+nm_status nm_ipc_close(void* dptr, int64_t offset);
+nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, void* const* C_peers, int G,
+                        int64_t ldc, int64_t col_off, int64_t n_valid, int64_t m, int64_t nr, int64_t k, int N,
+                        int M, int L, void* stream);
+nm_status nm_peer_barrier(void* const* flag_peers, int G, int rank, int epoch, void* stream);
+
+/*
  * nm_profile_begin / nm_profile_end -- launch accounting for measurement
  * (bench.py).  Between the two calls the library counts every kernel it
  * launches and records a CUDA event pair on the launching stream around each

@@ -52,7 +52,7 @@ int num_sms() {
     return g_num_sms > 0 ? g_num_sms : 148;
 }
 
-static nm_status require_device() {
+nm_status require_device() {  // also used by peer.cu
     int n = 0;
     cudaError_t e = cudaGetDeviceCount(&n);
     if (e != cudaSuccess || n == 0) {
@@ -201,7 +201,7 @@ bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s);
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr);
 bool simt_pipe_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 nm_status simt_pipe_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                            int N, int M, int L, cudaStream_t s);

@@ -40,6 +40,15 @@ void note_launch();
 void prof_begin(cudaStream_t s);
 void prof_end(cudaStream_t s);
 
+// Peer-store destinations of the fused column all-gather (nm_spmm_peers): up to 8 ranks'
+// C buffers (device pointers valid in this process: own or IPC-opened), row pitch ldc,
+// this shard's first global column col_off, its n_valid real (unpadded) columns.
+struct PeerOut {
+    float* c[8];
+    int np;
+    int64_t ldc, col_off, n_valid;
+};
+
 // TMA descriptor encoding (cuTensorMapEncodeTiled fetched via cudaGetDriverEntryPoint).
 // 2-D row-major tensor [rows][cols] of elem_bytes elements; box [box_rows][box_cols].
 // swizzle: 0 none, 128 = 128-byte swizzle.  OOB elements are zero-filled.

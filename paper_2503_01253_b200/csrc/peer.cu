@@ -1,0 +1,150 @@
+// peer.cu -- the multi-GPU exchange of the column-sharded layer fused into
+// the SpMM: every rank's SpMM epilogue stores its C columns straight into every rank's C buffer
+// over NVLink peer memory (CUDA IPC mappings), then a flag barrier in peer memory orders the
+// ranks -- no separate all-gather pass and no unshard pass.  Column j of C depends only on A,
+// B'[:, j] and D[:, j / L] (Eq. 1), so the ranks' stores never overlap.
+#include <cstdint>
+#include <cstring>
+
+#include "common.cuh"
+
+namespace nm {
+
+nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po);
+bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
+                         int L);
+nm_status require_device();
+
+struct PeerFlags {
+    int* f[8];  // f[p] = rank p's flag array (int[G]) as mapped in this process
+};
+
+// One warp.  Lane p < G: publish "rank `rank` reached `epoch`" in rank p's flags (system-scope
+// release after a system fence, so this rank's earlier peer stores -- the SpMM kernel before
+// this one on the stream -- are visible to whoever acquires the flag), then wait until rank p
+// has published the same epoch in ours.  Bounded spin: a missing rank is a bug, trap, do not hang.
+__global__ void peer_barrier_kernel(PeerFlags pf, int G, int rank, int epoch) {
+    const int t = threadIdx.x;
+    if (t < G) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(pf.f[t] + rank), "r"(epoch) : "memory");
+    }
+    __syncwarp();
+    if (t < G) {
+        const int* mine = pf.f[rank] + t;
+        for (long long spin = 0;; ++spin) {
+            int v;
+            asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
+            if (v - epoch >= 0) break;  // epochs increase by one per call (wrap-safe compare)
+            __nanosleep(128);
+            if (spin > (1ll << 26)) __trap();
+        }
+    }
+}
+
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+static AddrRangeFn get_addr_range() {
+    static AddrRangeFn fn = nullptr;
+    static bool done = false;
+    if (!done) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<AddrRangeFn>(p);
+        cudaGetLastError();
+        done = true;
+    }
+    return fn;
+}
+
+}  // namespace nm
+
+using namespace nm;
+
+extern "C" {
+
+nm_status nm_ipc_get_handle(const void* dptr, void* handle, int64_t* offset) {
+    if (!dptr || !handle || !offset) return fail(NM_ERR_NULL, "nm_ipc_get_handle: NULL pointer");
+    nm_status st = require_device();
+    if (st) return st;
+    AddrRangeFn fn = get_addr_range();
+    if (!fn) return fail(NM_ERR_CUDA, "cuMemGetAddressRange unavailable");
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(dptr)) != CUDA_SUCCESS)
+        return fail(NM_ERR_CUDA, "cuMemGetAddressRange failed (not a device allocation?)");
+    NM_CUDA_TRY(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle), reinterpret_cast<void*>(base)));
+    *offset = static_cast<int64_t>(reinterpret_cast<CUdeviceptr>(dptr) - base);
+    return NM_OK;
+}
+
+nm_status nm_ipc_open_handle(const void* handle, int64_t offset, void** dptr) {
+    if (!handle || !dptr) return fail(NM_ERR_NULL, "nm_ipc_open_handle: NULL pointer");
+    nm_status st = require_device();
+    if (st) return st;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    void* base = nullptr;
+    NM_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *dptr = static_cast<uint8_t*>(base) + offset;
+    return NM_OK;
+}
+
+nm_status nm_ipc_close(void* dptr, int64_t offset) {
+    if (!dptr) return fail(NM_ERR_NULL, "nm_ipc_close: NULL pointer");
+    NM_CUDA_TRY(cudaIpcCloseMemHandle(static_cast<uint8_t*>(dptr) - offset));
+    return NM_OK;
+}
+
+nm_status nm_peer_barrier(void* const* flag_peers, int G, int rank, int epoch, void* stream) {
+    if (G < 1 || G > 8 || rank < 0 || rank >= G) return fail(NM_ERR_SHAPE, "nm_peer_barrier: 1 <= G <= 8, 0 <= rank < G");
+    if (!flag_peers) return fail(NM_ERR_NULL, "nm_peer_barrier: NULL pointer");
+    PeerFlags pf{};
+    for (int i = 0; i < G; ++i) {
+        if (!flag_peers[i]) return fail(NM_ERR_NULL, "nm_peer_barrier: NULL flag pointer");
+        pf.f[i] = static_cast<int*>(flag_peers[i]);
+    }
+    nm_status st = require_device();
+    if (st) return st;
+    peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(pf, G, rank, epoch);
+    note_launch();
+    NM_LAUNCH_CHECK("peer_barrier_kernel");
+    return NM_OK;
+}
+
+nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, void* const* C_peers, int G, int64_t ldc,
+                        int64_t col_off, int64_t n_valid, int64_t m, int64_t nr, int64_t k, int N, int M, int L,
+                        void* stream) {
+    if (N < 1 || M < N || M > 256 || L < 1) return fail(NM_ERR_INVALID_CONFIG, "invalid N:M/L");
+    if (m < 0 || nr < 0 || k < 0 || k % M || nr % L) return fail(NM_ERR_SHAPE, "nm_spmm_peers: shape");
+    if (G < 1 || G > 8) return fail(NM_ERR_SHAPE, "nm_spmm_peers: 1 <= G <= 8");
+    if (col_off < 0 || n_valid < 0 || n_valid > nr || col_off + n_valid > ldc)
+        return fail(NM_ERR_SHAPE, "nm_spmm_peers: columns [col_off, col_off + n_valid) outside ldc, or n_valid > nr");
+    if (m == 0 || nr == 0 || n_valid == 0) return NM_OK;
+    if (!A || !C_peers || (k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_spmm_peers: NULL pointer");
+    PeerOut po{};
+    po.np = G;
+    po.ldc = ldc;
+    po.col_off = col_off;
+    po.n_valid = n_valid;
+    uintptr_t al = static_cast<uintptr_t>(ldc | col_off) * 4u;
+    for (int i = 0; i < G; ++i) {
+        if (!C_peers[i]) return fail(NM_ERR_NULL, "nm_spmm_peers: NULL C pointer");
+        po.c[i] = static_cast<float*>(C_peers[i]);
+        al |= reinterpret_cast<uintptr_t>(C_peers[i]);
+    }
+    // the fused path is the fp32 SIMT kernel's epilogue: 16-B stores at [row][col_off + col]
+    if (k == 0 || (al & 15) || !simt_f32_applicable(A, values, po.c[0], m, nr, k, N, M, L))
+        return fail(NM_ERR_UNSUPPORTED, "nm_spmm_peers: needs the fp32 SIMT kernel's geometry (L % 4 == 0, M <= 64, "
+                                        "N <= 32, k > 0, 16-B aligned operands, ldc and col_off multiples of 4)");
+    nm_status st = require_device();
+    if (st) return st;
+    const int mode = m % 4 == 0 ? 1 : 0;  // A^T staging needs m % 4 == 0 (as in the selector)
+    return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx, po.c[0], m, nr, k, N,
+                           M, L, mode, static_cast<cudaStream_t>(stream), &po);
+}
+
+}  // extern "C"

@@ -52,6 +52,12 @@ struct Params {
     int ntn, full_tiles, split;
     float* ws;
     int* counters;
+    // peer-store epilogue (nm_spmm_peers): the C tile goes to cpeer[0 .. npeer) at
+    // [row][col_off + col] (row pitch ldc), columns < n_valid only -- the column all-gather of a
+    // sharded layer fused into the SpMM's stores over NVLink peer memory.  npeer = 0: C.
+    float* cpeer[8];
+    int npeer, n_valid;
+    int64_t ldc, col_off;
 };
 
 // Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
@@ -303,6 +309,21 @@ __global__ void __launch_bounds__(THREADS, 2)
 
     // epilogue: registers -> global (float4 stores, guarded for ragged m / n)
     const int gc0 = n0 + col0;
+    if (p.npeer) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int row = m0 + wm * 64 + (AT ? (i & 3) + 4 * t_m + 32 * (i >> 2) : 8 * i + t_m);
+            if (row >= p.m) continue;
+            for (int pi = 0; pi < p.npeer; ++pi) {
+                float* crow = p.cpeer[pi] + static_cast<int64_t>(row) * p.ldc + p.col_off;
+                if (gc0 < p.n_valid)
+                    *reinterpret_cast<float4*>(crow + gc0) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                if (gc0 + 16 < p.n_valid)
+                    *reinterpret_cast<float4*>(crow + gc0 + 16) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int row = m0 + wm * 64 + (AT ? (i & 3) + 4 * t_m + 32 * (i >> 2) : 8 * i + t_m);
@@ -410,11 +431,18 @@ static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, con
 // mode: 0 = A panels straight from A (swizzled [m][k] boxes), 1 = A^T staged (tile TMA),
 // 2 = A^T staged + packed col_info loads (high sparsity).  The selector decides.
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s) {
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po) {
     using namespace simt;
     Params p{};
     p.D = D;
     p.C = C;
+    if (po) {
+        p.npeer = po->np;
+        for (int i = 0; i < po->np && i < 8; ++i) p.cpeer[i] = po->c[i];
+        p.ldc = po->ldc;
+        p.col_off = po->col_off;
+        p.n_valid = static_cast<int>(po->n_valid);
+    }
     p.m = static_cast<int>(m);
     p.n = static_cast<int>(n);
     p.k = static_cast<int>(k);

@@ -27,7 +27,8 @@ MATH = {"auto": 0, "f32_simt": 1, "tf32_tc": 2, "bf16_tc": 3}
 EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_decompress", "nm_validate",
            "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
            "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked",
-           "nm_prepack_bytes_ex", "nm_prepack_ex"]
+           "nm_prepack_bytes_ex", "nm_prepack_ex", "nm_ipc_get_handle", "nm_ipc_open_handle", "nm_ipc_close",
+           "nm_spmm_peers", "nm_peer_barrier"]
 
 
 class NmError(RuntimeError):
@@ -89,6 +90,11 @@ def lib():
         L.nm_prepack_bytes_ex.restype = I64
         L.nm_prepack_ex.argtypes = [P, P, I64, I64, I, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
         L.nm_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), ctypes.POINTER(I64)]
+        L.nm_ipc_get_handle.argtypes = [P, P, ctypes.POINTER(I64)]
+        L.nm_ipc_open_handle.argtypes = [P, I64, ctypes.POINTER(P)]
+        L.nm_ipc_close.argtypes = [P, I64]
+        L.nm_spmm_peers.argtypes = [P, P, P, ctypes.POINTER(P), I, I64, I64, I64, I64, I64, I64, I, I, I, P]
+        L.nm_peer_barrier.argtypes = [ctypes.POINTER(P), I, I, I, P]
         for name in EXPORTS[2:]:
             if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes", "nm_prepack_bytes_ex"):
                 getattr(L, name).restype = I
@@ -289,3 +295,46 @@ def nm_unshard_columns(src: torch.Tensor, dst: torch.Tensor, G: int, m: int, nr:
     _check(lib().nm_unshard_columns(src.data_ptr(), dst.data_ptr(), G, m, nr, n, L, src.element_size(),
                                     _stream(src, stream)), "nm_unshard_columns")
     return dst
+
+
+# ----------------------------------------------------------------------------- fused peer exchange
+def nm_ipc_get_handle(t: torch.Tensor) -> tuple[bytes, int]:
+    """(64-byte CUDA IPC handle of t's allocation, byte offset of t in it)."""
+    h = ctypes.create_string_buffer(64)
+    off = ctypes.c_int64()
+    _check(lib().nm_ipc_get_handle(t.data_ptr(), h, ctypes.byref(off)), "nm_ipc_get_handle")
+    return h.raw, int(off.value)
+
+
+def nm_ipc_open_handle(handle: bytes, offset: int) -> int:
+    """Map another process's allocation; returns the device address of (its base + offset)."""
+    p = ctypes.c_void_p()
+    _check(lib().nm_ipc_open_handle(ctypes.create_string_buffer(handle, 64), offset, ctypes.byref(p)),
+           "nm_ipc_open_handle")
+    return int(p.value)
+
+
+def nm_ipc_close(ptr: int, offset: int) -> None:
+    _check(lib().nm_ipc_close(ctypes.c_void_p(ptr), offset), "nm_ipc_close")
+
+
+def _ptr_array(ptrs):
+    arr = (ctypes.c_void_p * len(ptrs))()
+    for i, v in enumerate(ptrs):
+        arr[i] = v
+    return arr
+
+
+def nm_spmm_peers(A: torch.Tensor, W: NmWeight, c_ptrs, ldc: int, col_off: int, n_valid: int, stream=None) -> None:
+    """Fused sharded product: this shard's C columns [0, n_valid) stored at [row][col_off + j] of
+    every buffer in c_ptrs (own or IPC-mapped device addresses, row pitch ldc)."""
+    _dev(A, "A")
+    m, k = A.shape
+    _check(lib().nm_spmm_peers(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), _ptr_array(c_ptrs), len(c_ptrs),
+                               ldc, col_off, n_valid, m, W.n, k, W.N, W.M, W.L, _stream(A, stream)), "nm_spmm_peers")
+
+
+def nm_peer_barrier(flag_ptrs, rank: int, epoch: int, device=None, stream=None) -> None:
+    s = ctypes.c_void_p(stream.cuda_stream) if stream is not None else \
+        ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    _check(lib().nm_peer_barrier(_ptr_array(flag_ptrs), len(flag_ptrs), rank, epoch, s), "nm_peer_barrier")

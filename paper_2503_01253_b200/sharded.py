@@ -7,6 +7,15 @@ ceil(q/G) groups (zero values, a valid index pattern) so that the NCCL
 all-gather moves equal-size [m][nr] blocks; nm_unshard_columns (our kernel)
 drops the padding and writes the m x n row-major C.  A is replicated (the
 input of a column-parallel layer).  No reduction is needed.
+
+exchange="p2p" fuses the exchange into the SpMM (fp32): the ranks' C buffers are
+mapped into every process by CUDA IPC, each rank's SpMM epilogue stores its
+columns into all of them over NVLink (nm_spmm_peers), and a flag barrier in
+peer memory (nm_peer_barrier) orders the ranks -- stream-ordered, no all-gather
+pass, no unshard pass.  The C buffers are double-buffered: the tensor returned
+by call i stays valid for work this rank enqueues on its stream before its call
+i + 1 (the peers overwrite it in call i + 2, which they start only after call
+i + 1's barrier has seen this rank's stream reach call i + 1).
 """
 from __future__ import annotations
 
@@ -37,22 +46,69 @@ def shard_weight(values: torch.Tensor, idx: torch.Tensor, L: int, N: int, rank: 
     return v.contiguous(), d.contiguous()
 
 
-class ShardedNmLinear:
-    """y = x . B~ with B~'s column groups sharded over a process group (NCCL)."""
+class PeerExchange:
+    """Per-layer peer mappings for exchange="p2p": two C buffers (m x n) and one int[G] flag
+    array per rank, allocated by torch, exported by CUDA IPC, exchanged with
+    all_gather_object over the group and opened in every other process."""
 
-    def __init__(self, local_weight, n: int, group=None):
+    def __init__(self, group, m: int, n: int, dtype, device):
         from . import nmspmm
+        self.G, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        self.m, self.n = m, n
+        self.C = [torch.empty((m, n), dtype=dtype, device=device) for _ in range(2)]
+        self.flags = torch.zeros(self.G, dtype=torch.int32, device=device)
+        torch.cuda.synchronize(device)  # zeroed flags before any peer can write them
+        mine = [nmspmm.nm_ipc_get_handle(t) for t in (self.C[0], self.C[1], self.flags)]
+        allh = [None] * self.G
+        dist.all_gather_object(allh, mine, group=group)
+        self.opened = []  # (ptr, offset) to close
+        self.ptrs = [[0] * self.G for _ in range(3)]  # [buffer][rank]
+        for r in range(self.G):
+            for b in range(3):
+                if r == self.rank:
+                    self.ptrs[b][r] = (self.C[0], self.C[1], self.flags)[b].data_ptr()
+                else:
+                    h, off = allh[r][b]
+                    ptr = nmspmm.nm_ipc_open_handle(h, off)
+                    self.opened.append((ptr, off))
+                    self.ptrs[b][r] = ptr
+        self.epoch = 0
+        dist.barrier(group=group)  # every rank mapped before anyone stores
+
+    def close(self):
+        from . import nmspmm
+        for ptr, off in self.opened:
+            nmspmm.nm_ipc_close(ptr, off)
+        self.opened = []
+
+
+class ShardedNmLinear:
+    """y = x . B~ with B~'s column groups sharded over a process group: exchange="nccl"
+    (all-gather + unshard kernel) or "p2p" (fused peer-store epilogue, fp32)."""
+
+    def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl"):
+        from . import nmspmm
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' or 'p2p'")
+        if exchange == "p2p" and local_weight.values.dtype != torch.float32:
+            raise ValueError("exchange='p2p' is the fp32 SIMT kernel's epilogue: fp32 weights only")
         self.W = local_weight  # nmspmm.NmWeight of this rank's padded shard
         # the offline weight prepack (P:470-475) once per layer: the bf16 sparse-tensor-core
         # kernel's slot packing and images; plain values/idx for the fp32 path
         self.PW = nmspmm.nm_prepack(local_weight) if local_weight.values.is_cuda else None
         self.group = group
         self.G = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
         self.n = n
         self.nr = local_weight.n
+        self.exchange = exchange
+        self.peers = None
+        q = n // local_weight.L
+        g0, g1 = shard_ranges(q, self.G)[self.rank]
+        self.col_off, self.n_valid = g0 * local_weight.L, (g1 - g0) * local_weight.L
 
     @classmethod
-    def from_dense(cls, B: torch.Tensor, N: int, M: int, L: int, group=None):
+    def from_dense(cls, B: torch.Tensor, N: int, M: int, L: int, group=None, exchange: str = "nccl"):
         """Compress only this rank's columns (compression is per column group, so
         the shard of compress(B) equals compress of the shard)."""
         from . import nmspmm
@@ -65,7 +121,7 @@ class ShardedNmLinear:
         Bs[:, :(g1 - g0) * L] = B[:, g0 * L:g1 * L]
         # padding groups are all-zero: compress gives zero values and the pattern 0..N-1
         W = nmspmm.nm_compress(Bs.contiguous(), N, M, L)
-        return cls(W, n, group)
+        return cls(W, n, group, exchange)
 
     def local(self, A: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         from . import nmspmm
@@ -73,8 +129,24 @@ class ShardedNmLinear:
             return nmspmm.nm_spmm_prepacked(A, self.PW, out=out)
         return nmspmm.nm_spmm(A, self.W, out=out)
 
+    def _call_p2p(self, A: torch.Tensor) -> torch.Tensor:
+        from . import nmspmm
+        m = A.shape[0]
+        if self.peers is None or self.peers.m != m:  # collective: every rank calls with the same m
+            if self.peers is not None:
+                self.peers.close()
+            self.peers = PeerExchange(self.group, m, self.n, A.dtype, A.device)
+        ex = self.peers
+        ex.epoch += 1
+        b = ex.epoch & 1
+        nmspmm.nm_spmm_peers(A, self.W, ex.ptrs[b], self.n, self.col_off, self.n_valid)
+        nmspmm.nm_peer_barrier(ex.ptrs[2], self.rank, ex.epoch, device=A.device)
+        return ex.C[b]
+
     def __call__(self, A: torch.Tensor) -> torch.Tensor:
         from . import nmspmm
+        if self.exchange == "p2p":
+            return self._call_p2p(A)
         m = A.shape[0]
         c_local = self.local(A)
         if self.G == 1 and self.nr == self.n:  # a single shard is already C (no exchange step)

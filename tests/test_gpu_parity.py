@@ -2,6 +2,8 @@
 same seeded inputs.  Bars (BASELINE.json north star): compression and indices
 bit-exact; fp32 CUDA-core C within 1e-5 relative Frobenius of the fp64 oracle
 (O2); tf32/bf16 within 5e-3; integer-valued inputs bit-exact on every path."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -581,3 +583,60 @@ def test_spmm_host_path_chunked(nm, oracle, monkeypatch, chunks):
     vi, Di = oracle.compress(synth.integer((k, n), 46, 2), N, M, L)
     run(torch.from_numpy(Ai).pin_memory(), torch.from_numpy(vi).pin_memory(), torch.from_numpy(Di).pin_memory(), C)
     assert np.array_equal(C.numpy().astype(np.float64), oracle.spmm_sparse_f64(Ai, vi, Di, k, N, M, L))
+
+
+# --------------------------------------------------------------- fused peer exchange (S10, p2p)
+def _shards(nm, oracle, m, n, k, N, M, L, G, seed):
+    from paper_2503_01253_b200 import sharded
+    A = synth.uniform((m, k), seed, synth.TID_A)
+    B = synth.uniform((k, n), seed + 1, synth.TID_B)
+    vals, D = oracle.compress(B, N, M, L)
+    q, out = n // L, []
+    for r in range(G):
+        v, d = sharded.shard_weight(torch.from_numpy(vals), torch.from_numpy(D), L, N, r, G)
+        g0, g1 = sharded.shard_ranges(q, G)[r]
+        out.append((nm.NmWeight(v.cuda(), d.cuda(), k, N, M, L), g0 * L, (g1 - g0) * L))
+    return A, vals, D, out
+
+
+@pytest.mark.parametrize("G,m,n,k,N,M,L", [(2, 300, 640, 512, 8, 32, 32), (3, 256, 768, 1024, 4, 32, 32),
+                                           (2, 130, 520, 256, 4, 32, 8)])
+def test_spmm_peers_two_streams(nm, oracle, G, m, n, k, N, M, L):
+    """The fused exchange's device logic with G 'ranks' on G streams of one process: every rank's
+    epilogue stores its shard into all G C buffers, the flag barrier orders them; after the
+    barrier every buffer holds the whole C (oracle), for several epochs."""
+    A, vals, D, shards = _shards(nm, oracle, m, n, k, N, M, L, G, 181)
+    ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)
+    Ad = dev(A)
+    Cs = [torch.full((m, n), float("nan"), device="cuda") for _ in range(G)]
+    flags = [torch.zeros(G, dtype=torch.int32, device="cuda") for _ in range(G)]
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    for epoch in (1, 2, 3):
+        for r in range(G):
+            W, col_off, n_valid = shards[r]
+            with torch.cuda.stream(streams[r]):
+                nm.nm_spmm_peers(Ad, W, [c.data_ptr() for c in Cs], n, col_off, n_valid, stream=streams[r])
+                nm.nm_peer_barrier([f.data_ptr() for f in flags], r, epoch, stream=streams[r])
+        torch.cuda.synchronize()
+        for r in range(G):
+            assert oracle.rel_frobenius(Cs[r].cpu().numpy(), ref) <= TOL_F32
+            assert int(flags[r].min()) == epoch
+
+
+def test_sharded_p2p_two_processes_one_gpu(nm, oracle):
+    """The IPC plumbing of exchange='p2p': two processes (gloo for the handle exchange) on one
+    GPU map each other's C buffers and flags; each call's C equals the oracle on both ranks."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29000 + os.getpid() % 1000
+    import p2p_worker
+    procs = [ctx.Process(target=p2p_worker.run, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert isinstance(res[r], float) and res[r] <= TOL_F32, res
