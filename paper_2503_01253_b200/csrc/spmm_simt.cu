@@ -322,6 +322,9 @@ __global__ void __launch_bounds__(THREADS, 2)
                     *reinterpret_cast<float4*>(crow + gc0 + 16) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
             }
         }
+        // the peer stores are visible system-wide before this kernel completes, so the barrier
+        // kernel that follows on the stream may publish them with its release flag
+        __threadfence_system();
         return;
     }
 #pragma unroll

@@ -77,6 +77,7 @@ class PeerExchange:
 
     def close(self):
         from . import nmspmm
+        torch.cuda.synchronize()  # no kernel of ours may still be storing through a mapping
         for ptr, off in self.opened:
             nmspmm.nm_ipc_close(ptr, off)
         self.opened = []
