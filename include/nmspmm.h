@@ -258,6 +258,12 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
                         int64_t ldc, int64_t col_off, int64_t n_valid, int64_t m, int64_t nr, int64_t k, int N,
                         int M, int L, void* stream);
 nm_status nm_peer_barrier(void* const* flag_peers, int G, int rank, int epoch, void* stream);
+/* The same for a prepacked shard (nm_prepack / nm_prepack_ex): kind 0 -> nm_spmm_peers; kind 2
+ * (bf16) / 3 (tf32, c_dt NM_F32) -> the sparse-tensor-core slot kernel with its direct-store
+ * epilogue writing every C element to all G buffers (c_dt bf16 or fp32; C pointers, ldc and
+ * col_off 4-B aligned, A 16-B aligned, k % 8 == 0); kind 1 -> NM_ERR_UNSUPPORTED.  Asynchronous. */
+nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* const* C_peers, int G, int64_t ldc,
+                                  int64_t col_off, int64_t n_valid, int64_t m, nm_dtype c_dt, void* stream);
 
 /*
  * nm_profile_begin / nm_profile_end -- launch accounting for measurement

@@ -217,7 +217,7 @@ void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int*
 nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, void* buf,
                         cudaStream_t s);
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
-                    int M, int L, bool tf, cudaStream_t s);
+                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po = nullptr);
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                        int64_t k, int N, int M, int L, bool tf, cudaStream_t s);
 

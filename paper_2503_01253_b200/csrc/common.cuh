@@ -40,11 +40,12 @@ void note_launch();
 void prof_begin(cudaStream_t s);
 void prof_end(cudaStream_t s);
 
-// Peer-store destinations of the fused column all-gather (nm_spmm_peers): up to 8 ranks'
+// Peer-store destinations of the fused column all-gather (nm_spmm_peers,
+// nm_spmm_prepacked_peers): up to 8 ranks'
 // C buffers (device pointers valid in this process: own or IPC-opened), row pitch ldc,
 // this shard's first global column col_off, its n_valid real (unpadded) columns.
 struct PeerOut {
-    float* c[8];
+    void* c[8];
     int np;
     int64_t ldc, col_off, n_valid;
 };

@@ -15,6 +15,9 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 nm_status require_device();
+nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M,
+                    int L, bool tf, cudaStream_t s, const PeerOut* po);
+bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 
 struct PeerFlags {
     int* f[8];  // f[p] = rank p's flag array (int[G]) as mapped in this process
@@ -133,7 +136,7 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
     uintptr_t al = static_cast<uintptr_t>(ldc | col_off) * 4u;
     for (int i = 0; i < G; ++i) {
         if (!C_peers[i]) return fail(NM_ERR_NULL, "nm_spmm_peers: NULL C pointer");
-        po.c[i] = static_cast<float*>(C_peers[i]);
+        po.c[i] = C_peers[i];
         al |= reinterpret_cast<uintptr_t>(C_peers[i]);
     }
     // the fused path is the fp32 SIMT kernel's epilogue: 16-B stores at [row][col_off + col]
@@ -143,8 +146,44 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
     nm_status st = require_device();
     if (st) return st;
     const int mode = m % 4 == 0 ? 1 : 0;  // A^T staging needs m % 4 == 0 (as in the selector)
-    return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx, po.c[0], m, nr, k, N,
-                           M, L, mode, static_cast<cudaStream_t>(stream), &po);
+    return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
+                           static_cast<float*>(po.c[0]), m, nr, k, N, M, L, mode, static_cast<cudaStream_t>(stream), &po);
+}
+
+nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* const* C_peers, int G, int64_t ldc,
+                                  int64_t col_off, int64_t n_valid, int64_t m, nm_dtype c_dt, void* stream) {
+    if (!w || w->magic != 0x4B504D4E) return fail(NM_ERR_NULL, "nm_spmm_prepacked_peers: descriptor not filled by nm_prepack");
+    if (w->kind == 0)  // fp32 weights: the SIMT kernel's peer epilogue
+        return nm_spmm_peers(A, w->values, w->idx, C_peers, G, ldc, col_off, n_valid, m, w->n, w->k, w->N, w->M, w->L,
+                             stream);
+    if (w->kind != 2 && w->kind != 3)
+        return fail(NM_ERR_UNSUPPORTED, "nm_spmm_prepacked_peers: prepack kind 0, 2 or 3 (slot kernels) only");
+    if (G < 1 || G > 8) return fail(NM_ERR_SHAPE, "nm_spmm_prepacked_peers: 1 <= G <= 8");
+    if (m < 0 || col_off < 0 || n_valid < 0 || n_valid > w->n || col_off + n_valid > ldc)
+        return fail(NM_ERR_SHAPE, "nm_spmm_prepacked_peers: columns [col_off, col_off + n_valid) outside ldc");
+    const bool tf = w->kind == 3;
+    if (tf && c_dt != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
+    if (m == 0 || w->n == 0 || n_valid == 0) return NM_OK;
+    if (!A || !C_peers) return fail(NM_ERR_NULL, "nm_spmm_prepacked_peers: NULL pointer");
+    PeerOut po{};
+    po.np = G;
+    po.ldc = ldc;
+    po.col_off = col_off;
+    po.n_valid = n_valid;
+    const int eb = c_dt == NM_BF16 ? 2 : 4;
+    uintptr_t al = reinterpret_cast<uintptr_t>(A) & 15;
+    for (int i = 0; i < G; ++i) {
+        if (!C_peers[i]) return fail(NM_ERR_NULL, "nm_spmm_prepacked_peers: NULL C pointer");
+        po.c[i] = C_peers[i];
+        al |= (reinterpret_cast<uintptr_t>(C_peers[i]) | static_cast<uintptr_t>((ldc | col_off) * eb)) & 3;
+    }
+    if (al || w->k % 8 || !tc_sp_applicable(m, w->n, w->k, w->N, w->M, w->L))
+        return fail(NM_ERR_UNSUPPORTED, "nm_spmm_prepacked_peers: A 16-B aligned, C pointers / ldc / col_off 4-B aligned, "
+                                        "k % 8 == 0");
+    nm_status st = require_device();
+    if (st) return st;
+    return tc_sp_run(A, w->bperm, po.c[0], c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, tf,
+                     static_cast<cudaStream_t>(stream), &po);
 }
 
 }  // extern "C"

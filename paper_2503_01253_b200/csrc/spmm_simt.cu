@@ -441,7 +441,7 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     p.C = C;
     if (po) {
         p.npeer = po->np;
-        for (int i = 0; i < po->np && i < 8; ++i) p.cpeer[i] = po->c[i];
+        for (int i = 0; i < po->np && i < 8; ++i) p.cpeer[i] = static_cast<float*>(po->c[i]);
         p.ldc = po->ldc;
         p.col_off = po->col_off;
         p.n_valid = static_cast<int>(po->n_valid);

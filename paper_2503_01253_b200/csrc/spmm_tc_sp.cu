@@ -134,6 +134,11 @@ struct Params {
     int* flags;      // tail split: flags[tail] = 1 once part 1's partial is in ws (zeroed per launch)
     int dbg;  // NM_SP_DBG (timing studies only): 1 skip gathers, 2 skip MMAs, 8 skip C stores, 16 skip weights,
               // 64 per-stage clock64 trace, 128 plain arrive for commits (no MMA), 256 per-CTA timeline
+    // fused column all-gather (nm_spmm_prepacked_peers): the direct-store epilogue writes every C
+    // element to cpeer[0 .. npeer) at [token][col_off + col] (row pitch ldc), columns < n_valid
+    void* cpeer[8];
+    int npeer, n_valid;
+    int64_t ldc, col_off;
 };
 
 // 16-B global -> shared copy (L2 only); src_bytes = 0 zero-fills the destination
@@ -535,6 +540,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0u;
                 }
+                // destinations: C itself, or (fused exchange) every rank's C at column col_off + col
+                const int npeer = p.npeer ? p.npeer : 1;
+                const int64_t ldc = p.npeer ? p.ldc : p.n, coff = p.npeer ? p.col_off : 0;
+                const int ncol = p.npeer ? p.n_valid : p.n;
                 if (p.c_bf16) {
                     // lanes (2p, 2p+1) swap so each stores a bf16 pair (columns pc, pc+1): even lane token i, odd i+1
 #pragma unroll
@@ -544,23 +553,27 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const float lo = __uint_as_float(odd ? y : v[i]);
                         const float hi = __uint_as_float(odd ? v[i + 1] : y);
                         const int tl = t0 + i + (odd ? 1 : 0), t = m0 + tl;  // tl < NT: stay inside the tile
-                        if (tl < NT && t < p.m && pc < p.n && !(p.dbg & (8 | 64))) {
+                        if (tl < NT && t < p.m && pc < ncol && !(p.dbg & (8 | 64))) {
                             __nv_bfloat162 hh = __floats2bfloat162_rn(lo, hi);
-                            *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.C) +
-                                                               static_cast<int64_t>(t) * p.n + pc) = hh;
+                            for (int pi = 0; pi < npeer; ++pi)
+                                *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.npeer ? p.cpeer[pi] : p.C) +
+                                                                   static_cast<int64_t>(t) * ldc + coff + pc) = hh;
                         }
                     }
                 } else {
 #pragma unroll
                     for (int i = 0; i < 32; ++i) {
                         const int t = m0 + t0 + i;
-                        if (t0 + i < NT && t < p.m && col < p.n && !(p.dbg & (8 | 64)))
-                            static_cast<float*>(p.C)[static_cast<int64_t>(t) * p.n + col] = __uint_as_float(v[i]);
+                        if (t0 + i < NT && t < p.m && col < ncol && !(p.dbg & (8 | 64)))
+                            for (int pi = 0; pi < npeer; ++pi)
+                                static_cast<float*>(p.npeer ? p.cpeer[pi] : p.C)[static_cast<int64_t>(t) * ldc + coff + col] =
+                                    __uint_as_float(v[i]);
                     }
                 }
             }
         }
         }
+        if (p.npeer) __threadfence_system();  // peer stores visible before the kernel completes
         tc_fence_before();
         if (warp == 0) SP_TS(nst, 0);
     }
@@ -1084,7 +1097,7 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     const int eb = p.c_bf16 ? 2 : 4;
     p.tma_c = 0;
     const char* te = std::getenv("NM_SP_TMA_C");
-    if (!(te && te[0] == '0') && (n * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
+    if (!p.npeer && !(te && te[0] == '0') && (n * eb) % 16 == 0 && (reinterpret_cast<uintptr_t>(p.C) & 15) == 0 &&
         (NT + 31) / 32 * 32 * CF::MC * eb <= CF::ST * (CF::B_BYTES + CF::W_BYTES)) {
         const CUtensorMapDataType dt = p.c_bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
         if (make_tma_2d(&tmC, p.C, dt, eb, m, n, 32, CF::MC, 0) == NM_OK &&
@@ -1162,7 +1175,7 @@ static nm_status sp_dispatch(int H, int nt, const void* at, const tcs::Params& p
 }
 
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M, int L,
-                    bool tf, cudaStream_t s) {
+                    bool tf, cudaStream_t s, const PeerOut* po) {
     using namespace tcs;
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
@@ -1210,6 +1223,13 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
         p.c_bf16 = c_bf16 ? 1 : 0;
         const char* dbg = std::getenv("NM_SP_DBG");
         p.dbg = dbg ? std::atoi(dbg) : 0;
+        if (po) {
+            p.npeer = po->np;
+            for (int i = 0; i < po->np && i < 8; ++i) p.cpeer[i] = po->c[i];
+            p.ldc = po->ldc;
+            p.col_off = po->col_off;
+            p.n_valid = static_cast<int>(po->n_valid);
+        }
 
         const int H = sp_halves(L, N, M), nt = sp_tokens(H, m, n);
         st = tf ? sp_dispatch<true>(H, nt, at, p, m, n, s) : sp_dispatch<false>(H, nt, at, p, m, n, s);
@@ -1238,7 +1258,7 @@ nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C,
     nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k, N, M, L, tf), s);
     if (st) return st;
     st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, buf, s);
-    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, tf, s);
+    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, tf, s, nullptr);
     const cudaError_t e = cudaFreeAsync(buf, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;

@@ -28,7 +28,7 @@ EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_
            "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
            "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked",
            "nm_prepack_bytes_ex", "nm_prepack_ex", "nm_ipc_get_handle", "nm_ipc_open_handle", "nm_ipc_close",
-           "nm_spmm_peers", "nm_peer_barrier"]
+           "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers"]
 
 
 class NmError(RuntimeError):
@@ -95,6 +95,8 @@ def lib():
         L.nm_ipc_close.argtypes = [P, I64]
         L.nm_spmm_peers.argtypes = [P, P, P, ctypes.POINTER(P), I, I64, I64, I64, I64, I64, I64, I, I, I, P]
         L.nm_peer_barrier.argtypes = [ctypes.POINTER(P), I, I, I, P]
+        L.nm_spmm_prepacked_peers.argtypes = [P, ctypes.POINTER(Prepacked), ctypes.POINTER(P), I, I64, I64, I64, I64, I,
+                                              P]
         for name in EXPORTS[2:]:
             if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes", "nm_prepack_bytes_ex"):
                 getattr(L, name).restype = I
@@ -338,3 +340,21 @@ def nm_peer_barrier(flag_ptrs, rank: int, epoch: int, device=None, stream=None) 
     s = ctypes.c_void_p(stream.cuda_stream) if stream is not None else \
         ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
     _check(lib().nm_peer_barrier(_ptr_array(flag_ptrs), len(flag_ptrs), rank, epoch, s), "nm_peer_barrier")
+
+
+def nm_spmm_prepacked_peers(A: torch.Tensor, PW: "PrepackedWeight", c_ptrs, ldc: int, col_off: int, n_valid: int,
+                            out_dtype=None, stream=None) -> None:
+    """nm_spmm_peers for a prepacked shard (bf16 / tf32 slot kernels, or kind 0 -> the SIMT path)."""
+    _dev(A, "A")
+    cdt = _dt_of(out_dtype or A.dtype)
+    _check(lib().nm_spmm_prepacked_peers(A.data_ptr(), ctypes.byref(PW.desc), _ptr_array(c_ptrs), len(c_ptrs), ldc,
+                                         col_off, n_valid, A.shape[0], cdt, _stream(A, stream)),
+           "nm_spmm_prepacked_peers")
+
+
+def _dt_of(dtype) -> int:
+    if dtype == torch.float32:
+        return NM_F32
+    if dtype == torch.bfloat16:
+        return NM_BF16
+    raise TypeError(f"unsupported dtype {dtype}")

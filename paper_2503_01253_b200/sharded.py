@@ -8,7 +8,7 @@ all-gather moves equal-size [m][nr] blocks; nm_unshard_columns (our kernel)
 drops the padding and writes the m x n row-major C.  A is replicated (the
 input of a column-parallel layer).  No reduction is needed.
 
-exchange="p2p" fuses the exchange into the SpMM (fp32): the ranks' C buffers are
+exchange="p2p" fuses the exchange into the SpMM (fp32 SIMT or bf16 slot kernel): the ranks' C buffers are
 mapped into every process by CUDA IPC, each rank's SpMM epilogue stores its
 columns into all of them over NVLink (nm_spmm_peers), and a flag barrier in
 peer memory (nm_peer_barrier) orders the ranks -- stream-ordered, no all-gather
@@ -85,14 +85,13 @@ class PeerExchange:
 
 class ShardedNmLinear:
     """y = x . B~ with B~'s column groups sharded over a process group: exchange="nccl"
-    (all-gather + unshard kernel) or "p2p" (fused peer-store epilogue, fp32)."""
+    (all-gather + unshard kernel) or "p2p" (fused peer-store epilogue: fp32 SIMT kernel, or the bf16
+    sparse-tensor-core kernel's direct-store epilogue)."""
 
     def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl"):
         from . import nmspmm
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' or 'p2p'")
-        if exchange == "p2p" and local_weight.values.dtype != torch.float32:
-            raise ValueError("exchange='p2p' is the fp32 SIMT kernel's epilogue: fp32 weights only")
         self.W = local_weight  # nmspmm.NmWeight of this rank's padded shard
         # the offline weight prepack (P:470-475) once per layer: the bf16 sparse-tensor-core
         # kernel's slot packing and images; plain values/idx for the fp32 path
@@ -140,7 +139,10 @@ class ShardedNmLinear:
         ex = self.peers
         ex.epoch += 1
         b = ex.epoch & 1
-        nmspmm.nm_spmm_peers(A, self.W, ex.ptrs[b], self.n, self.col_off, self.n_valid)
+        if self.PW is not None and self.PW.kind in (2, 3):  # bf16 / tf32 slot kernel, direct-store epilogue
+            nmspmm.nm_spmm_prepacked_peers(A, self.PW, ex.ptrs[b], self.n, self.col_off, self.n_valid)
+        else:  # fp32 SIMT kernel's peer epilogue
+            nmspmm.nm_spmm_peers(A, self.W, ex.ptrs[b], self.n, self.col_off, self.n_valid)
         nmspmm.nm_peer_barrier(ex.ptrs[2], self.rank, ex.epoch, device=A.device)
         return ex.C[b]
 

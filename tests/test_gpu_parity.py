@@ -640,3 +640,47 @@ def test_sharded_p2p_two_processes_one_gpu(nm, oracle):
         p.join(timeout=60)
     for r in range(2):
         assert isinstance(res[r], float) and res[r] <= TOL_F32, res
+
+
+@pytest.mark.parametrize("dt", ["bf16", "tf32"])
+@pytest.mark.parametrize("cdt", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("G,m,n,k,N,M,L", [(2, 300, 1024, 512, 8, 32, 32), (3, 260, 768, 1024, 4, 32, 32)])
+def test_spmm_prepacked_peers_two_streams(nm, oracle, dt, cdt, G, m, n, k, N, M, L):
+    """Fused exchange on the sparse-tensor-core slot kernel (bf16 kind 2 / tf32 kind 3 shards):
+    the direct-store epilogue writes each shard into all G buffers; integer inputs -> fp32 C
+    bit-exact, bf16 C = its RNE."""
+    if dt == "tf32" and cdt == torch.bfloat16:
+        pytest.skip("fp32 operands need an fp32 C")
+    from paper_2503_01253_b200 import sharded
+    A = synth.integer((m, k), 201, synth.TID_A)
+    B = synth.integer((k, n), 202, synth.TID_B)
+    bits = synth.to_bf16_bits(B) if dt == "bf16" else B
+    vals, D = oracle.compress(bits, N, M, L)
+    vals_f = oracle.bf16_to_f32(vals) if dt == "bf16" else vals
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A) if dt == "bf16" else A, vals, D, k, N, M, L)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    Ad = dev(A, tdt)
+    q = n // L
+    Cs = [torch.full((m, n), float("nan"), device="cuda", dtype=cdt) for _ in range(G)]
+    flags = [torch.zeros(G, dtype=torch.int32, device="cuda") for _ in range(G)]
+    shards = []
+    for r in range(G):
+        v, d = sharded.shard_weight(torch.from_numpy(vals_f), torch.from_numpy(D), L, N, r, G)
+        W = nm.NmWeight(v.cuda().to(tdt), d.cuda(), k, N, M, L)
+        PW = nm.nm_prepack(W, math="tf32_tc" if dt == "tf32" else "auto")
+        assert PW.kind == (3 if dt == "tf32" else 2)
+        g0, g1 = sharded.shard_ranges(q, G)[r]
+        shards.append((PW, g0 * L, (g1 - g0) * L))
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in range(G)]
+    want = ref if cdt == torch.float32 else torch.from_numpy(ref.astype(np.float32)).bfloat16().float().numpy()
+    for epoch in (1, 2):
+        for r in range(G):
+            PW, col_off, n_valid = shards[r]
+            with torch.cuda.stream(streams[r]):
+                nm.nm_spmm_prepacked_peers(Ad, PW, [c.data_ptr() for c in Cs], n, col_off, n_valid, out_dtype=cdt,
+                                           stream=streams[r])
+                nm.nm_peer_barrier([f.data_ptr() for f in flags], r, epoch, stream=streams[r])
+        torch.cuda.synchronize()
+        for r in range(G):
+            assert np.array_equal(Cs[r].float().cpu().numpy().astype(np.float64), want)
