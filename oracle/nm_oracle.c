@@ -257,6 +257,33 @@ int nmo_spmm_sparse_f64(const void* A, int a_bf16, const void* values, int v_bf1
     return NMO_OK;
 }
 
+/* O2s: Eq. 1 as printed, WITH the M/N factor: C'[i][j] =   */
+/* (M/N) * sum_u A[i][(u/N)M + D[u][j/L]] * B'[u][j] (the paper's      */
+/* approximation of the unpruned C; R1 reads the product     */
+/* path unscaled, nm_spmm_scaled exposes the factor as alpha).  The    */
+/* sum in fp64, ascending u; the factor applied once, in fp64.         */
+int nmo_spmm_eq1_scaled_f64(const void* A, int a_bf16, const void* values, int v_bf16, const uint8_t* D,
+                            int64_t m, int64_t n, int64_t k, int N, int M, int L, double* C, int nthreads) {
+    int s = nmo_check_shape(k, n, N, M, L);
+    if (s) return s;
+    const int64_t w = k / M * N, q = n / L;
+    const double scale = (double)M / (double)N;
+    int nt = omp_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 1) num_threads(nt)
+    for (int64_t i = 0; i < m; ++i) {
+        for (int64_t j = 0; j < n; ++j) {
+            const int64_t g = j / L;
+            double sum = 0.0;
+            for (int64_t u = 0; u < w; ++u) {
+                const double a = load_elem(A, a_bf16, i * k + (u / N) * M + D[u * q + g]);
+                sum = sum + a * load_elem(values, v_bf16, u * n + j);
+            }
+            C[i * n + j] = scale * sum;
+        }
+    }
+    return NMO_OK;
+}
+
 /* O2f: the same sum with a 32-bit float accumulator, ascending u     */
 /* (SPEC's spmm_naive semantics).                              */
 int nmo_spmm_sparse_f32seq(const void* A, int a_bf16, const void* values, int v_bf16,

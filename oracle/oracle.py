@@ -59,6 +59,7 @@ def lib():
         L.nmo_validate.restype = I64
         L.nmo_spmm_sparse_f64.argtypes = [P, I, P, I, P, I64, I64, I64, I, I, I, P, I64, P, I]
         L.nmo_spmm_sparse_f32seq.argtypes = [P, I, P, I, P, I64, I64, I64, I, I, I, P, I]
+        L.nmo_spmm_eq1_scaled_f64.argtypes = [P, I, P, I, P, I64, I64, I64, I, I, I, P, I]
         L.nmo_gemm_dense_f64.argtypes = [P, I, P, I, I64, I64, I64, P, I]
         L.nmo_gemm_dense_f32seq.argtypes = [P, I, P, I, I64, I64, I64, P, I]
         L.nmo_confusion.argtypes = [P, P, I64, I64, P]
@@ -150,6 +151,18 @@ def spmm_sparse_f64(A: np.ndarray, values: np.ndarray, D: np.ndarray, k: int, N:
                                   N, M, L, rp, nr, _p(C), nthreads)
     if s:
         raise OracleError(s, "spmm_sparse_f64")
+    return C
+
+
+def spmm_eq1_scaled_f64(A, values, D, k, N, M, L, nthreads: int = 0) -> np.ndarray:
+    """O2s: Eq. 1 as printed, with the M/N factor, fp64."""
+    A, values, D = _c(A), _c(values), _c(D)
+    m, n = A.shape[0], values.shape[1]
+    C = np.empty((m, n), dtype=np.float64)
+    s = lib().nmo_spmm_eq1_scaled_f64(_p(A), _is_bf16(A), _p(values), _is_bf16(values), _p(D), m, n, k, N, M,
+                                      L, _p(C), nthreads)
+    if s:
+        raise OracleError(s, "spmm_eq1_scaled_f64")
     return C
 
 

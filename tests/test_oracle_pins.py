@@ -382,3 +382,34 @@ def test_bf16_operands_exact_products(oracle):
     C = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
     exact = A.astype(np.int64) @ brute_force_prune(B, N, M, L).astype(np.int64)
     assert np.array_equal(C, exact)
+
+
+def test_eq1_scaled_hand_example(oracle):
+    """Eq. 1 as printed (with M/N) and Eq. 2 on a hand-worked case:
+    A = [1 2 3 4], B = [1 5 2 3]^T, 2:4, L = 1 -> keep offsets 1 and 3 (|5|, |3|),
+    sum = 2*5 + 4*3 = 22, C' = (4/2)*22 = 44; unpruned C = 1 + 10 + 6 + 12 = 29; W = |44-29|/1 = 15."""
+    A = np.array([[1, 2, 3, 4]], dtype=np.float32)
+    B = np.array([[1], [5], [2], [3]], dtype=np.float32)
+    vals, D = oracle.compress(B, 2, 4, 1)
+    assert D.ravel().tolist() == [1, 3] and vals.ravel().tolist() == [5.0, 3.0]
+    Cs = oracle.spmm_eq1_scaled_f64(A, vals, D, 4, 2, 4, 1)
+    assert Cs.tolist() == [[44.0]]
+    assert oracle.spmm_sparse_f64(A, vals, D, 4, 2, 4, 1).tolist() == [[22.0]]
+    C = oracle.gemm_dense_f64(A, B)
+    assert C.tolist() == [[29.0]]
+    assert oracle.confusion(Cs, C).tolist() == [[15.0]]
+
+
+@pytest.mark.parametrize("L", [1, 4, 8])
+def test_eq1_scaled_dense_window_is_gemm(oracle, L):
+    """N = M: nothing is pruned and M/N = 1, so Eq. 1 as printed is the dense product (checked
+    against the independent dense triple loop) and the confusion W of Eq. 2 is zero."""
+    from paper_2503_01253_b200 import synth
+    m, k, n = 9, 16, 4 * L
+    A = synth.uniform((m, k), 61, synth.TID_A)
+    B = synth.uniform((k, n), 62, synth.TID_B)
+    vals, D = oracle.compress(B, 8, 8, L)
+    Cs = oracle.spmm_eq1_scaled_f64(A, vals, D, k, 8, 8, L)
+    C = oracle.gemm_dense_f64(A, B)
+    assert np.allclose(Cs, C, rtol=1e-12, atol=1e-12)
+    assert np.abs(oracle.confusion(Cs, C)).max() <= 1e-12
