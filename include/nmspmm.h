@@ -149,6 +149,19 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
                   void* stream);
 
 /*
+ * nm_spmm_scaled -- Eq. 1 as printed: C = alpha . A . decompress(values, idx), the
+ * paper's approximation C' of the unpruned product being alpha = M/N (R1 reads the product
+ * path unscaled: nm_spmm == nm_spmm_scaled with alpha = 1).  alpha is applied in fp32 to the
+ * fp32 accumulators inside the epilogue of the SIMT and sparse-tensor-core kernels (after any
+ * split-k / tail-split addition, before the bf16 rounding); the other kernels (older tcgen05,
+ * generic, pipelined SIMT mode 3) are followed by one in-place scaling pass over C (for a bf16
+ * C: a second rounding, exact when alpha is a power of two).  Otherwise as nm_spmm.
+ */
+nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
+                         int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math, float alpha,
+                         void* stream);
+
+/*
  * nm_spmm_host -- the same product with HOST operands (end-to-end path):
  * copies A, values, idx from host memory (pinned for async copies) into the
  * caller's device workspace, runs nm_spmm, copies C back to C_host.  On the fp32

@@ -201,7 +201,8 @@ bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr);
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
+                          float alpha = 1.f);
 bool simt_pipe_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 nm_status simt_pipe_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                            int N, int M, int L, cudaStream_t s);
@@ -217,9 +218,9 @@ void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int*
 nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, void* buf,
                         cudaStream_t s);
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
-                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po = nullptr);
+                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po = nullptr, float alpha = 1.f);
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s);
+                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha = 1.f);
 
 // Sparse-tensor-core slot path (spmm_tc_sp.cu): bf16, L in {16, 32, 64, 128}, A 16-B aligned with
 // k % 8 == 0 (the per-call transpose reads 16-B chunks), C 4-B aligned.  NM_TC_SP=0 disables it.
@@ -351,6 +352,28 @@ static nm_status select(const void* A, const void* Bv, const void* C, int64_t m,
     return fail(NM_ERR_UNSUPPORTED, "math mode not available for bf16 operands");
 }
 
+// C *= alpha (nm_spmm_scaled after a kernel without a fused alpha); grid-stride, 4 elements per
+// iteration where aligned, rounding bf16 to nearest even as the fused epilogues do.
+__global__ void scale_kernel(void* C, int c_bf16, int64_t count, float alpha) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride) {
+        if (c_bf16) {
+            __nv_bfloat16* c = static_cast<__nv_bfloat16*>(C) + i;
+            *c = __float2bfloat16_rn(__bfloat162float(*c) * alpha);
+        } else {
+            static_cast<float*>(C)[i] *= alpha;
+        }
+    }
+}
+
+static nm_status scale_launch(void* C, bool c_bf16, int64_t count, float alpha, cudaStream_t s) {
+    const int64_t blocks = std::min<int64_t>(ceil_div(count, 256), 8 * static_cast<int64_t>(num_sms()));
+    scale_kernel<<<static_cast<unsigned>(blocks), 256, 0, s>>>(C, c_bf16 ? 1 : 0, count, alpha);
+    note_launch();
+    NM_LAUNCH_CHECK("scale_kernel");
+    return NM_OK;
+}
+
 static nm_status check_common(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     if (N < 1 || M < N || M > 256 || L < 1)
         return fail(NM_ERR_INVALID_CONFIG, "invalid N:M/L: need 1 <= N <= M <= 256 and L >= 1");
@@ -405,8 +428,9 @@ nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, in
     return validate_launch(idx, k, n, N, M, L, first_bad_host, static_cast<cudaStream_t>(stream));
 }
 
-nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n, int64_t k,
-                  int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math, void* stream) {
+nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
+                         int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math, float alpha,
+                         void* stream) {
     nm_status st = check_common(m, n, k, N, M, L);
     if (st) return st;
     if (ab_dt > NM_BF16 || c_dt > NM_BF16 || math > NM_MATH_BF16_TC) return fail(NM_ERR_UNSUPPORTED, "dtype/math");
@@ -421,21 +445,38 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
     int kernel = K_GENERIC;
     nm_math used = NM_MATH_AUTO;
     if ((st = select(A, values, C, m, n, k, N, M, L, ab_dt, c_dt, math, &kernel, &used))) return st;
-    if (kernel == K_SIMT_F32)
-    {
+    // alpha is fused into the epilogues of the SIMT (modes 0-2) and sparse-tensor-core kernels; the
+    // others are followed by one scaling pass over C when alpha != 1
+    bool fused = false;
+    if (kernel == K_SIMT_F32) {
         const int mode = simt_mode(m, n, k, N, M, L);
-        if (mode == 3)
-            return simt_pipe_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
-                                    static_cast<float*>(C), m, n, k, N, M, L, s);
-        return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
-                               static_cast<float*>(C), m, n, k, N, M, L, mode, s);
+        if (mode == 3) {
+            st = simt_pipe_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
+                                  static_cast<float*>(C), m, n, k, N, M, L, s);
+        } else {
+            st = simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
+                                 static_cast<float*>(C), m, n, k, N, M, L, mode, s, nullptr, alpha);
+            fused = true;
+        }
+    } else if (kernel == K_TC_SP || kernel == K_TC_TF32) {
+        st = tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, kernel == K_TC_TF32, s, alpha);
+        fused = true;
+    } else if (kernel == K_TC_BF16) {
+        st = tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
+    } else if (ab_dt == NM_F32) {
+        st = generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
+    } else if (c_dt == NM_BF16) {
+        st = generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);
+    } else {
+        st = generic_launch<__nv_bfloat16, float>(A, values, idx, C, m, n, k, N, M, L, s);
     }
-    if (kernel == K_TC_SP) return tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, false, s);
-    if (kernel == K_TC_TF32) return tc_sp_launch(A, values, idx, C, false, m, n, k, N, M, L, true, s);
-    if (kernel == K_TC_BF16) return tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
-    if (ab_dt == NM_F32) return generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
-    if (c_dt == NM_BF16) return generic_launch<__nv_bfloat16, __nv_bfloat16>(A, values, idx, C, m, n, k, N, M, L, s);
-    return generic_launch<__nv_bfloat16, float>(A, values, idx, C, m, n, k, N, M, L, s);
+    if (st || fused || alpha == 1.f) return st;
+    return scale_launch(C, c_dt == NM_BF16, m * n, alpha, s);
+}
+
+nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n, int64_t k,
+                  int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math, void* stream) {
+    return nm_spmm_scaled(A, values, idx, C, m, n, k, N, M, L, ab_dt, c_dt, math, 1.f, stream);
 }
 
 int64_t nm_spmm_host_ws_bytes(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt) {

@@ -11,12 +11,12 @@
 namespace nm {
 
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po);
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha);
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 nm_status require_device();
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M,
-                    int L, bool tf, cudaStream_t s, const PeerOut* po);
+                    int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 
 struct PeerFlags {
@@ -147,7 +147,8 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
     if (st) return st;
     const int mode = m % 4 == 0 ? 1 : 0;  // A^T staging needs m % 4 == 0 (as in the selector)
     return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
-                           static_cast<float*>(po.c[0]), m, nr, k, N, M, L, mode, static_cast<cudaStream_t>(stream), &po);
+                           static_cast<float*>(po.c[0]), m, nr, k, N, M, L, mode, static_cast<cudaStream_t>(stream), &po,
+                           1.f);
 }
 
 nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* const* C_peers, int G, int64_t ldc,
@@ -183,7 +184,7 @@ nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* co
     nm_status st = require_device();
     if (st) return st;
     return tc_sp_run(A, w->bperm, po.c[0], c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, tf,
-                     static_cast<cudaStream_t>(stream), &po);
+                     static_cast<cudaStream_t>(stream), &po, 1.f);
 }
 
 }  // extern "C"

@@ -58,6 +58,7 @@ struct Params {
     float* cpeer[8];
     int npeer, n_valid;
     int64_t ldc, col_off;
+    float alpha;  // C = alpha . A B~ (1: the product; M/N: Eq. 1 as printed, nm_spmm_scaled)
 };
 
 // Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
@@ -307,7 +308,12 @@ __global__ void __launch_bounds__(THREADS, 2)
         if (tid == 0) p.counters[ti] = 0;  // ready for the next launch
     }
 
-    // epilogue: registers -> global (float4 stores, guarded for ragged m / n)
+    // epilogue: registers -> global (float4 stores, guarded for ragged m / n); alpha after any
+    // k-split reduction (x 1.0f is exact)
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] *= p.alpha;
     const int gc0 = n0 + col0;
     if (p.npeer) {
 #pragma unroll
@@ -434,11 +440,12 @@ static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, con
 // mode: 0 = A panels straight from A (swizzled [m][k] boxes), 1 = A^T staged (tile TMA),
 // 2 = A^T staged + packed col_info loads (high sparsity).  The selector decides.
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po) {
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha) {
     using namespace simt;
     Params p{};
     p.D = D;
     p.C = C;
+    p.alpha = alpha;
     if (po) {
         p.npeer = po->np;
         for (int i = 0; i < po->np && i < 8; ++i) p.cpeer[i] = static_cast<float*>(po->c[i]);

@@ -139,6 +139,7 @@ struct Params {
     void* cpeer[8];
     int npeer, n_valid;
     int64_t ldc, col_off;
+    float alpha;  // C = alpha . A B~ (nm_spmm_scaled); applied after the tail-split addition
 };
 
 // 16-B global -> shared copy (L2 only); src_bytes = 0 zero-fills the destination
@@ -244,8 +245,10 @@ __device__ __forceinline__ void cluster_sync_all() {
 // ranges); each CTA bulk-copies half of every weight image with .multicast::cluster into both,
 // and every MMA commit releases the stage in both CTAs (empty count 2): the weight stream's L2
 // traffic per SM halves.
-// TF: fp32 operands on kind::tf32 (El<true>), else bf16 on kind::f16.
-template <int H, int NT_, bool MCAST, bool TF>
+// TF: fp32 operands on kind::tf32 (El<true>), else bf16 on kind::f16.  PEER: the fused exchange's
+// direct-store epilogue into every rank's C (a separate instantiation: the peer loop in the
+// common kernel cost 30 % on the tf32 NT = 208 variant through register allocation).
+template <int H, int NT_, bool MCAST, bool TF, bool PEER = false>
 __global__ void __launch_bounds__(THREADS, 1)
     spmm_tc_sp_kernel(const void* __restrict__ At, const __grid_constant__ CUtensorMap tmC,
                       const __grid_constant__ CUtensorMap tmC16, const Params p) {
@@ -503,6 +506,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                         for (int i = 0; i < 32; ++i)
                             if (i < nv) v[i] = __float_as_uint(__uint_as_float(v[i]) + src[static_cast<int64_t>(i) * MC]);
                     }
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.alpha);
                     uint8_t* cb = buf + (h * 128 + qw * 32 + lane) * eb;
                     // NT % 32 == 16 (176, 208 tokens): the last chunk holds 16 tokens of this tile
                     const int rows = NT - t0 < 32 ? NT - t0 : 32;
@@ -540,10 +545,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = 0u;
                 }
-                // destinations: C itself, or (fused exchange) every rank's C at column col_off + col
-                const int npeer = p.npeer ? p.npeer : 1;
-                const int64_t ldc = p.npeer ? p.ldc : p.n, coff = p.npeer ? p.col_off : 0;
-                const int ncol = p.npeer ? p.n_valid : p.n;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.alpha);
+                // destinations: C itself, or (PEER, fused exchange) every rank's C at col_off + col
+                const int npeer = PEER ? p.npeer : 1;
+                const int64_t ldc = PEER ? p.ldc : p.n, coff = PEER ? p.col_off : 0;
+                const int ncol = PEER ? p.n_valid : p.n;
                 if (p.c_bf16) {
                     // lanes (2p, 2p+1) swap so each stores a bf16 pair (columns pc, pc+1): even lane token i, odd i+1
 #pragma unroll
@@ -556,7 +563,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         if (tl < NT && t < p.m && pc < ncol && !(p.dbg & (8 | 64))) {
                             __nv_bfloat162 hh = __floats2bfloat162_rn(lo, hi);
                             for (int pi = 0; pi < npeer; ++pi)
-                                *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(p.npeer ? p.cpeer[pi] : p.C) +
+                                *reinterpret_cast<__nv_bfloat162*>(static_cast<__nv_bfloat16*>(PEER ? p.cpeer[pi] : p.C) +
                                                                    static_cast<int64_t>(t) * ldc + coff + pc) = hh;
                         }
                     }
@@ -566,14 +573,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const int t = m0 + t0 + i;
                         if (t0 + i < NT && t < p.m && col < ncol && !(p.dbg & (8 | 64)))
                             for (int pi = 0; pi < npeer; ++pi)
-                                static_cast<float*>(p.npeer ? p.cpeer[pi] : p.C)[static_cast<int64_t>(t) * ldc + coff + col] =
+                                static_cast<float*>(PEER ? p.cpeer[pi] : p.C)[static_cast<int64_t>(t) * ldc + coff + col] =
                                     __uint_as_float(v[i]);
                     }
                 }
             }
         }
         }
-        if (p.npeer) __threadfence_system();  // peer stores visible before the kernel completes
+        if (PEER) __threadfence_system();  // peer stores visible before the kernel completes
         tc_fence_before();
         if (warp == 0) SP_TS(nst, 0);
     }
@@ -1089,6 +1096,8 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, true, TF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false, TF, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         attr = true;
     }
     // C through TMA stores when its rows are 16-B aligned (the staged tile, NT/32 chunks of
@@ -1146,6 +1155,8 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
         lc.attrs = la;
         lc.numAttrs = 1;
         cudaLaunchKernelEx(&lc, spmm_tc_sp_kernel<H, NT, true, TF>, at, tmC, tmC16, p);
+    } else if (p.npeer) {
+        spmm_tc_sp_kernel<H, NT, false, TF, true><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
     } else {
         spmm_tc_sp_kernel<H, NT, false, TF><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
     }
@@ -1175,7 +1186,7 @@ static nm_status sp_dispatch(int H, int nt, const void* at, const tcs::Params& p
 }
 
 nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M, int L,
-                    bool tf, cudaStream_t s, const PeerOut* po) {
+                    bool tf, cudaStream_t s, const PeerOut* po, float alpha) {
     using namespace tcs;
     size_t os, ot, on, oq, oi, tot;
     int smax, mst;
@@ -1223,6 +1234,7 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
         p.c_bf16 = c_bf16 ? 1 : 0;
         const char* dbg = std::getenv("NM_SP_DBG");
         p.dbg = dbg ? std::atoi(dbg) : 0;
+        p.alpha = alpha;
         if (po) {
             p.npeer = po->np;
             for (int i = 0; i < po->np && i < 8; ++i) p.cpeer[i] = po->c[i];
@@ -1253,12 +1265,12 @@ size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf) {
 
 // nm_spmm without a prepacked weight: prepack into pooled scratch, run, release.
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s) {
+                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha) {
     void* buf = nullptr;
     nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k, N, M, L, tf), s);
     if (st) return st;
     st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, buf, s);
-    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, tf, s, nullptr);
+    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, tf, s, nullptr, alpha);
     const cudaError_t e = cudaFreeAsync(buf, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;

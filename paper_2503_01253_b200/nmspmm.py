@@ -28,7 +28,7 @@ EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_
            "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
            "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked",
            "nm_prepack_bytes_ex", "nm_prepack_ex", "nm_ipc_get_handle", "nm_ipc_open_handle", "nm_ipc_close",
-           "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers"]
+           "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled"]
 
 
 class NmError(RuntimeError):
@@ -75,6 +75,7 @@ def lib():
         L.nm_decompress.argtypes = [P, I, P, I64, I64, I, I, I, P, P]
         L.nm_validate.argtypes = [P, I64, I64, I, I, I, ctypes.POINTER(ctypes.c_int64), P]
         L.nm_spmm.argtypes = [P, P, P, P, I64, I64, I64, I, I, I, I, I, I, P]
+        L.nm_spmm_scaled.argtypes = [P, P, P, P, I64, I64, I64, I, I, I, I, I, I, ctypes.c_float, P]
         L.nm_spmm_host_ws_bytes.argtypes = [I64, I64, I64, I, I, I, I, I]
         L.nm_spmm_host_ws_bytes.restype = I64
         L.nm_spmm_host.argtypes = [P, P, P, P, I64, I64, I64, I, I, I, I, I, I, P, P]
@@ -188,8 +189,9 @@ def nm_validate(idx: torch.Tensor, k: int, n: int, N: int, M: int, L: int, strea
 
 
 def nm_spmm(A: torch.Tensor, W: NmWeight, out: torch.Tensor | None = None, out_dtype=None, math: str = "auto",
-            stream=None) -> torch.Tensor:
-    """C = A . decompress(W) (Eq. 1, unscaled) on the device."""
+            stream=None, alpha: float = 1.0) -> torch.Tensor:
+    """C = alpha . A . decompress(W) on the device (Eq. 1: alpha = 1 is the product,
+    alpha = M/N the paper's scaled approximation C'; nm_spmm_scaled)."""
     _dev(A, "A")
     _dev(W.values, "values")
     _dev(W.idx, "idx")
@@ -203,8 +205,13 @@ def nm_spmm(A: torch.Tensor, W: NmWeight, out: torch.Tensor | None = None, out_d
         out = torch.empty((m, W.n), dtype=cdt, device=A.device)
     else:
         _dev(out, "out")
-    _check(lib().nm_spmm(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), out.data_ptr(), m, W.n, k, W.N, W.M,
-                         W.L, _dt(A), _dt(out), MATH[math], _stream(A, stream)), "nm_spmm")
+    if alpha == 1.0:
+        _check(lib().nm_spmm(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), out.data_ptr(), m, W.n, k, W.N,
+                             W.M, W.L, _dt(A), _dt(out), MATH[math], _stream(A, stream)), "nm_spmm")
+    else:
+        _check(lib().nm_spmm_scaled(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), out.data_ptr(), m, W.n, k,
+                                    W.N, W.M, W.L, _dt(A), _dt(out), MATH[math], float(alpha), _stream(A, stream)),
+               "nm_spmm_scaled")
     return out
 
 

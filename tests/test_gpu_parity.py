@@ -684,3 +684,47 @@ def test_spmm_prepacked_peers_two_streams(nm, oracle, dt, cdt, G, m, n, k, N, M,
         torch.cuda.synchronize()
         for r in range(G):
             assert np.array_equal(Cs[r].float().cpu().numpy().astype(np.float64), want)
+
+
+# --------------------------------------------------------------- Eq. 1 as printed: alpha = M/N
+SCALED_PATHS = [  # (name, ab dtype, math, env, expected kernel id)
+    ("simt", torch.float32, "f32_simt", {}, 1),
+    ("generic", torch.float32, "f32_simt", {}, 0),          # L = 3 -> generic kernel + scaling pass
+    ("sp_bf16", torch.bfloat16, "bf16_tc", {}, 4),
+    ("pair_bf16", torch.bfloat16, "bf16_tc", {"NM_TC_SP": "0"}, 2),
+    ("tf32", torch.float32, "tf32_tc", {}, 3),
+]
+
+
+@pytest.mark.parametrize("name,tdt,math,env,kid", SCALED_PATHS)
+@pytest.mark.parametrize("cdt", [torch.float32, torch.bfloat16])
+def test_spmm_scaled_eq1(nm, oracle, monkeypatch, name, tdt, math, env, kid, cdt):
+    """nm_spmm_scaled with alpha = M/N against the oracle's Eq. 1 as printed (O2s): integer inputs
+    and M/N a power of two, so fp32 C is exact and bf16 C is its RNE on every path."""
+    if tdt == torch.float32 and cdt == torch.bfloat16:
+        pytest.skip("fp32 operands need an fp32 C")
+    for key, val in env.items():
+        monkeypatch.setenv(key, val)
+    m, n, k, N, M, L = (130, 258, 256, 2, 8, 3) if name == "generic" else (300, 512, 512, 8, 32, 32)
+    assert nm.nm_plan_query(m, n, k, N, M, L, tdt, math)["kernel"] == kid
+    A = synth.integer((m, k), 211, synth.TID_A)
+    B = synth.integer((k, n), 212, synth.TID_B)
+    bits = synth.to_bf16_bits(B) if tdt == torch.bfloat16 else B
+    vals, D = oracle.compress(bits, N, M, L)
+    vf = oracle.bf16_to_f32(vals) if tdt == torch.bfloat16 else vals
+    W = nm.NmWeight(dev(vf, tdt), dev(D, torch.uint8), k, N, M, L)
+    ref = oracle.spmm_eq1_scaled_f64(synth.to_bf16_bits(A) if tdt == torch.bfloat16 else A, vals, D, k, N, M, L)
+    C = nm.nm_spmm(dev(A, tdt), W, out_dtype=cdt, math=math, alpha=M / N).float().cpu().numpy()
+    want = ref if cdt == torch.float32 else torch.from_numpy(ref.astype(np.float32)).bfloat16().float().numpy()
+    assert np.array_equal(C.astype(np.float64), want)
+
+
+def test_spmm_scaled_uniform_and_unit_alpha(nm, oracle):
+    """Uniform inputs within the fp32 bound; alpha = 1 gives nm_spmm's bits exactly."""
+    m, n, k, N, M, L = 257, 384, 512, 12, 32, 32
+    A = synth.uniform((m, k), 221, synth.TID_A)
+    vals, D = oracle.compress(synth.uniform((k, n), 222, synth.TID_B), N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A), W, alpha=M / N).cpu().numpy()
+    assert oracle.rel_frobenius(C, oracle.spmm_eq1_scaled_f64(A, vals, D, k, N, M, L)) <= TOL_F32
+    assert torch.equal(nm.nm_spmm(dev(A), W, alpha=1.0), nm.nm_spmm(dev(A), W))
