@@ -12,3 +12,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 80 --cs
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_simt -s 3 -c 1 -o gpurun_out/prof_simt -f python bench.py --profile --steps 2 --warmup 3 > gpurun_out/ncu_simt.out 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_tc -s 3 -c 1 -o gpurun_out/prof_tc -f python bench.py --dtype bf16 --profile --steps 2 --warmup 3 > gpurun_out/ncu_tc.out 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:spmm_tc_sp -s 3 -c 1 -o gpurun_out/prof_tf32 -f python scripts/tf32_profile.py > gpurun_out/ncu_tf32.out 2>&1
+# summaries on the box; the .ncu-rep files are dropped so gpurun_out stays under the 64 MiB pull limit
+for r in simt tc tf32; do python scripts/ncu_summary.py gpurun_out/prof_$r.ncu-rep > gpurun_out/ncu_${r}_summary.txt 2>&1; done
+rm -f gpurun_out/*.ncu-rep
