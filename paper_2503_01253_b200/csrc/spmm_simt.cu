@@ -77,7 +77,9 @@ __device__ __forceinline__ int a_col_offset(int kk) {
 //      fetched -- one 512-B A^T row per warp-wide cp.async, the rows spread over all
 //      warps -- into consecutive panel rows, and the indices are remapped to packed
 //      positions (reorderingIdx) by a popcount over the col_info mask.
-template <bool TWO, bool AT, bool PK>
+// PEER: the fused exchange's peer-store epilogue (nm_spmm_peers), a separate instantiation so the
+// common kernel's code and register allocation stay as they were.
+template <bool TWO, bool AT, bool PK, bool PEER = false>
 __global__ void __launch_bounds__(THREADS, 2)
     spmm_simt_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const Params p) {
@@ -315,7 +317,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] *= p.alpha;
     const int gc0 = n0 + col0;
-    if (p.npeer) {
+    if (PEER) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             const int row = m0 + wm * 64 + (AT ? (i & 3) + 4 * t_m + 32 * (i >> 2) : 8 * i + t_m);
@@ -427,10 +429,16 @@ static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, con
     if (!attr_done) {
         NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smem));
+        if (!PK)
+            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT, false, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr_done = true;
     }
     prof_begin(s);
-    spmm_simt_f32_kernel<TWO, AT, PK><<<grid, THREADS, smem, s>>>(tmA, tmB, p);
+    if (!PK && p.npeer)
+        spmm_simt_f32_kernel<TWO, AT, false, true><<<grid, THREADS, smem, s>>>(tmA, tmB, p);
+    else
+        spmm_simt_f32_kernel<TWO, AT, PK><<<grid, THREADS, smem, s>>>(tmA, tmB, p);
     prof_end(s);
     note_launch();
     NM_LAUNCH_CHECK("spmm_simt_f32_kernel");
