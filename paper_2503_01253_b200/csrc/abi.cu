@@ -493,11 +493,12 @@ namespace nm {
 // the tensor-core paths would be repeated per chunk); 4 chunks of whole 128-row tiles once m >=
 // 1024.  Measured on B200 (profiles/r01p_host_e2e_chunks.txt): 4 chunks beat 2 and 3 at cfg2
 // and cfg4-65B even where a chunk's grid ends in a partial wave -- the overlap gained exceeds
-// the quantization lost.  NM_HOST_CHUNKS=1..4 overrides (ablation).
+// the quantization lost (6 / 8 chunks: no better at cfg2, +5 % at cfg4).  NM_HOST_CHUNKS=1..8
+// overrides (ablation).
 static int host_chunks(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab, nm_math math) {
     const char* e = getenv("NM_HOST_CHUNKS");
     int force = e ? atoi(e) : 0;
-    if (force < 0 || force > 4) force = 0;
+    if (force < 0 || force > 8) force = 0;
     static const float dummy[4] = {0, 0, 0, 0};
     if (ab != NM_F32 || !(math == NM_MATH_AUTO || math == NM_MATH_F32_SIMT) ||
         !simt_f32_applicable(dummy, dummy, dummy, m, n, k, N, M, L))
@@ -542,7 +543,7 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     // (fixed order).
     const int64_t rc = ceil_div(ceil_div(m, nch), 128) * 128;
     cudaStream_t hs = nullptr, ds = nullptr;
-    cudaEvent_t ev[2 * 4 + 1] = {};
+    cudaEvent_t ev[2 * 8 + 1] = {};
     auto cleanup = [&]() {
         for (cudaEvent_t x : ev)
             if (x) cudaEventDestroy(x);
