@@ -165,9 +165,11 @@ nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, 
  * nm_spmm_host -- the same product with HOST operands (end-to-end path):
  * copies A, values, idx from host memory (pinned for async copies) into the
  * caller's device workspace, runs nm_spmm, copies C back to C_host.  On the fp32
- * SIMT path with m >= 1024 the rows of A / C go in 4 chunks so that the copies of
- * one chunk overlap the SpMM of another (two library-created copy streams,
- * destroyed before return); other paths copy, compute and copy back in sequence.
+ * SIMT path and the bf16 / tf32 slot kernels with m >= 1024 the rows of A / C go in
+ * 4 chunks so that the copies of one chunk overlap the SpMM of another (two
+ * library-created copy streams, destroyed before return; the slot kernels prepack the
+ * weight once per call into pooled scratch first); other paths copy, compute and copy
+ * back in sequence.
  * Workspace `dev_ws` must hold nm_spmm_host_ws_bytes(...) bytes (device).
  * SYNCHRONOUS (returns after C_host is written).
  */

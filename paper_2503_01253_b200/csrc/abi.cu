@@ -495,14 +495,14 @@ namespace nm {
 // and cfg4-65B even where a chunk's grid ends in a partial wave -- the overlap gained exceeds
 // the quantization lost (6 / 8 chunks: no better at cfg2, +5 % at cfg4).  NM_HOST_CHUNKS=1..8
 // overrides (ablation).
-static int host_chunks(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm_dtype ab, nm_math math) {
+// kernel: the selector's choice; the slot kernels (bf16 / tf32 sparse TC) chunk too, with the
+// weight prepacked once per call ahead of the chunks.
+static int host_chunks(int64_t m, int kernel, nm_math math) {
     const char* e = getenv("NM_HOST_CHUNKS");
     int force = e ? atoi(e) : 0;
     if (force < 0 || force > 8) force = 0;
-    static const float dummy[4] = {0, 0, 0, 0};
-    if (ab != NM_F32 || !(math == NM_MATH_AUTO || math == NM_MATH_F32_SIMT) ||
-        !simt_f32_applicable(dummy, dummy, dummy, m, n, k, N, M, L))
-        return 1;
+    const bool simt = kernel == K_SIMT_F32 && (math == NM_MATH_AUTO || math == NM_MATH_F32_SIMT);
+    if (!simt && kernel != K_TC_SP && kernel != K_TC_TF32) return 1;
     if (force) return force;
     return m >= 1024 ? 4 : 1;
 }
@@ -529,7 +529,10 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     uint8_t* dC = dD + al(w * q);
     NM_CUDA_TRY(cudaMemcpyAsync(dV, values_host, static_cast<size_t>(w * n * e), cudaMemcpyHostToDevice, s));
     NM_CUDA_TRY(cudaMemcpyAsync(dD, idx_host, static_cast<size_t>(w * q), cudaMemcpyHostToDevice, s));
-    const int nch = host_chunks(m, n, k, N, M, L, ab_dt, math);
+    int kernel = K_GENERIC;
+    nm_math used = NM_MATH_AUTO;
+    if ((st = select(dA, dV, dC, m, n, k, N, M, L, ab_dt, c_dt, math, &kernel, &used))) return st;
+    const int nch = k > 0 ? host_chunks(m, kernel, math) : 1;
     if (nch == 1) {
         NM_CUDA_TRY(cudaMemcpyAsync(dA, A_host, static_cast<size_t>(m * k * e), cudaMemcpyHostToDevice, s));
         if ((st = nm_spmm(dA, dV, dD, dC, m, n, k, N, M, L, ab_dt, c_dt, math, stream))) return st;
@@ -542,6 +545,16 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     // is the same product on a row range, so C is unchanged up to the k-split of sub-wave grids
     // (fixed order).
     const int64_t rc = ceil_div(ceil_div(m, nch), 128) * 128;
+    // slot kernels: prepack the weight once (the paper's offline step, here per call) on s
+    const bool slot = kernel == K_TC_SP || kernel == K_TC_TF32, tf = kernel == K_TC_TF32;
+    void* pbuf = nullptr;
+    if (slot) {
+        if ((st = scratch_alloc(&pbuf, tc_sp_prepack_bytes(n, k, N, M, L, tf), s))) return st;
+        if ((st = tc_sp_prepack(dV, dD, n, k, N, M, L, tf, pbuf, s))) {
+            cudaFreeAsync(pbuf, s);
+            return st;
+        }
+    }
     cudaStream_t hs = nullptr, ds = nullptr;
     cudaEvent_t ev[2 * 8 + 1] = {};
     auto cleanup = [&]() {
@@ -549,6 +562,7 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
             if (x) cudaEventDestroy(x);
         if (hs) cudaStreamDestroy(hs);
         if (ds) cudaStreamDestroy(ds);
+        if (pbuf) cudaFreeAsync(pbuf, s);
     };
     cudaError_t ce = cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking);
     if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking);
@@ -561,7 +575,9 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
         if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i], hs);
         if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * i], 0);
         if (ce != cudaSuccess) break;
-        if ((st = nm_spmm(dA + r0 * k * e, dV, dD, dC + r0 * n * ec, r1 - r0, n, k, N, M, L, ab_dt, c_dt, math, stream))) {
+        st = slot ? tc_sp_run(dA + r0 * k * e, pbuf, dC + r0 * n * ec, c_dt == NM_BF16, r1 - r0, n, k, N, M, L, tf, s)
+                  : nm_spmm(dA + r0 * k * e, dV, dD, dC + r0 * n * ec, r1 - r0, n, k, N, M, L, ab_dt, c_dt, math, stream);
+        if (st) {
             cudaStreamSynchronize(s);
             cudaStreamSynchronize(hs);
             cleanup();

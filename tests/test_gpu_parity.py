@@ -728,3 +728,25 @@ def test_spmm_scaled_uniform_and_unit_alpha(nm, oracle):
     C = nm.nm_spmm(dev(A), W, alpha=M / N).cpu().numpy()
     assert oracle.rel_frobenius(C, oracle.spmm_eq1_scaled_f64(A, vals, D, k, N, M, L)) <= TOL_F32
     assert torch.equal(nm.nm_spmm(dev(A), W, alpha=1.0), nm.nm_spmm(dev(A), W))
+
+
+@pytest.mark.parametrize("dt", ["bf16", "tf32"])
+@pytest.mark.parametrize("chunks", ["1", "3", "4"])
+def test_spmm_host_path_chunked_slot_kernels(nm, oracle, monkeypatch, dt, chunks):
+    """nm_spmm_host on the sparse-tensor-core slot kernels: one prepack per call, then the row
+    chunks overlapped with the copies; integer inputs -> fp32 C bit-exact."""
+    monkeypatch.setenv("NM_HOST_CHUNKS", chunks)
+    m, n, k, N, M, L = 700, 512, 1024, 8, 32, 32
+    A = synth.integer((m, k), 231, 1)
+    B = synth.integer((k, n), 232, 2)
+    tdt = torch.bfloat16 if dt == "bf16" else torch.float32
+    bits = synth.to_bf16_bits(B) if dt == "bf16" else B
+    vals, D = oracle.compress(bits, N, M, L)
+    vf = oracle.bf16_to_f32(vals) if dt == "bf16" else vals
+    run = nm.HostSpmm(m, n, k, N, M, L, ab_dtype=tdt, c_dtype=torch.float32,
+                      math="tf32_tc" if dt == "tf32" else "bf16_tc")
+    C = torch.full((m, n), float("nan")).pin_memory()
+    run(torch.from_numpy(A).to(tdt).pin_memory(), torch.from_numpy(vf).to(tdt).pin_memory(),
+        torch.from_numpy(D).pin_memory(), C)
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A) if dt == "bf16" else A, vals, D, k, N, M, L)
+    assert np.array_equal(C.numpy().astype(np.float64), ref)
