@@ -6,7 +6,12 @@ JSON line on rank 0.  A "step" is one pass of the hot path over one batch:
   N = 1 : nm_spmm(A, B', D) -> C  (one launch of our kernel);
   N > 1 : column-sharded: each rank runs nm_spmm on its slice of
           the column groups, C is assembled with an NCCL all-gather and our
-          unshard kernel (strong scaling: the problem size is fixed).
+          unshard kernel (strong scaling: the problem size is fixed);
+          `--exchange p2p` instead fuses the assembly into the SpMM epilogue
+          (peer stores over CUDA IPC / NVLink + a flag barrier).
+Variants (not the headline): the other BASELINE configs in fp32 and bf16, and
+tf32 (fp32 operands on the tf32 sparse tensor cores, also timed against
+cuBLAS with TF32 tensor cores).
 Metric (BASELINE.json): effective TFLOPS = 2*m*n*w / t, w = k*N/M (kept MACs
 only), plus speedup over cuBLAS dense GEMM of the same shape and dtype
 on the same GPU.  Inputs are resident in HBM when the timed region starts;
