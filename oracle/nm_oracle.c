@@ -361,3 +361,62 @@ int nmo_confusion(const double* Capprox, const double* Cexact, int64_t m, int64_
     for (int64_t i = 0; i < m * n; ++i) W[i] = fabs(Capprox[i] - Cexact[i]) / mn;
     return NMO_OK;
 }
+
+/* ------------------------------------------------------------------ */
+/* Bit-packed, tile-major index matrix ("each element requires   */
+/* only log2 M bits"; P:419 / Listing 3 transformLayout "transform the */
+/* data layout of matrix D to reduce the number of global memory       */
+/* transactions").  The layout (R28) written out plainly:    */
+/*   b = bits per entry = max(1, ceil(log2 M)); e = floor(32 / b)      */
+/*   entries per 32-bit word (no entry straddles a word);              */
+/*   the q column groups are cut into tiles of T = 128 / L groups      */
+/*   (the 128 output columns of one CTA tile; 128 % L == 0);           */
+/*   a tile's entries are numbered x = u*T + t (row u < w, t < T) and  */
+/*   stored in Wt = ceil(w*T / e) words: word P[tile*Wt + x/e] holds   */
+/*   D[u][tile*T + t] in bits [(x%e)*b, (x%e)*b + b)                   */
+/*   (groups >= q and unused bits: 0).                                 */
+/* So a tile's whole index stream (all w rows) is one contiguous run.  */
+/* ------------------------------------------------------------------ */
+int nmo_index_bits(int M) {
+    int b = 1;
+    while ((1 << b) < M) ++b;
+    return b;
+}
+
+int64_t nmo_index_packed_words(int64_t k, int64_t n, int N, int M, int L) {
+    if (nmo_check_shape(k, n, N, M, L) || 128 % L) return -1;
+    const int64_t w = k / M * N, q = n / L, T = 128 / L;
+    const int e = 32 / nmo_index_bits(M);
+    const int64_t ntiles = (q + T - 1) / T, Wt = (w * T + e - 1) / e;
+    return ntiles * Wt;
+}
+
+int nmo_index_pack(const uint8_t* D, int64_t k, int64_t n, int N, int M, int L, uint32_t* P) {
+    const int64_t nw = nmo_index_packed_words(k, n, N, M, L);
+    if (nw < 0) return NMO_ERR_SHAPE;
+    const int64_t w = k / M * N, q = n / L, T = 128 / L;
+    const int b = nmo_index_bits(M), e = 32 / b;
+    const int64_t ntiles = (q + T - 1) / T, Wt = (w * T + e - 1) / e;
+    for (int64_t i = 0; i < nw; ++i) P[i] = 0u;
+    for (int64_t tile = 0; tile < ntiles; ++tile)
+        for (int64_t u = 0; u < w; ++u)
+            for (int64_t t = 0; t < T; ++t) {
+                const int64_t g = tile * T + t, x = u * T + t;
+                if (g < q) P[tile * Wt + x / e] |= (uint32_t)D[u * q + g] << ((x % e) * b);
+            }
+    return NMO_OK;
+}
+
+int nmo_index_unpack(const uint32_t* P, int64_t k, int64_t n, int N, int M, int L, uint8_t* D) {
+    if (nmo_index_packed_words(k, n, N, M, L) < 0) return NMO_ERR_SHAPE;
+    const int64_t w = k / M * N, q = n / L, T = 128 / L;
+    const int b = nmo_index_bits(M), e = 32 / b;
+    const int64_t Wt = (w * T + e - 1) / e;
+    const uint32_t mask = (1u << b) - 1u;
+    for (int64_t u = 0; u < w; ++u)
+        for (int64_t g = 0; g < q; ++g) {
+            const int64_t tile = g / T, x = u * T + g % T;
+            D[u * q + g] = (uint8_t)((P[tile * Wt + x / e] >> ((x % e) * b)) & mask);
+        }
+    return NMO_OK;
+}

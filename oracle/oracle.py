@@ -66,6 +66,11 @@ def lib():
         L.nmo_f32_to_bf16_rne.argtypes = [ctypes.c_float]
         L.nmo_f32_to_bf16_rne.restype = ctypes.c_uint16
         L.nmo_num_threads.argtypes = [I]
+        L.nmo_index_bits.argtypes = [I]
+        L.nmo_index_packed_words.argtypes = [I64, I64, I, I, I]
+        L.nmo_index_packed_words.restype = I64
+        L.nmo_index_pack.argtypes = [P, I64, I64, I, I, I, P]
+        L.nmo_index_unpack.argtypes = [P, I64, I64, I, I, I, P]
         _lib = L
     return _lib
 
@@ -225,3 +230,30 @@ def rel_frobenius(C: np.ndarray, C_ref: np.ndarray) -> float:
     den = np.linalg.norm(np.asarray(C_ref, dtype=np.float64))
     num = np.linalg.norm(d)
     return float(num / den) if den > 0 else float(num)
+
+
+def index_bits(M: int) -> int:
+    """bits per packed index entry, max(1, ceil(log2 M))."""
+    return int(lib().nmo_index_bits(M))
+
+
+def index_pack(D: np.ndarray, k: int, n: int, N: int, M: int, L: int) -> np.ndarray:
+    """P:288 + P:419 (transformLayout): D (w x q uint8) -> the tile-major bit-packed words
+    (R28; layout in nm_oracle.c).  Needs 128 % L == 0."""
+    nw = int(lib().nmo_index_packed_words(k, n, N, M, L))
+    if nw < 0:
+        raise OracleError(ERR_SHAPE, "index_pack")
+    out = np.empty(max(nw, 1), dtype=np.uint32)
+    s = lib().nmo_index_pack(_p(_c(D.astype(np.uint8, copy=False))), k, n, N, M, L, _p(out))
+    if s:
+        raise OracleError(s, "index_pack")
+    return out[:nw]
+
+
+def index_unpack(P: np.ndarray, k: int, n: int, N: int, M: int, L: int) -> np.ndarray:
+    w, q = k // M * N, n // L
+    D = np.empty((w, q), dtype=np.uint8)
+    s = lib().nmo_index_unpack(_p(_c(P.astype(np.uint32, copy=False))), k, n, N, M, L, _p(D))
+    if s:
+        raise OracleError(s, "index_unpack")
+    return D

@@ -413,3 +413,70 @@ def test_eq1_scaled_dense_window_is_gemm(oracle, L):
     C = oracle.gemm_dense_f64(A, B)
     assert np.allclose(Cs, C, rtol=1e-12, atol=1e-12)
     assert np.abs(oracle.confusion(Cs, C)).max() <= 1e-12
+
+
+def test_rel_frobenius_hand_values(oracle):
+    """SURVEY 8(c)5 tolerance metric ||C - C_ref||_F / ||C_ref||_F, pinned by hand-computed
+    values (not by restating the formula): a dropped square root, a swapped numerator /
+    denominator or a missing zero-reference branch each fails one of these."""
+    # ||(0, -4)|| / ||(3, 4)|| = 4 / 5
+    assert oracle.rel_frobenius(np.array([[3.0, 0.0]]), np.array([[3.0, 4.0]])) == 0.8
+    # the reference is the denominator: ||(0, 4)|| / ||(3, 0)|| = 4 / 3
+    assert abs(oracle.rel_frobenius(np.array([[3.0, 4.0]]), np.array([[3.0, 0.0]])) - 4.0 / 3.0) < 1e-15
+    # Frobenius over all elements of a 2-D array: diff (1, 2; 2, 0) has norm 3, ref (2, 0; 0, 0) norm 2
+    assert oracle.rel_frobenius(np.array([[3.0, 2.0], [2.0, 0.0]]), np.array([[2.0, 0.0], [0.0, 0.0]])) == 1.5
+    # zero reference: the absolute norm of C (||(3, 4)|| = 5), and 0 for C = C_ref = 0
+    assert oracle.rel_frobenius(np.array([[3.0, 4.0]]), np.zeros((1, 2))) == 5.0
+    assert oracle.rel_frobenius(np.zeros((2, 2)), np.zeros((2, 2))) == 0.0
+    # identical inputs give exactly 0; a uniform 1e-3 relative perturbation gives 1e-3
+    R = np.arange(1.0, 13.0).reshape(3, 4)
+    assert oracle.rel_frobenius(R, R) == 0.0
+    assert abs(oracle.rel_frobenius(R * (1 + 1e-3), R) - 1e-3) < 1e-12
+    # fp32 / bf16-widened inputs are compared in fp64 (no float32 cancellation): 1 + 2^-30 vs 1
+    assert oracle.rel_frobenius(np.array([[1.0 + 2.0 ** -30]]), np.array([[1.0]], dtype=np.float32)) == 2.0 ** -30
+
+
+# ----------------------------------------------------------------------------- bit-packed indices
+def test_index_bits_closed_form(oracle):
+    """an index needs only ceil(log2 M) bits: the largest offset M - 1 fits in b bits and
+    not in b - 1 (b >= 1)."""
+    for M in [1, 2, 3, 4, 5, 7, 8, 9, 16, 31, 32, 33, 64, 100, 128, 129, 255, 256]:
+        b = oracle.index_bits(M)
+        assert (M - 1) < (1 << b)
+        assert b == 1 or (M - 1) >= (1 << (b - 1))
+
+
+def test_index_pack_hand_example(oracle):
+    """Hand-packed words (R28).  M = 4 -> 2-bit entries, 16 per word; L = 32 -> tiles of
+    T = 4 groups, a tile's entries numbered x = u*T + t.  w = 4 rows -> 16 entries = 1 word per tile.
+    Row 0 of groups 0..7 = [1, 3, 0, 2 | 2, 1, 3, 0], row 1 = [3, 0, 0, 0 | 0, 0, 0, 1]:
+    tile 0 = 1 + 3*4 + 0*16 + 2*64 + 3*256 = 909, tile 1 = 2 + 1*4 + 3*16 + 0*64 + 1*2^14 = 16438."""
+    k, n, N, M, L = 8, 256, 2, 4, 32
+    D = np.zeros((4, 8), dtype=np.uint8)
+    D[0] = [1, 3, 0, 2, 2, 1, 3, 0]
+    D[1] = [3, 0, 0, 0, 0, 0, 0, 1]
+    P = oracle.index_pack(D, k, n, N, M, L)
+    assert list(P) == [909, 16438]
+    # M = 32 -> 5-bit entries, 6 per word; L = 16 -> tiles of 8 groups; one row = 2 words:
+    # [31, 0, 7, 16, 1, 2 | 30, 5] -> 31 + 7*2^10 + 16*2^15 + 2^20 + 2*2^25 = 68688927, 30 + 5*32 = 190
+    D2 = np.array([[31, 0, 7, 16, 1, 2, 30, 5]], dtype=np.uint8)
+    P2 = oracle.index_pack(D2, 32, 128, 1, 32, 16)
+    assert list(P2) == [68688927, 190]
+
+
+@pytest.mark.parametrize("N,M,L", [(2, 4, 4), (16, 32, 32), (4, 32, 8), (3, 8, 16), (1, 2, 64), (5, 256, 128),
+                                   (12, 32, 32), (7, 100, 4)])
+def test_index_pack_roundtrip_and_size(oracle, N, M, L):
+    """Lossless (unpack . pack = identity on compressed indices, ragged last tile included) and the
+    footprint of log2-M-bit entries: 32 / floor(32 / b) bits per entry + at most one partial word
+    per tile (b = 5 at M = 32: 5.33 bits instead of the 8 of a byte)."""
+    k, n = 8 * M, 128 * 3 + 2 * L
+    B = synth.uniform((k, n), 31, synth.TID_B)
+    _, D = oracle.compress(B, N, M, L)
+    P = oracle.index_pack(D, k, n, N, M, L)
+    assert np.array_equal(oracle.index_unpack(P, k, n, N, M, L), D)
+    b, w, q, T = oracle.index_bits(M), k // M * N, n // L, 128 // L
+    e = 32 // b
+    ntiles = -(-q // T)
+    assert P.size == ntiles * -(-(w * T) // e)
+    assert P.nbytes * 8 * e <= ntiles * T * w * 32 + 32 * ntiles * e  # 32 / e bits per entry
