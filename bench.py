@@ -45,6 +45,8 @@ CONFIGS = {
     "cfg4_65b": (2048, 22016, 8192, 4, 32, 32),
 }
 HEADLINE = "cfg2"
+# one metric string for both arms (the driver pairs the lines by it)
+METRIC = "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M"
 VARIANTS = ["cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_13b:f32", "cfg4_65b:f32", "cfg3_62:bf16",
             "cfg3_75:bf16", "cfg4_13b:bf16", "cfg4_65b:bf16", "cfg2:tf32", "cfg3_62:tf32", "cfg3_75:tf32",
             "cfg4_65b:tf32"]  # tf32 = fp32 operands on the tf32 sparse tensor cores (opt-in math)
@@ -187,7 +189,7 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True, math=None
     nmspmm.nm_profile_begin()
     ms = time_steps(step, steps, 0, stream, flush)
     k_ms, k_cnt, launches = nmspmm.nm_profile_end()
-    t = statistics.fmean(ms)
+    t = statistics.median(ms)
     kms = k_ms / max(1, k_cnt)
     res = {"ms": t, "tflops": flop_count(cfg) / (t * 1e-3) / 1e12, "kernel_ms": kms,
            "kernel_tflops": flop_count(cfg) / (kms * 1e-3) / 1e12, "launches_per_step": launches / steps,
@@ -197,7 +199,7 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True, math=None
         torch.backends.cuda.matmul.allow_tf32 = False
         Cd = torch.empty_like(C)
         msd = time_steps(lambda: torch.mm(A, Bd, out=Cd), steps, warmup, stream, flush)
-        td = statistics.fmean(msd)
+        td = statistics.median(msd)
         m, n, k = cfg[:3]
         res.update({"cublas_ms": td, "cublas_dense_tflops": 2.0 * m * n * k / (td * 1e-3) / 1e12,
                     "speedup_vs_cublas": td / t, "target_speedup": 0.7 * cfg[4] / cfg[3]})
@@ -205,7 +207,7 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True, math=None
             torch.backends.cuda.matmul.allow_tf32 = True
             mst = time_steps(lambda: torch.mm(A, Bd, out=Cd), steps, warmup, stream, flush)
             torch.backends.cuda.matmul.allow_tf32 = False
-            tt = statistics.fmean(mst)
+            tt = statistics.median(mst)
             res.update({"cublas_tf32_dense_tflops": 2.0 * m * n * k / (tt * 1e-3) / 1e12,
                         "speedup_vs_cublas_tf32": tt / t})
     del A, Bd, W, C
@@ -253,9 +255,21 @@ def cpu_baseline(cfg, target_s=10.0):
     t = time.perf_counter() - t0
     w = k // M * N
     return {"value": round(2.0 * rows * n * w / t / 1e12, 6), "unit": "TFLOP/s (effective, kept MACs)",
-            "cores": threads, "kind": "oracle",
+            "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{rows} of {m} rows (all {n} columns) of {cfg_name(cfg)}, O2 fp64 sparse loop, {t:.1f} s",
             "seconds": round(t, 3)}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
 
 
 def cfg_name(cfg):
@@ -296,11 +310,13 @@ def run_reference(args):
     timed = runs[args.warmup:]
     v = statistics.median(r["value"] for r in timed)
     w = cfg[2] // cfg[4] * cfg[3]
-    line = {"impl": "reference", "metric": "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M",
+    line = {"impl": "reference", "metric": METRIC,
             "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": None, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": config_dict(cfg, "f32 in, fp64 accumulate"),
-            "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample")} | {"value": v},
+            "dtype": "f64", "data": "synthetic",
+            "config": config_dict(cfg, args.dtype, {"parallelism": "single GPU" if args.gpus == 1 else
+                                                    f"col{args.gpus}"}),
+            "cpu_baseline": {k: timed[-1][k] for k in ("kind", "cores", "sample", "cpu_model")} | {"value": v},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "note": "CPU oracle (plain C, OpenMP over rows) on a bounded row sample per step; "
                     f"full step would be {2.0 * cfg[0] * cfg[1] * w / (v * 1e12):.1f} s"}
@@ -352,7 +368,7 @@ def run_ours(args):
             ms = time_steps(step, args.steps, 0, stream, flush)
             k_ms, k_cnt, launches = nmspmm.nm_profile_end()
             wall = time.perf_counter() - t0
-        t_step = statistics.fmean(ms)
+        t_step = statistics.median(ms)
         value = flop_count(cfg) / (t_step * 1e-3) / 1e12
         kernel_ms = k_ms / max(1, k_cnt)  # dominant SpMM kernel, CUDA events on its stream
         del Bd
@@ -366,7 +382,7 @@ def run_ours(args):
             Bdense = nmspmm.nm_decompress(W)  # same shape as the dense weight
             Cd = torch.empty_like(C)
             msd = time_steps(lambda: torch.mm(Ad, Bdense, out=Cd), args.steps, args.warmup, stream, flush)
-            td = statistics.fmean(msd)
+            td = statistics.median(msd)
             res = {"cublas_ms": td, "cublas_dense_tflops": 2.0 * m * n * k / (td * 1e-3) / 1e12,
                    "speedup_vs_cublas": td / t_step, "target_speedup_0.7xM/N": 0.7 * M / N}
             del Bdense, Cd
@@ -397,7 +413,7 @@ def run_ours(args):
     roof["traffic"] = tr["dram_bytes_per_launch"] if tr else None
     roof["traffic_source"] = tr["source"] if tr else "no ncu capture for this config"
 
-    line = {"metric": "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M; speedup vs cuBLAS dense",
+    line = {"metric": METRIC,
             "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
@@ -469,7 +485,7 @@ def run_sharded(args):
         ms = time_steps(step, args.steps, 0, stream, flush)
         k_ms, k_cnt, launches = nmspmm.nm_profile_end()
     dist.barrier()
-    t = torch.tensor([statistics.fmean(ms), k_ms / max(1, k_cnt)], device="cuda")
+    t = torch.tensor([statistics.median(ms), k_ms / max(1, k_cnt)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks (step, dominant kernel)
     t_step, t_kernel = t[0].item(), t[1].item()
     # end to end: each rank copies A from pinned host memory, runs the layer, rank 0 reads C back
@@ -484,7 +500,7 @@ def run_sharded(args):
             Ch.copy_(C, non_blocking=True)
 
     mse = time_steps(e2e_step, max(3, args.steps // 4), args.warmup, stream)
-    te = torch.tensor([statistics.fmean(mse)], device="cuda")
+    te = torch.tensor([statistics.median(mse)], device="cuda")
     dist.all_reduce(te, op=dist.ReduceOp.MAX)
     if rank == 0:
         value = flop_count(cfg) / (t_step * 1e-3) / 1e12
@@ -493,7 +509,7 @@ def run_sharded(args):
         local_flops = flop_count(cfg) * layer.nr / n  # this rank's (padded) share
         peak = fp32_alu_peak_tflops(sm_mhz) if dtype == torch.float32 else peaks.get("bf16_tflops", 1590.0)
         ach = local_flops / (t_kernel * 1e-3) / 1e12
-        line = {"metric": "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M; speedup vs cuBLAS dense",
+        line = {"metric": METRIC,
                 "value": round(value, 4), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
@@ -518,6 +534,39 @@ def run_sharded(args):
     return 0
 
 
+def launch_check() -> int:
+    '''--launch-check: every rank joins a gloo group and contributes 1 to an all-reduce; rank 0
+    prints how many ranks it saw (tests the --gpus N self-launch without a GPU).'''
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    t = torch.ones(1)
+    if world > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "world_size": world, "ranks_seen": int(t.item())}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def self_launch(n: int) -> int:
+    '''`python bench.py --gpus N` without torchrun: re-run this command as N ranks under
+    torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1); rank 0 prints the line.'''
+    import socket
+    import subprocess
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -532,11 +581,17 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="column-sharded path even at one rank (testing)")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--launch-check", action="store_true",
+                    help="start the ranks, all-reduce a count over gloo, rank 0 prints it (no GPU needed)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
                     help="sharded path: NCCL all-gather + unshard, or the fused peer-store epilogue (fp32)")
     args = ap.parse_args()
     if args.warmup < 3 and not args.profile:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
+    if args.launch_check:
+        return launch_check()
     if args.impl == "reference":
         return run_reference(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1 or args.sharded:

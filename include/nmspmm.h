@@ -135,13 +135,13 @@ nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, in
  *                                                        tensor-core kernel (tcgen05.mma.sp over the
  *                                                        offline slot packing) when L is 16/32/64/128,
  *                                                        k % 8 == 0, A 16-B and C 4-B aligned; else
- *                                                        the dense-MMA tcgen05 kernels or the generic one
+ *                                                        the generic kernel (one thread per element)
  *                         NM_MATH_AUTO                -> selector (nm_plan_query)
  * bf16 / tf32 without a prepack re-pack the weight on every call (ms); use
  * nm_prepack (nm_prepack_ex for tf32) / nm_spmm_prepacked for repeated products with one weight.
- * No atomics on data: where a tile's k range is split over CTAs (fp32: grids below
- * one wave; bf16: the partial last wave) the partials are added in a fixed order,
- * so results are bit-reproducible run to run (R13).
+ * No atomics on data: where a tile's k range is split over CTAs (grids below one wave, the
+ * partial last wave of the slot kernels) the partials are added in a fixed order, so results
+ * are bit-reproducible run to run for a given shape (R13).
  * m == 0 or n == 0 is a no-op returning NM_OK.  Asynchronous.
  */
 nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
@@ -153,8 +153,8 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
  * paper's approximation C' of the unpruned product being alpha = M/N (R1 reads the product
  * path unscaled: nm_spmm == nm_spmm_scaled with alpha = 1).  alpha is applied in fp32 to the
  * fp32 accumulators inside the epilogue of the SIMT and sparse-tensor-core kernels (after any
- * split-k / tail-split addition, before the bf16 rounding); the other kernels (older tcgen05,
- * generic, pipelined SIMT mode 3) are followed by one in-place scaling pass over C (for a bf16
+ * split-k / tail-split addition, before the bf16 rounding); the other kernels (generic,
+ * pipelined SIMT mode 3) are followed by one in-place scaling pass over C (for a bf16
  * C: a second rounding, exact when alpha is a power of two).  Otherwise as nm_spmm.
  */
 nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
@@ -202,30 +202,40 @@ nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, i
 /*
  * Weight prepack -- the paper's offline PreProcessing step (Listing 3, P:470-475:
  * queryColInfo / reoderingIdx / transformLayout), done once per weight.  For the
- * tcgen05 token-pair path it computes, from B' and D alone: a per-(panel, column
- * group) order of the compressed rows that keeps the gather's shared-memory loads
- * conflict-free, the correspondingly reordered B' and the gather's cell tables.
- * Other paths keep using `values` / `idx` directly (kind 0).
- *   nm_prepack_bytes : device bytes needed in `buf` (0 for kind 0; -1 on bad args).
- *   nm_prepack       : fills `buf` (device, caller-owned) and the host descriptor
- *                      `*out`; `values` and `idx` must stay alive and unmodified
- *                      while `*out` is used.  Asynchronous on `stream`.
- *   nm_spmm_prepacked: C (m x n, c_dt) = A (m x k) . decompress(values, idx), same
- *                      semantics and parity as nm_spmm.  Asynchronous.
+ * sparse-tensor-core slot kernels (bf16: kind 2; tf32: kind 3) it computes, from B' and D
+ * alone: per column tile of 128 H output columns the union of the k rows its groups keep (the
+ * paper's col_info) packed into 2:4-compatible slot quads (bf16) or 1:2 pairs (tf32),
+ * the slot list (row of A^T per slot) and the exact shared-memory images of the compressed
+ * weights + sparse-MMA metadata per 64- (bf16) / 32-slot (tf32) stage.  The buffer is compact:
+ *   [header 256 B | per tile {stages, first slot, image offset, image size} | slot lists |
+ *    stage images (even stages: H x (8 KB weights + 2 KB metadata of the stage pair), odd: H x 8 KB)]
+ * Other weights keep using `values` / `idx` directly (kind 0, no buffer).
+ *   nm_prepack_bytes[_ex]: a data-independent UPPER BOUND of the buffer (0 for kind 0; -1 on bad
+ *                      args).  Host only.
+ *   nm_prepack_size  : the EXACT buffer size for this weight (*bytes; 0 for kind 0): runs the slot
+ *                      packing on `stream` and SYNCHRONIZES it.  Device pointers values / idx.
+ *   nm_prepack[_ex]  : fills `buf` (device, caller-owned, buf_bytes >= nm_prepack_size; a buffer
+ *                      below the bound makes the call check the exact size, synchronizing) and the
+ *                      host descriptor `*out`; `values` and `idx` must stay alive and unmodified
+ *                      while `*out` is used.  Asynchronous on `stream` otherwise.
+ *   nm_spmm_prepacked: C (m x n, c_dt) = A (m x k) . decompress(values, idx), same semantics and
+ *                      parity as nm_spmm (A's dtype must be the weight's).  Asynchronous.
  */
 typedef struct {
     int32_t magic;   /* 0x4B504D4E ("NMPK") once filled */
-    int32_t kind;    /* 0 = plain (values/idx used directly), 1 = tcgen05 token-pair prepack,
+    int32_t kind;    /* 0 = plain (values/idx used directly),
                         2 = sparse-tensor-core slot prepack, bf16 (whole buffer at `bperm`),
                         3 = the same for tf32 (fp32 weights, nm_prepack_ex with NM_MATH_TF32_TC) */
     int32_t dtype, N, M, L;
     int64_t n, k;
-    int32_t bn, wp, bk, bkw, bkw_pad, npanels;
+    int32_t bn;      /* kind 2/3: output columns per tile (128 H) */
+    int32_t wp, bk, bkw, bkw_pad;  /* reserved (0) */
+    int32_t npanels; /* kind 2/3: column tiles */
     const void* values;
     const uint8_t* idx;
-    void* perm;      /* inside buf (kind 1) */
-    void* tbl;
-    void* bperm;     /* reordered B' as per-(column tile, panel) swizzled shared-memory images */
+    void* perm;      /* reserved (NULL) */
+    void* tbl;       /* reserved (NULL) */
+    void* bperm;     /* kind 2/3: the prepacked buffer */
 } nm_prepacked;
 
 int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt);
@@ -238,6 +248,8 @@ nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64
  * nm_spmm_prepacked on kind 3 runs the tf32 kernel (c_dt must be NM_F32) and reports
  * NM_ERR_UNSUPPORTED where nm_spmm with NM_MATH_TF32_TC would. */
 int64_t nm_prepack_bytes_ex(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math);
+nm_status nm_prepack_size(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L,
+                          nm_dtype dt, nm_math math, int64_t* bytes, void* stream);
 nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
                         nm_math math, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
 
@@ -257,14 +269,16 @@ nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64
  *                       G, i < m, j < n_valid (the shard's unpadded columns; nr = its padded
  *                       width, values w x nr, idx w x nr/L); C_p are device pointers valid in
  *                       this process (own buffer or IPC-mapped peers), row pitch ldc floats.
- *                       fp32 operands on the SIMT kernel (16-B aligned, ldc and col_off
- *                       multiples of 4), else NM_ERR_UNSUPPORTED.  Asynchronous.
+ *                       fp32 operands on the SIMT kernel (16-B aligned, ldc, col_off and
+ *                       n_valid multiples of 4), else NM_ERR_UNSUPPORTED / NM_ERR_SHAPE.
+ *                       Asynchronous.
  *   nm_peer_barrier   : flag_peers[p] = rank p's int[G] flag array (mapped here); publishes
  *                       `epoch` in every rank's flags[rank] (system-scope release after the
  *                       stream's earlier work, i.e. after this rank's peer stores) and waits on
  *                       the stream until every rank has published `epoch` in ours.  Epochs
  *                       must increase by one per call on all ranks; a rank that never arrives
- *                       makes the kernel trap after ~2^26 polls instead of hanging.  1 <= G <= 8.
+ *                       makes the kernel trap after NM_PEER_TIMEOUT_MS (environment, default
+ *                       120000 ms of wall time) instead of hanging.  1 <= G <= 8.
  */
 nm_status nm_ipc_get_handle(const void* dptr, void* handle, int64_t* offset);
 nm_status nm_ipc_open_handle(const void* handle, int64_t offset, void** dptr);
@@ -273,10 +287,11 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
                         int64_t ldc, int64_t col_off, int64_t n_valid, int64_t m, int64_t nr, int64_t k, int N,
                         int M, int L, void* stream);
 nm_status nm_peer_barrier(void* const* flag_peers, int G, int rank, int epoch, void* stream);
-/* The same for a prepacked shard (nm_prepack / nm_prepack_ex): kind 0 -> nm_spmm_peers; kind 2
- * (bf16) / 3 (tf32, c_dt NM_F32) -> the sparse-tensor-core slot kernel with its direct-store
- * epilogue writing every C element to all G buffers (c_dt bf16 or fp32; C pointers, ldc and
- * col_off 4-B aligned, A 16-B aligned, k % 8 == 0); kind 1 -> NM_ERR_UNSUPPORTED.  Asynchronous. */
+/* The same for a prepacked shard (nm_prepack / nm_prepack_ex): kind 0 with fp32 values and an
+ * fp32 C -> nm_spmm_peers (any other kind-0 weight: NM_ERR_UNSUPPORTED); kind 2 (bf16) / 3
+ * (tf32, c_dt NM_F32) -> the sparse-tensor-core slot kernel with its direct-store epilogue
+ * writing every C element to all G buffers (c_dt bf16 or fp32; C pointers, ldc and col_off 4-B
+ * aligned, A 16-B aligned, k % 8 == 0; a bf16 C needs an even n_valid).  Asynchronous. */
 nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* const* C_peers, int G, int64_t ldc,
                                   int64_t col_off, int64_t n_valid, int64_t m, nm_dtype c_dt, void* stream);
 

@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 #include <vector>
 
@@ -29,27 +30,36 @@ nm_status cuda_fail(cudaError_t e, const char* what) {
     return NM_ERR_CUDA;
 }
 
-static std::once_flag g_props_once;
-static int g_num_sms = 0;
-static int g_cc = 0;
+// Device properties, cached per device ordinal (a process may drive several GPUs): SM count and
+// compute capability of the CURRENT device.  Benign races: every thread computes the same values.
+constexpr int kMaxDev = 64;
+static std::atomic<int> g_sms[kMaxDev];
+static std::atomic<int> g_ccs[kMaxDev];
 
-static void read_props() {
+int current_device() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) {
         cudaGetLastError();
-        return;
+        return -1;
     }
+    return dev;
+}
+
+static void read_props(int dev) {
+    if (dev < 0 || dev >= kMaxDev || g_ccs[dev].load(std::memory_order_acquire) != 0) return;
     int sms = 0, major = 0, minor = 0;
-    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) g_num_sms = sms;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) g_sms[dev].store(sms);
     if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) == cudaSuccess &&
         cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) == cudaSuccess)
-        g_cc = major * 10 + minor;
+        g_ccs[dev].store(major * 10 + minor, std::memory_order_release);
     cudaGetLastError();
 }
 
 int num_sms() {
-    std::call_once(g_props_once, read_props);
-    return g_num_sms > 0 ? g_num_sms : 148;
+    const int dev = current_device();
+    read_props(dev);
+    const int v = (dev >= 0 && dev < kMaxDev) ? g_sms[dev].load() : 0;
+    return v > 0 ? v : 148;
 }
 
 nm_status require_device() {  // also used by peer.cu
@@ -59,11 +69,23 @@ nm_status require_device() {  // also used by peer.cu
         cudaGetLastError();
         return fail(NM_ERR_CUDA, "no CUDA device: libnmspmm has no CPU fallback");
     }
-    std::call_once(g_props_once, read_props);
-    if (g_cc != 100)
+    const int dev = current_device();
+    read_props(dev);
+    const int cc = (dev >= 0 && dev < kMaxDev) ? g_ccs[dev].load() : 0;
+    if (cc != 100)
         return fail(NM_ERR_UNSUPPORTED, "libnmspmm is built for sm_100a (B200); device compute capability is " +
-                                            std::to_string(g_cc));
+                                            std::to_string(cc));
     return NM_OK;
+}
+
+bool attr_once(std::atomic<uint64_t>& mask) {
+    const int dev = current_device();
+    if (dev < 0 || dev >= 64) return true;
+    return (mask.load(std::memory_order_acquire) >> dev) & 1u;
+}
+void attr_done(std::atomic<uint64_t>& mask) {
+    const int dev = current_device();
+    if (dev >= 0 && dev < 64) mask.fetch_or(1ull << dev, std::memory_order_acq_rel);
 }
 
 // ------------------------------------------------------------ profiling
@@ -97,26 +119,33 @@ void prof_end(cudaStream_t s) { prof_record(s); }
 // Per-call scratch (the tcgen05 path's cell tables) comes from a library-owned
 // stream-ordered pool whose release threshold keeps freed blocks cached, so a
 // steady stream of nm_spmm calls allocates nothing after the first one.
-static std::once_flag g_pool_once;
-static cudaMemPool_t g_pool = nullptr;
+// One pool per device (the pool of the current device, which owns the caller's stream).
+static std::mutex g_pool_mu;
+static cudaMemPool_t g_pool[kMaxDev] = {};
+static bool g_pool_tried[kMaxDev] = {};
 
 nm_status scratch_alloc(void** p, size_t bytes, cudaStream_t s) {
-    std::call_once(g_pool_once, [] {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaMemPoolProps props{};
-        props.allocType = cudaMemAllocationTypePinned;
-        props.location.type = cudaMemLocationTypeDevice;
-        props.location.id = dev;
-        if (cudaMemPoolCreate(&g_pool, &props) == cudaSuccess) {
-            uint64_t thr = ~0ull;
-            cudaMemPoolSetAttribute(g_pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        } else {
-            g_pool = nullptr;
+    const int dev = current_device();
+    cudaMemPool_t pool = nullptr;
+    if (dev >= 0 && dev < kMaxDev) {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (!g_pool_tried[dev]) {
+            g_pool_tried[dev] = true;
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            if (cudaMemPoolCreate(&g_pool[dev], &props) == cudaSuccess) {
+                uint64_t thr = ~0ull;
+                cudaMemPoolSetAttribute(g_pool[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+            } else {
+                g_pool[dev] = nullptr;
+            }
+            cudaGetLastError();
         }
-        cudaGetLastError();
-    });
-    cudaError_t e = g_pool ? cudaMallocFromPoolAsync(p, bytes, g_pool, s) : cudaMallocAsync(p, bytes, s);
+        pool = g_pool[dev];
+    }
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(p, bytes, pool, s) : cudaMallocAsync(p, bytes, s);
     if (e != cudaSuccess) return cuda_fail(e, "scratch allocation");
     return NM_OK;
 }
@@ -206,18 +235,14 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
 bool simt_pipe_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 nm_status simt_pipe_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                            int N, int M, int L, cudaStream_t s);
-bool tc_bf16_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
-                        int L);
-void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn);
-nm_status tc_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                         int64_t k, int N, int M, int L, cudaStream_t s);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 // tf: fp32 operands on the tf32 sparse tensor cores (1:2 slot pairs), else bf16 (2:4 slot quads)
-size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf);
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf);  // bound (no data)
+int tc_sp_halves(int N, int M, int L);
 void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int* tokens);
-nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, void* buf,
-                        cudaStream_t s);
-nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
+nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, int H,
+                        void* buf, int64_t buf_bytes, int64_t* exact, bool query_only, cudaStream_t s);
+nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
                     int M, int L, bool tf, cudaStream_t s, const PeerOut* po = nullptr, float alpha = 1.f);
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                        int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha = 1.f);
@@ -344,9 +369,7 @@ static nm_status select(const void* A, const void* Bv, const void* C, int64_t m,
     }
     if (math == NM_MATH_AUTO || math == NM_MATH_BF16_TC) {
         *used = NM_MATH_BF16_TC;
-        *kernel = tc_sp_ok(A, C, m, n, k, N, M, L)                  ? K_TC_SP
-                  : tc_bf16_applicable(A, Bv, C, m, n, k, N, M, L) ? K_TC_BF16
-                                                                    : K_GENERIC;
+        *kernel = tc_sp_ok(A, C, m, n, k, N, M, L) ? K_TC_SP : K_GENERIC;
         return NM_OK;
     }
     return fail(NM_ERR_UNSUPPORTED, "math mode not available for bf16 operands");
@@ -461,8 +484,6 @@ nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, 
     } else if (kernel == K_TC_SP || kernel == K_TC_TF32) {
         st = tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, kernel == K_TC_TF32, s, alpha);
         fused = true;
-    } else if (kernel == K_TC_BF16) {
-        st = tc_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, s);
     } else if (ab_dt == NM_F32) {
         st = generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
     } else if (c_dt == NM_BF16) {
@@ -547,10 +568,12 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     const int64_t rc = ceil_div(ceil_div(m, nch), 128) * 128;
     // slot kernels: prepack the weight once (the paper's offline step, here per call) on s
     const bool slot = kernel == K_TC_SP || kernel == K_TC_TF32, tf = kernel == K_TC_TF32;
+    const int hsp = tc_sp_halves(N, M, L);
     void* pbuf = nullptr;
     if (slot) {
-        if ((st = scratch_alloc(&pbuf, tc_sp_prepack_bytes(n, k, N, M, L, tf), s))) return st;
-        if ((st = tc_sp_prepack(dV, dD, n, k, N, M, L, tf, pbuf, s))) {
+        const size_t pb = tc_sp_prepack_bytes(n, k, N, M, L, tf);
+        if ((st = scratch_alloc(&pbuf, pb, s))) return st;
+        if ((st = tc_sp_prepack(dV, dD, n, k, N, M, L, tf, hsp, pbuf, static_cast<int64_t>(pb), nullptr, false, s))) {
             cudaFreeAsync(pbuf, s);
             return st;
         }
@@ -575,7 +598,7 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
         if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i], hs);
         if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * i], 0);
         if (ce != cudaSuccess) break;
-        st = slot ? tc_sp_run(dA + r0 * k * e, pbuf, dC + r0 * n * ec, c_dt == NM_BF16, r1 - r0, n, k, N, M, L, tf, s)
+        st = slot ? tc_sp_run(dA + r0 * k * e, pbuf, hsp, dC + r0 * n * ec, c_dt == NM_BF16, r1 - r0, n, k, N, M, L, tf, s)
                   : nm_spmm(dA + r0 * k * e, dV, dD, dC + r0 * n * ec, r1 - r0, n, k, N, M, L, ab_dt, c_dt, math, stream);
         if (st) {
             cudaStreamSynchronize(s);
@@ -645,17 +668,6 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
             out->stages = st;
             out->smem_bytes = st * per + 1280;
         }
-    } else if (kernel == K_TC_BF16) {
-        int wp, bk, bkw, bkwp, bn;
-        tc_bf16_geometry(N, M, L, &wp, &bk, &bkw, &bkwp, &bn);
-        out->bm = 128;
-        out->bn = bn;
-        out->bk = bk;
-        out->bkw = bkw;
-        out->stages = 3;
-        out->threads = 544;
-        out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, bn));
-        out->smem_bytes = 3 * 64 * bn * 2 + 2 * 128 * (128 * 2 + 4) + 2 * 3 * 256 * 4 + 15 * 8 + 16 + 1024;
     } else {
         out->bm = 8;
         out->bn = 32;
@@ -676,28 +688,8 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
 // ------------------------------------------------------------------ prepack
 }  // extern "C"
 namespace nm {
-void tc_bf16_geometry(int N, int M, int L, int* wp, int* bk, int* bkw, int* bkw_pad, int* bn);
-bool tc_pair_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L, int bn, int bkw_pad);
-void tc_pair_sizes(int64_t n, int64_t k, int N, int M, int L, int wp, int bkwp, int bn, size_t* perm_bytes,
-                   size_t* tbl_bytes, size_t* bp_bytes);
-nm_status tc_pair_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, int wp, int bk,
-                          int bkw, int bkwp, int bn, uint8_t* perm, uint32_t* tbl, void* bp, cudaStream_t s);
-nm_status tc_pair_run(const void* A, const uint32_t* tbl, const void* bp, void* C, bool c_bf16, int64_t m, int64_t n,
-                      int64_t k, int N, int M, int L, int wp, int bk, int bkw, int bkwp, int bn, cudaStream_t s);
-
 static const int32_t kPrepackMagic = 0x4B504D4E;
-static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
 
-// kind 1 iff the bf16 tcgen05 token-pair kernel would run for this weight
-static bool prepack_kind1(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, int* g) {
-    if (dt != NM_BF16) return false;
-    static const float dummy[4] = {0, 0, 0, 0};
-    if (!tc_bf16_applicable(dummy, dummy, dummy, 1, n, k, N, M, L)) return false;
-    const char* pe = getenv("NM_TC_PAIR");
-    if (pe && pe[0] == '0') return false;
-    tc_bf16_geometry(N, M, L, &g[0], &g[1], &g[2], &g[3], &g[4]);
-    return tc_pair_applicable(1, n, k, N, M, L, g[4], g[3]);
-}
 // kind 3 iff the tf32 slot kernel is asked for and applies (aligned operands assumed)
 static bool prepack_kind3(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
     static const float dummy[4] = {0, 0, 0, 0};
@@ -708,22 +700,37 @@ static bool prepack_kind2(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt
     static const float dummy[4] = {0, 0, 0, 0};
     return dt == NM_BF16 && k > 0 && tc_sp_ok(dummy, dummy, 1, n, k, N, M, L);
 }
+// 2 / 3 = slot images (bf16 / tf32), 0 = none (values / idx used directly)
+static int prepack_kind(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
+    if (prepack_kind3(n, k, N, M, L, dt, math)) return 3;
+    if (prepack_kind2(n, k, N, M, L, dt)) return 2;
+    return 0;
+}
 }  // namespace nm
 extern "C" {
 
 int64_t nm_prepack_bytes_ex(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
     if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16 || math > NM_MATH_BF16_TC) return -1;
-    if (prepack_kind3(n, k, N, M, L, dt, math)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, true));
-    if (prepack_kind2(n, k, N, M, L, dt)) return static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, false));
-    int g[5];
-    if (!prepack_kind1(n, k, N, M, L, dt, g)) return 0;
-    size_t pb, tb, bb;
-    tc_pair_sizes(n, k, N, M, L, g[0], g[3], g[4], &pb, &tb, &bb);
-    return static_cast<int64_t>(al256(pb) + al256(tb) + al256(bb));
+    const int kind = prepack_kind(n, k, N, M, L, dt, math);
+    return kind ? static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, kind == 3)) : 0;
 }
 
 int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt) {
     return nm_prepack_bytes_ex(n, k, N, M, L, dt, NM_MATH_AUTO);
+}
+
+nm_status nm_prepack_size(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                          nm_math math, int64_t* bytes, void* stream) {
+    nm_status st = check_common(0, n, k, N, M, L);
+    if (st) return st;
+    if (!bytes || (n * k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_prepack_size: NULL pointer");
+    if (dt > NM_BF16 || math > NM_MATH_BF16_TC) return fail(NM_ERR_UNSUPPORTED, "dtype/math");
+    const int kind = prepack_kind(n, k, N, M, L, dt, math);
+    *bytes = 0;
+    if (!kind) return NM_OK;
+    if ((st = require_device())) return st;
+    return tc_sp_prepack(values, idx, n, k, N, M, L, kind == 3, tc_sp_halves(N, M, L), nullptr, 0, bytes, true,
+                         static_cast<cudaStream_t>(stream));
 }
 
 nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
@@ -741,43 +748,21 @@ nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64
     out->k = k;
     out->values = values;
     out->idx = idx;
-    int g[5];
-    if (prepack_kind3(n, k, N, M, L, dt, math)) {
-        const int64_t need = nm_prepack_bytes_ex(n, k, N, M, L, dt, math);
-        if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
+    const int kind = prepack_kind(n, k, N, M, L, dt, math);
+    if (kind) {
+        if (!buf) return fail(NM_ERR_NULL, "nm_prepack: buffer missing (size: nm_prepack_size)");
         if ((st = require_device())) return st;
-        out->kind = 3;
+        const int H = tc_sp_halves(N, M, L);
+        // exact size check when the buffer is below the data-independent bound (synchronizes)
+        const bool check = buf_bytes < static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, kind == 3));
+        int64_t need = 0;
+        st = tc_sp_prepack(values, idx, n, k, N, M, L, kind == 3, H, buf, buf_bytes, check ? &need : nullptr, false,
+                           static_cast<cudaStream_t>(stream));
+        if (st) return st;
+        out->kind = kind;
         out->bperm = buf;
-        st = tc_sp_prepack(values, idx, n, k, N, M, L, true, buf, static_cast<cudaStream_t>(stream));
-        if (st) return st;
-    } else if (prepack_kind2(n, k, N, M, L, dt)) {
-        const int64_t need = nm_prepack_bytes(n, k, N, M, L, dt);
-        if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
-        if ((st = require_device())) return st;
-        out->kind = 2;
-        out->bperm = buf;
-        st = tc_sp_prepack(values, idx, n, k, N, M, L, false, buf, static_cast<cudaStream_t>(stream));
-        if (st) return st;
-    } else if (prepack_kind1(n, k, N, M, L, dt, g)) {
-        const int64_t need = nm_prepack_bytes(n, k, N, M, L, dt);
-        if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or smaller than nm_prepack_bytes");
-        if ((st = require_device())) return st;
-        size_t pb, tb, bb;
-        tc_pair_sizes(n, k, N, M, L, g[0], g[3], g[4], &pb, &tb, &bb);
-        uint8_t* base = static_cast<uint8_t*>(buf);
-        out->perm = base;
-        out->tbl = base + al256(pb);
-        out->bperm = base + al256(pb) + al256(tb);
-        out->wp = g[0];
-        out->bk = g[1];
-        out->bkw = g[2];
-        out->bkw_pad = g[3];
-        out->bn = g[4];
-        out->npanels = static_cast<int32_t>((k / M + g[0] - 1) / g[0]);
-        out->kind = 1;
-        st = tc_pair_prepack(values, idx, n, k, N, M, L, g[0], g[1], g[2], g[3], g[4], static_cast<uint8_t*>(out->perm),
-                             static_cast<uint32_t*>(out->tbl), out->bperm, static_cast<cudaStream_t>(stream));
-        if (st) return st;
+        out->bn = 128 * H;                                                    // output columns per tile
+        out->npanels = static_cast<int32_t>((n + 128 * H - 1) / (128 * H));  // column tiles
     }
     out->magic = kPrepackMagic;
     return NM_OK;
@@ -790,38 +775,18 @@ nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t 
 
 nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt, void* stream) {
     if (!w || w->magic != kPrepackMagic) return fail(NM_ERR_NULL, "nm_spmm_prepacked: descriptor not filled by nm_prepack");
-    if (w->kind == 3) {  // tf32 slot images: the tf32 kernel or the same error nm_spmm gives
+    if (w->kind == 2 || w->kind == 3) {
+        const bool tf = w->kind == 3;
         nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
         if (st) return st;
-        if (c_dt != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
-        if (m == 0 || w->n == 0) return NM_OK;
-        if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
-        if ((st = require_device())) return st;
-        if (!tc_sp_ok(A, C, m, w->n, w->k, w->N, w->M, w->L))
-            return fail(NM_ERR_UNSUPPORTED, "tf32 sparse-tensor-core path needs A 16-B and C 4-B aligned");
-        return tc_sp_run(A, w->bperm, C, false, m, w->n, w->k, w->N, w->M, w->L, true, static_cast<cudaStream_t>(stream));
-    }
-    if (w->kind == 2) {
-        nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
-        if (st) return st;
+        if (tf && c_dt != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
         if (m == 0 || w->n == 0) return NM_OK;
         if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
         if ((st = require_device())) return st;
         if (tc_sp_ok(A, C, m, w->n, w->k, w->N, w->M, w->L))
-            return tc_sp_run(A, w->bperm, C, c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, false,
+            return tc_sp_run(A, w->bperm, w->bn / 128, C, c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, tf,
                              static_cast<cudaStream_t>(stream));
-    }
-    if (w->kind == 1) {
-        nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
-        if (st) return st;
-        if (m == 0 || w->n == 0) return NM_OK;
-        if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
-        if ((st = require_device())) return st;
-        // the token-pair kernel needs 16-B aligned A / C; otherwise fall through to the plain path
-        if (((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(C)) & 15) == 0 && w->k > 0)
-            return tc_pair_run(A, static_cast<const uint32_t*>(w->tbl), w->bperm, C, c_dt == NM_BF16, m, w->n, w->k,
-                               w->N, w->M, w->L, w->wp, w->bk, w->bkw, w->bkw_pad, w->bn,
-                               static_cast<cudaStream_t>(stream));
+        if (tf) return fail(NM_ERR_UNSUPPORTED, "tf32 sparse-tensor-core path needs A 16-B and C 4-B aligned");
     }
     return nm_spmm(A, w->values, w->idx, C, m, w->n, w->k, w->N, w->M, w->L, static_cast<nm_dtype>(w->dtype), c_dt,
                    NM_MATH_AUTO, stream);

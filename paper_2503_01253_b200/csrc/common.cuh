@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 
 #include "../../include/nmspmm.h"
@@ -30,7 +31,13 @@ nm_status cuda_fail(cudaError_t e, const char* what);
         if (_e != cudaSuccess) return ::nm::cuda_fail(_e, what);  \
     } while (0)
 
-int num_sms();  // cached device property (148 on B200)
+int num_sms();         // SM count of the current device (cached per device; 148 on B200)
+int current_device();  // cudaGetDevice, -1 on error
+// Once-per-device guards for cudaFuncSetAttribute (MaxDynamicSharedMemorySize is a per-device
+// setting): attr_once(mask) is true once attr_done(mask) ran on the current device.  Racing
+// threads may both set the attribute, which is idempotent.
+bool attr_once(std::atomic<uint64_t>& mask);
+void attr_done(std::atomic<uint64_t>& mask);
 nm_status scratch_alloc(void** p, size_t bytes, cudaStream_t s);  // library-owned stream-ordered pool
 
 // Launch accounting for nm_profile_begin/end: every kernel launch of the product

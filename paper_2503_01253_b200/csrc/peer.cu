@@ -4,6 +4,7 @@
 // ranks -- no separate all-gather pass and no unshard pass.  Column j of C depends only on A,
 // B'[:, j] and D[:, j / L] (Eq. 1), so the ranks' stores never overlap.
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -15,8 +16,8 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 nm_status require_device();
-nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M,
-                    int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha);
+nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
+                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 
 struct PeerFlags {
@@ -27,7 +28,7 @@ struct PeerFlags {
 // release after a system fence, so this rank's earlier peer stores -- the SpMM kernel before
 // this one on the stream -- are visible to whoever acquires the flag), then wait until rank p
 // has published the same epoch in ours.  Bounded spin: a missing rank is a bug, trap, do not hang.
-__global__ void peer_barrier_kernel(PeerFlags pf, int G, int rank, int epoch) {
+__global__ void peer_barrier_kernel(PeerFlags pf, int G, int rank, int epoch, unsigned long long timeout_ns) {
     const int t = threadIdx.x;
     if (t < G) {
         __threadfence_system();
@@ -36,12 +37,17 @@ __global__ void peer_barrier_kernel(PeerFlags pf, int G, int rank, int epoch) {
     __syncwarp();
     if (t < G) {
         const int* mine = pf.f[rank] + t;
-        for (long long spin = 0;; ++spin) {
+        unsigned long long t0, now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        for (;;) {
             int v;
             asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(mine) : "memory");
             if (v - epoch >= 0) break;  // epochs increase by one per call (wrap-safe compare)
             __nanosleep(128);
-            if (spin > (1ll << 26)) __trap();
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            // a peer that never arrives is a bug (a crashed rank): fail loudly after the timeout
+            // (NM_PEER_TIMEOUT_MS, default 120 s, wall time) instead of hanging the stream forever
+            if (now - t0 > timeout_ns) __trap();
         }
     }
 }
@@ -112,7 +118,10 @@ nm_status nm_peer_barrier(void* const* flag_peers, int G, int rank, int epoch, v
     }
     nm_status st = require_device();
     if (st) return st;
-    peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(pf, G, rank, epoch);
+    const char* te = std::getenv("NM_PEER_TIMEOUT_MS");
+    const long long ms = te ? std::atoll(te) : 120000;
+    const unsigned long long timeout_ns = static_cast<unsigned long long>(ms > 0 ? ms : 120000) * 1000000ull;
+    peer_barrier_kernel<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(pf, G, rank, epoch, timeout_ns);
     note_launch();
     NM_LAUNCH_CHECK("peer_barrier_kernel");
     return NM_OK;
@@ -126,6 +135,9 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
     if (G < 1 || G > 8) return fail(NM_ERR_SHAPE, "nm_spmm_peers: 1 <= G <= 8");
     if (col_off < 0 || n_valid < 0 || n_valid > nr || col_off + n_valid > ldc)
         return fail(NM_ERR_SHAPE, "nm_spmm_peers: columns [col_off, col_off + n_valid) outside ldc, or n_valid > nr");
+    // the SIMT peer epilogue stores float4s guarded by col < n_valid: a ragged n_valid would write
+    // up to 3 columns of another rank's range
+    if (n_valid % 4) return fail(NM_ERR_SHAPE, "nm_spmm_peers: n_valid must be a multiple of 4");
     if (m == 0 || nr == 0 || n_valid == 0) return NM_OK;
     if (!A || !C_peers || (k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_spmm_peers: NULL pointer");
     PeerOut po{};
@@ -154,9 +166,13 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
 nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* const* C_peers, int G, int64_t ldc,
                                   int64_t col_off, int64_t n_valid, int64_t m, nm_dtype c_dt, void* stream) {
     if (!w || w->magic != 0x4B504D4E) return fail(NM_ERR_NULL, "nm_spmm_prepacked_peers: descriptor not filled by nm_prepack");
-    if (w->kind == 0)  // fp32 weights: the SIMT kernel's peer epilogue
+    if (w->kind == 0) {  // fp32 weights: the SIMT kernel's peer epilogue (fp32 A, B' and C only)
+        if (w->dtype != NM_F32 || c_dt != NM_F32)
+            return fail(NM_ERR_UNSUPPORTED, "nm_spmm_prepacked_peers: a weight without slot images (prepack kind 0) "
+                                            "takes the fp32 SIMT peer path, which needs fp32 values and an fp32 C");
         return nm_spmm_peers(A, w->values, w->idx, C_peers, G, ldc, col_off, n_valid, m, w->n, w->k, w->N, w->M, w->L,
                              stream);
+    }
     if (w->kind != 2 && w->kind != 3)
         return fail(NM_ERR_UNSUPPORTED, "nm_spmm_prepacked_peers: prepack kind 0, 2 or 3 (slot kernels) only");
     if (G < 1 || G > 8) return fail(NM_ERR_SHAPE, "nm_spmm_prepacked_peers: 1 <= G <= 8");
@@ -164,6 +180,9 @@ nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* co
         return fail(NM_ERR_SHAPE, "nm_spmm_prepacked_peers: columns [col_off, col_off + n_valid) outside ldc");
     const bool tf = w->kind == 3;
     if (tf && c_dt != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
+    // the direct-store epilogue writes bf16 C as column pairs guarded by pair < n_valid
+    if (c_dt == NM_BF16 && (n_valid % 2))
+        return fail(NM_ERR_SHAPE, "nm_spmm_prepacked_peers: bf16 C needs an even n_valid");
     if (m == 0 || w->n == 0 || n_valid == 0) return NM_OK;
     if (!A || !C_peers) return fail(NM_ERR_NULL, "nm_spmm_prepacked_peers: NULL pointer");
     PeerOut po{};
@@ -183,7 +202,7 @@ nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* co
                                         "k % 8 == 0");
     nm_status st = require_device();
     if (st) return st;
-    return tc_sp_run(A, w->bperm, po.c[0], c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, tf,
+    return tc_sp_run(A, w->bperm, w->bn / 128, po.c[0], c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, tf,
                      static_cast<cudaStream_t>(stream), &po, 1.f);
 }
 

@@ -425,14 +425,14 @@ static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, con
                              cudaStream_t s) {
     using namespace simt;
     const int smem = PK ? SMEM_BYTES_PACKED : SMEM_BYTES;
-    static bool attr_done = false;
-    if (!attr_done) {
+    static std::atomic<uint64_t> attr_mask{0};
+    if (!attr_once(attr_mask)) {
         NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          smem));
         if (!PK)
             NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT, false, true>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_done = true;
+        attr_done(attr_mask);
     }
     prof_begin(s);
     if (!PK && p.npeer)

@@ -177,12 +177,9 @@ __global__ void build_simt_table_kernel(const uint8_t* __restrict__ D, uint16_t*
 template <int SL, bool TWO>
 static nm_status launch_pipe(const CUtensorMap& tmA, const CUtensorMap& tmB, const simt3::Params& p, dim3 grid, int smem,
                              cudaStream_t s) {
-    static int attr_smem = 0;
-    if (attr_smem < smem) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(simt3::spmm_simt_pipe_kernel<SL, TWO>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_smem = smem;
-    }
+    // set per call (an ablation-only path; the attribute is per device and smem varies per shape)
+    NM_CUDA_TRY(cudaFuncSetAttribute(simt3::spmm_simt_pipe_kernel<SL, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
     prof_begin(s);
     simt3::spmm_simt_pipe_kernel<SL, TWO><<<grid, simt3::THREADS, smem, s>>>(tmA, tmB, p);
     prof_end(s);

@@ -23,8 +23,11 @@
 // weight multicast over 2-CTA clusters (NM_SP_MC=1).
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "tcgen05.cuh"
 
@@ -65,6 +68,11 @@ constexpr int WH_BYTES = A_BYTES + E_BYTES;
 // Weight image of one (column tile, stage): [A_0 .. A_{H-1} | E_0 .. E_{H-1}]; the E blocks are
 // present (and copied) only for even stages and carry the metadata of the stage pair, so an odd
 // stage moves H x A_BYTES and the metadata costs 1 KB per half and stage instead of 2.
+// Byte offset of stage st inside a tile's compact image block: even stages carry the pair's
+// metadata (H x (A + E)), odd stages only the A images (H x A).
+__host__ __device__ constexpr int64_t sp_stage_off(int st, int H) {
+    return static_cast<int64_t>(st >> 1) * H * (2 * A_BYTES + E_BYTES) + static_cast<int64_t>(st & 1) * H * (A_BYTES + E_BYTES);
+}
 constexpr int GATHER_WARPS = 8;            // also the epilogue warps (TMEM lane quarter = warp % 4)
 constexpr int MMA_WARP = GATHER_WARPS;
 constexpr int THREADS = (GATHER_WARPS + 1) * 32;
@@ -122,16 +130,20 @@ static int sp_halves(int L, int N, int M) {
 }
 
 struct Params {
-    const uint8_t* wimg;   // [ntiles][max_stages][H x A_BYTES | H x E_BYTES (even stages)]
-    const int* slots;      // [ntiles][smax] row of A^T per slot (k = padding, TMA zero fill)
-    const int* nstages;    // [ntiles]
+    // compact prepacked weight (tc_sp_prepack): tinfo[tile] = {stages, first slot, image offset / 1 KB,
+    // image bytes / 1 KB}; slots (row of A^T per slot, k = padding: the zero row) at base + slots_off;
+    // a tile's stage images at base + 1 KB x tinfo.z, stage st at sp_stage_off(st, H)
+    const uint8_t* base;
+    const int4* tinfo;
+    int64_t slots_off;
     void* C;
-    int m, n, k, mp, smax, max_stages, c_bf16;
+    int m, n, k, mp, c_bf16;
     int tma_c;  // 1: C tile staged in shared memory and written by TMA stores (tmC valid)
     int n_tok;       // token tiles (1-D grid: token tile fastest)
-    int full_ctas;   // CTAs [0, full_ctas) do one whole tile; the rest split the tail tiles in two
-    float* ws;       // tail split: fp32 partial of part 1 per tail tile, [tail][NT][MC]
-    int* flags;      // tail split: flags[tail] = 1 once part 1's partial is in ws (zeroed per launch)
+    int full_ctas;   // CTAs [0, full_ctas) do one whole tile; the rest split each remaining tile into
+    int split;       // `split` stage ranges (pair-aligned)
+    float* ws;       // split tiles: fp32 partials [tile - full tiles][part][NT][MC] (token-major)
+    int* counters;   // split tiles: [2 x (tile - full tiles)] = {tickets, partials published} (zeroed per launch)
     int dbg;  // NM_SP_DBG (timing studies only): 1 skip gathers, 2 skip MMAs, 8 skip C stores, 16 skip weights,
               // 64 per-stage clock64 trace, 128 plain arrive for commits (no MMA), 256 per-CTA timeline
     // fused column all-gather (nm_spmm_prepacked_peers): the direct-store epilogue writes every C
@@ -207,8 +219,8 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void st_release(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+    asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
@@ -272,16 +284,20 @@ __global__ void __launch_bounds__(THREADS, 1)
     // together, so it is read from DRAM once and served from L2 to the others).  The last,
     // partial wave's tiles are split in two stage ranges ("tail split"): part 1 leaves an fp32
     // partial in ws, part 0 adds it in its epilogue (a + b: order-independent, deterministic).
-    int tid_lin = blockIdx.x, part = -1;
+    int tid_lin = blockIdx.x, part = 0, nparts = 1;
     if (tid_lin >= p.full_ctas) {
-        part = (tid_lin - p.full_ctas) & 1;
-        tid_lin = p.full_ctas + ((tid_lin - p.full_ctas) >> 1);
+        nparts = p.split;
+        part = (tid_lin - p.full_ctas) % nparts;
+        tid_lin = p.full_ctas + (tid_lin - p.full_ctas) / nparts;
     }
     const int tile = tid_lin / p.n_tok;
     const int m0 = (tid_lin % p.n_tok) * NT;
-    const int nst_all = p.nstages[tile];
-    const int smid = min(nst_all, ((nst_all + 3) >> 2) << 1);  // even: a stage pair's metadata stays in one part
-    const int sa = part == 1 ? smid : 0, sb = part == 0 ? smid : nst_all;
+    const int4 ti = p.tinfo[tile];
+    const int nst_all = ti.x;
+    // pair-aligned stage ranges (a stage pair's metadata stays in one part)
+    const int npairs = (nst_all + 1) >> 1;
+    const int sa = min(nst_all, 2 * (part * npairs / nparts));
+    const int sb = min(nst_all, 2 * ((part + 1) * npairs / nparts));
     const int nst = sb - sa;  // stages this CTA runs (ring index = st - sa)
     const int tail_idx = tid_lin - p.full_ctas;
 
@@ -309,8 +325,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         // lane l copies tokens [8l, 8l+8) of the row: token atom l/8, 16-B chunk l%8 of the
         // 128-B swizzled row (chunk ^= row % 8).  Warp wg owns RPW consecutive rows of a stage.
         // Completion: cp.async.mbarrier.arrive.noinc per thread (no wait in the loop).
-        const uint8_t* wsrc = p.wimg + static_cast<int64_t>(tile) * p.max_stages * W_BYTES;
-        const int* ssrc = p.slots + static_cast<int64_t>(tile) * p.smax + warp * RPW + (lane % RPW);
+        const uint8_t* wsrc = p.base + static_cast<int64_t>(ti.z) * 1024;
+        const int* ssrc = reinterpret_cast<const int*>(p.base + p.slots_off) + ti.y + warp * RPW + (lane % RPW);
         // per-lane constants: source = A^T row base + E (m0 + token) bytes (row k of A^T is a zero
         // row, the padding slots' source); destination = stage + this lane's (atom, swizzled chunk)
         // of each of the warp's rows.  Eight 512-B copies per warp and stage:
@@ -350,6 +366,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         // register is reloaded only after PF iterations, so the load latency (~1-2k clk under load)
         // is not paid per stage -- at PF = 4 it was, and it paced the whole pipeline
         constexpr int PF = 16;
+
         int kq[PF];
 #pragma unroll
         for (int u = 0; u < PF; ++u) kq[u] = u < nst ? ssrc[(sa + u) * SLOTS] : 0;
@@ -371,12 +388,12 @@ __global__ void __launch_bounds__(THREADS, 1)
                         // even stages bring the pair's metadata blocks, odd ones only the A images
                         const uint32_t wb = ((sa + st) & 1) ? static_cast<uint32_t>(H * A_BYTES) : W_BYTES;
                         mbar_arrive_expect_tx(&full[s], wb);
+                        const uint8_t* wst = wsrc + sp_stage_off(sa + st, H);
                         if (MCAST)  // both halves land in both CTAs: copy (and multicast) ours
-                            bulk_load_mc(sW + s * W_BYTES + crank * (wb / 2),
-                                         wsrc + static_cast<int64_t>(sa + st) * W_BYTES + crank * (wb / 2), wb / 2,
-                                         &full[s], 0x3);
+                            bulk_load_mc(sW + s * W_BYTES + crank * (wb / 2), wst + crank * (wb / 2), wb / 2, &full[s],
+                                         0x3);
                         else
-                            bulk_load(sW + s * W_BYTES, wsrc + static_cast<int64_t>(sa + st) * W_BYTES, wb, &full[s]);
+                            bulk_load(sW + s * W_BYTES, wst, wb, &full[s]);
                     }
                 }
                 if (!(p.dbg & 1)) {
@@ -395,42 +412,49 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
     } else if (warp == MMA_WARP) {
         // ============ MMA issuer: per stage and half, metadata -> TMEM and two sparse MMAs ============
-        constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (EL::FMT << 7) | (EL::FMT << 10) | (1u << 16) |
-                                   (static_cast<uint32_t>(NT >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
-        for (int st = 0; st < nst; ++st) {
-            const int s = st % STAGES;
-            SP_TS(st, 3);
-            mbar_wait(&full[s], (st / STAGES) & 1);
-            SP_TS(st, 4);
-            tc_fence_after();
-            if (elect_one() && !(p.dbg & 2)) {
-                const uint32_t ba = smem_u32(sB + s * B_BYTES);
+        // The warp runs the loop converged (all values warp-uniform); one elect per stage issues the
+        // metadata copies, MMAs and the commit.  Descriptors of ring slot 0 are built once and
+        // advanced by immediate offsets (the 14-bit start-address field never carries: shared
+        // memory < 256 KB); ring slot / phase / metadata pair are kept incrementally.
+        {
+            constexpr uint32_t idesc = (1u << 2) | (1u << 4) | (EL::FMT << 7) | (EL::FMT << 10) | (1u << 16) |
+                                       (static_cast<uint32_t>(NT >> 3) << 17) | (static_cast<uint32_t>(128 >> 4) << 24);
+            const uint64_t bdesc0 = smem_desc(smem_u32(sB), SLOTS * 128, EL::B_SBO, EL::B_LAYOUT);
+            const uint64_t adesc0 = smem_desc(smem_u32(sW), 16, 512, 4);
+            const uint64_t edesc0 = smem_desc(smem_u32(sW) + H * A_BYTES, 2048, 128, 0);
+            const bool skip_mma = (p.dbg & 2) != 0;
+            int s = 0, pi = (sa >> 1) % CF::NPAIR;
+            uint32_t ph = 0;
+            for (int st = 0; st < nst; ++st) {
                 const int gs = sa + st;  // stage index in the tile (pairs: 2i, 2i+1)
-                const uint32_t pcol = tmem + CF::META_COL + 4 * H * ((gs >> 1) % CF::NPAIR);
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                if (elect_one()) {
+                    if (!skip_mma) {
+                        const uint64_t bo = static_cast<uint64_t>(s * (B_BYTES >> 4));
+                        const uint64_t wo = static_cast<uint64_t>(s * (W_BYTES >> 4));
+                        const uint32_t pcol = tmem + CF::META_COL + 4 * H * pi;
 #pragma unroll
-                for (int h = 0; h < H; ++h) {
-                    const uint32_t wa = smem_u32(sW + s * W_BYTES + h * A_BYTES);
-                    const uint32_t ecol = pcol + 4 * h;
-                    if (!(gs & 1))  // the pair's metadata arrives with its even stage (sa is even)
-                        tmem_cp_128x128b(ecol, smem_desc(smem_u32(sW + s * W_BYTES) + H * A_BYTES + h * E_BYTES, 2048,
-                                                         128, 0));
+                        for (int h = 0; h < H; ++h) {
+                            if (!(gs & 1))  // the pair's metadata arrives with its even stage (sa is even)
+                                tmem_cp_128x128b(pcol + 4 * h, edesc0 + wo + (h * E_BYTES >> 4));
 #pragma unroll
-                    for (int j = 0; j < 2; ++j)
-                        mma_sp<TF>(tmem + h * NT, smem_desc(wa + 32 * j, 16, 512, 4),
-                                   smem_desc(ba + EL::B_STEP * j, SLOTS * 128, EL::B_SBO, EL::B_LAYOUT),
-                                   idesc | static_cast<uint32_t>(j), (st | j) ? 1u : 0u, ecol + 2 * (gs & 1));
+                            for (int j = 0; j < 2; ++j)
+                                mma_sp<TF>(tmem + h * NT, adesc0 + wo + ((h * A_BYTES + 32 * j) >> 4),
+                                           bdesc0 + bo + ((EL::B_STEP * j) >> 4), idesc | static_cast<uint32_t>(j),
+                                           (st | j) ? 1u : 0u, pcol + 4 * h + 2 * (gs & 1));
+                        }
+                    }
+                    if (p.dbg & 128) mbar_arrive(&empty[s]);       // timing study: plain arrive instead of commit
+                    else if (MCAST) tc_commit_mc(&empty[s], 0x3);  // the stage is free once both CTAs are done
+                    else tc_commit(&empty[s]);
                 }
+                if (gs & 1) pi = pi + 1 == CF::NPAIR ? 0 : pi + 1;
+                if (++s == STAGES) s = 0, ph ^= 1u;
             }
-            if (elect_one()) {
-                if (p.dbg & 128) mbar_arrive(&empty[s]);  // timing study: plain arrive instead of commit
-                else if (MCAST) tc_commit_mc(&empty[s], 0x3);  // the stage is free once both CTAs are done
-                else tc_commit(&empty[s]);
-            }
+            if (elect_one()) tc_commit(acc_full);
             __syncwarp();
-            SP_TS(st, 5);
         }
-        if (elect_one()) tc_commit(acc_full);
-        __syncwarp();
     }
 
     if (warp < GATHER_WARPS) {
@@ -441,9 +465,21 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         if (warp == 0) SP_TS(nst, 7);
         const int qw = warp & 3;
-        if (part == 1) {
-            // tail split, part 1: fp32 partial to ws[tail_idx] ([MC][NT], lane = column), then flag
-            float* w = p.ws + static_cast<int64_t>(tail_idx) * MC * NT;
+        // split tiles (nparts > 1): the first nparts - 1 CTAs of a tile to finish publish their fp32
+        // partials in ws; the last one (by ticket) waits for them -- they hold tickets, so they are
+        // running: no co-residency assumption -- and adds all parts in the fixed order 0 .. nparts-1
+        // (bit-reproducible whichever CTA is last), then stores C
+        bool publish = false;
+        if (nparts > 1) {
+            volatile uint32_t* s_flag = tmem_slot + 1;
+            if (warp == 0 && lane == 0) *s_flag = atomicAdd(p.counters + 2 * tail_idx, 1) < nparts - 1 ? 1u : 0u;
+            named_bar_sync(1, 32 * GATHER_WARPS);
+            publish = *s_flag != 0;
+        }
+        if (publish) {
+            // ws[tile][part] is [NT][MC] (token-major): for each token the warp's 32 lanes write 128
+            // contiguous bytes
+            float* w = p.ws + (static_cast<int64_t>(tail_idx) * nparts + part) * MC * NT;
 #pragma unroll 1
             for (int h = 0; h < H; ++h)
 #pragma unroll 1
@@ -456,8 +492,6 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = 0u;
                     }
-                    // ws is [NT][MC] (token-major): for each token the warp's 32 lanes write 128
-                    // contiguous bytes (a column-major layout scattered every store over 32 rows)
                     const int nv = NT - t0 < 32 ? NT - t0 : 32;
                     float* dst = w + static_cast<int64_t>(t0) * MC + h * 128 + qw * 32 + lane;
 #pragma unroll
@@ -466,19 +500,22 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             __threadfence();
             named_bar_sync(1, 32 * GATHER_WARPS);
-            if (warp == 0 && lane == 0) st_release(p.flags + tail_idx, 1);
+            if (warp == 0 && lane == 0) red_release_add(p.counters + 2 * tail_idx + 1, 1);
         } else if (p.tma_c) {
-            if (part == 0) {  // tail split, part 0: part 1's partial must be in ws before it is added
-                if (warp == 0 && lane == 0)  // one poller with back-off (256 spinning threads per CTA
-                                             // measured 50 % slower: they load the L2 the others need)
-                    for (long long spin = 0; ld_acquire(p.flags + tail_idx) == 0; ++spin) {
+            if (nparts > 1) {
+                if (warp == 0 && lane == 0) {  // one poller with back-off
+                    unsigned long long t0g, tn;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0g));
+                    while (ld_acquire(p.counters + 2 * tail_idx + 1) < nparts - 1) {
                         __nanosleep(256);
-                        if (spin > (1ll << 24)) __trap();  // a missing partial is a bug: fail, do not hang
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tn));
+                        if (tn - t0g > 20000000000ull) __trap();  // 20 s: a lost partial is a bug, fail loudly
                     }
+                }
                 named_bar_sync(1, 32 * GATHER_WARPS);
                 __threadfence();
             }
-            const float* wpart = part == 0 ? p.ws + static_cast<int64_t>(tail_idx) * MC * NT : nullptr;
+            const float* wpart = nparts > 1 ? p.ws + static_cast<int64_t>(tail_idx) * nparts * MC * NT : nullptr;
             // staged: each 32-token chunk of the [NT][MC] C tile is assembled in the (now idle)
             // stage ring, then one TMA tensor store writes it (clipped at m, n).  Warps 0-3 take
             // the even chunks, 4-7 the odd ones; lane = column, so a warp's 32 stores per token row
@@ -499,12 +536,26 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                         for (int i = 0; i < 32; ++i) v[i] = 0u;
                     }
-                    if (wpart) {
-                        const float* src = wpart + static_cast<int64_t>(t0) * MC + h * 128 + qw * 32 + lane;
+                    if (wpart) {  // sum of the parts in the order 0 .. nparts-1 (this CTA's own from TMEM)
                         const int nv = NT - t0 < 32 ? NT - t0 : 32;
+                        float a[32];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i < nv) v[i] = __float_as_uint(__uint_as_float(v[i]) + src[static_cast<int64_t>(i) * MC]);
+                        for (int i = 0; i < 32; ++i) a[i] = 0.f;
+#pragma unroll 1
+                        for (int q2 = 0; q2 < nparts; ++q2) {
+                            if (q2 == part) {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) a[i] += __uint_as_float(v[i]);
+                            } else {
+                                const float* src = wpart + static_cast<int64_t>(q2) * MC * NT + static_cast<int64_t>(t0) * MC +
+                                                   h * 128 + qw * 32 + lane;
+#pragma unroll
+                                for (int i = 0; i < 32; ++i)
+                                    if (i < nv) a[i] += __ldcg(src + static_cast<int64_t>(i) * MC);
+                            }
+                        }
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(a[i]);
                     }
 #pragma unroll
                     for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.alpha);
@@ -938,8 +989,8 @@ __device__ __forceinline__ void sp_store_val(uint8_t* p, float v, bool tf) {
 template <bool TF>
 __global__ void sp_image_kernel(const void* __restrict__ Bv_, const uint8_t* __restrict__ D,
                                 const int* __restrict__ slots, const uint8_t* __restrict__ stype,
-                                const int* __restrict__ nstages, uint8_t* __restrict__ wimg, int n, int k, int N, int M,
-                                int L, int smax, int max_stages, int H) {
+                                const int* __restrict__ nstages, const int4* __restrict__ tinfo, uint8_t* __restrict__ base,
+                                int n, int k, int N, int M, int L, int smax, int max_stages, int H) {
     const int64_t gid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     const int MC = 128 * H;
     const int r = static_cast<int>(gid % MC);
@@ -953,10 +1004,10 @@ __global__ void sp_image_kernel(const void* __restrict__ Bv_, const uint8_t* __r
     const int g = j / L, gi = r / L;
     const bool live = j < n;
     const int hf = r / 128;
-    uint8_t* img = wimg + (static_cast<int64_t>(tile) * max_stages + st) * H * WH_BYTES + hf * A_BYTES;
+    uint8_t* timg = base + static_cast<int64_t>(tinfo[tile].z) * 1024;  // the tile's compact image block
+    uint8_t* img = timg + sp_stage_off(st, H) + hf * A_BYTES;
     // metadata of the pair (st & ~1, st | 1) lives in the even stage's E block of this half
-    uint32_t* meta = reinterpret_cast<uint32_t*>(wimg + (static_cast<int64_t>(tile) * max_stages + (st & ~1)) * H * WH_BYTES +
-                                                 H * A_BYTES + hf * E_BYTES);
+    uint32_t* meta = reinterpret_cast<uint32_t*>(timg + sp_stage_off(st & ~1, H) + H * A_BYTES + hf * E_BYTES);
     constexpr int SLOTS = El<TF>::SLOTS, PG = El<TF>::PG, NV = PG / 2, E = El<TF>::E;
     const int* sl = slots + static_cast<int64_t>(tile) * smax + st * SLOTS;
     const uint8_t* ty = stype + static_cast<int64_t>(tile) * smax + st * SLOTS;
@@ -1002,6 +1053,37 @@ __global__ void sp_image_kernel(const void* __restrict__ Bv_, const uint8_t* __r
     }
 }
 
+// Compact layout of the prepacked weight (one thread): per tile its stage count, first slot,
+// image block offset and size (1 KB units, images start 1 KB-aligned after the slot lists), and the
+// exact buffer size in the header.  Tiles are few (n / 128H), so one thread suffices.
+__global__ void sp_layout_kernel(const int* __restrict__ nstages, int4* __restrict__ tinfo, int64_t* __restrict__ header,
+                                 int ntiles, int H, int SLOTS, int64_t slots_off) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    int64_t nslots = 0;
+    for (int t = 0; t < ntiles; ++t) nslots += static_cast<int64_t>(nstages[t]) * SLOTS;
+    int64_t img_kb = (slots_off + nslots * 4 + 1023) / 1024;
+    int64_t sl = 0;
+    for (int t = 0; t < ntiles; ++t) {
+        const int nst = nstages[t];
+        const int64_t kb = sp_stage_off(nst, H) / 1024;
+        tinfo[t] = make_int4(nst, static_cast<int>(sl), static_cast<int>(img_kb), static_cast<int>(kb));
+        sl += static_cast<int64_t>(nst) * SLOTS;
+        img_kb += kb;
+    }
+    header[0] = img_kb * 1024;  // exact bytes of the prepacked buffer
+    header[1] = ntiles;
+    header[2] = H;
+}
+
+// A tile's slot list (scratch, smax per tile) -> its compact position (one block per tile).
+__global__ void sp_slots_copy_kernel(const int* __restrict__ slots, const int4* __restrict__ tinfo, int* __restrict__ out,
+                                     int smax, int SLOTS) {
+    const int tile = blockIdx.x;
+    const int4 ti = tinfo[tile];
+    const int cnt = ti.x * SLOTS;
+    for (int i = threadIdx.x; i < cnt; i += blockDim.x) out[ti.y + i] = slots[static_cast<int64_t>(tile) * smax + i];
+}
+
 }  // namespace tcs
 
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
@@ -1010,95 +1092,150 @@ bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     return (L == 16 || L == 32 || L == 64 || L == 128) && n % 2 == 0 && k > 0 && k < (1 << 30) && M <= 256;
 }
 
-void tc_sp_sizes(int64_t n, int64_t k, int N, int M, int L, bool tf, size_t* off_slots, size_t* off_stype,
-                 size_t* off_nst, size_t* off_q, size_t* off_img, size_t* total, int* smax, int* max_stages) {
+// Geometry of a prepacked weight (H column halves per tile, SLOTS slots per stage).
+struct SpGeom {
+    int H, SLOTS, PG, ntiles, KC, nchunks;
+    int64_t smax, max_stages, slots_off;
+};
+static SpGeom sp_geom(int64_t n, int64_t k, int N, int M, int L, bool tf, int H) {
     using namespace tcs;
-    const int H = sp_halves(L, N, M);
-    const int SLOTS = tf ? El<true>::SLOTS : El<false>::SLOTS;
-    const int64_t ntiles = (n + 128 * H - 1) / (128 * H);
-    const int64_t KC = sp_chunk_rows(M), nchunks = (k + KC - 1) / KC;
-    const int64_t sm = ((2 * k + 4 * nchunks) + SLOTS - 1) / SLOTS * SLOTS;  // >= sum of chunk bounds
-    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    size_t o = 0;
-    *off_slots = o;
-    o += al(static_cast<size_t>(ntiles * sm) * 4);
-    *off_stype = o;
-    o += al(static_cast<size_t>(ntiles * sm));
-    *off_nst = o;
-    o += al(static_cast<size_t>(ntiles) * 4);
-    *off_q = o;  // pack scratch: bucketed rows, chunk slot lists + types, chunk counts
-    const int64_t units = ntiles * nchunks;
-    o += al(static_cast<size_t>(units * KC) * 4) + al(static_cast<size_t>(units * (2 * KC + 4)) * 5) +
-         al(static_cast<size_t>(units) * 4);
-    *off_img = o;
-    o += static_cast<size_t>(ntiles * (sm / SLOTS) * H) * WH_BYTES;
-    *total = o;
-    *smax = static_cast<int>(sm);
-    *max_stages = static_cast<int>(sm / SLOTS);
+    SpGeom g{};
+    g.H = H > 0 ? H : sp_halves(L, N, M);
+    g.SLOTS = tf ? El<true>::SLOTS : El<false>::SLOTS;
+    g.PG = tf ? El<true>::PG : El<false>::PG;
+    g.ntiles = static_cast<int>((n + 128 * g.H - 1) / (128 * g.H));
+    g.KC = sp_chunk_rows(M);
+    g.nchunks = static_cast<int>((k + g.KC - 1) / g.KC);
+    g.smax = ((2 * k + 4 * g.nchunks) + g.SLOTS - 1) / g.SLOTS * g.SLOTS;  // >= sum of chunk bounds
+    g.max_stages = g.smax / g.SLOTS;
+    g.slots_off = (256 + 16 * static_cast<int64_t>(g.ntiles) + 255) / 256 * 256;
+    return g;
+}
+static size_t al256(size_t b) { return (b + 255) / 256 * 256; }
+
+// Retained prepacked buffer: [header 256 B: exact bytes, ntiles, H | tinfo ntiles x int4 | slots |
+// images (1 KB-aligned)].  The exact size depends on the slot counts (data); this is the bound.
+size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf) {
+    const SpGeom g = sp_geom(n, k, N, M, L, tf, 0);
+    return static_cast<size_t>(g.slots_off + (g.ntiles * g.smax * 4 + 1023) / 1024 * 1024 +
+                               g.ntiles * tcs::sp_stage_off(static_cast<int>(g.max_stages), g.H));
 }
 
-nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, void* buf,
-                        cudaStream_t s) {
+// Pack scratch (library pool, released after the prepack): chunk buckets, chunk slot lists and
+// types, chunk counts, per-tile slot lists / types / stage counts, tinfo, header.
+static size_t sp_scratch_bytes(const SpGeom& g) {
+    const int64_t units = static_cast<int64_t>(g.ntiles) * g.nchunks;
+    return al256(units * g.KC * 4) + al256(units * (2 * g.KC + 4) * 5) + al256(units * 4) +
+           al256(g.ntiles * g.smax * 4) + al256(g.ntiles * g.smax) + al256(g.ntiles * 4) + al256(g.ntiles * 16) + 256;
+}
+
+// Zero the metadata blocks (the image kernel ORs nibbles into them): one block per (tile, pair).
+__global__ void sp_meta_zero_kernel(const int4* __restrict__ tinfo, uint8_t* __restrict__ base, int H, int max_pairs) {
     using namespace tcs;
-    size_t os, ot, on, oq, oi, tot;
-    int smax, mst;
-    tc_sp_sizes(n, k, N, M, L, tf, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
-    uint8_t* b = static_cast<uint8_t*>(buf);
-    const int mc = 128 * sp_halves(L, N, M);
-    const int ntiles = static_cast<int>((n + mc - 1) / mc);
-    NM_CUDA_TRY(cudaMemsetAsync(b, 0, tot, s));  // slot lists past nstages and the images start zeroed
-    const int KC = sp_chunk_rows(M), nchunks = static_cast<int>((k + KC - 1) / KC);
-    const int64_t units = static_cast<int64_t>(ntiles) * nchunks;
-    auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-    int* qk = reinterpret_cast<int*>(b + oq);
-    uint8_t* tsl = b + oq + al(static_cast<size_t>(units * KC) * 4);
-    uint8_t* tty = tsl + static_cast<size_t>(units * (2 * KC + 4)) * 4;
-    int* ccnt = reinterpret_cast<int*>(b + oq + al(static_cast<size_t>(units * KC) * 4) +
-                                       al(static_cast<size_t>(units * (2 * KC + 4)) * 5));
+    const int tile = blockIdx.x / max_pairs, pr = blockIdx.x % max_pairs;
+    const int4 ti = tinfo[tile];
+    if (2 * pr >= ti.x) return;
+    uint4* e = reinterpret_cast<uint4*>(base + static_cast<int64_t>(ti.z) * 1024 + sp_stage_off(2 * pr, H) + H * A_BYTES);
+    for (int i = threadIdx.x; i < H * E_BYTES / 16; i += blockDim.x) e[i] = make_uint4(0, 0, 0, 0);
+}
+
+// The paper's offline PreProcessing (Listing 3) for the slot kernels: slot packing of
+// every column tile's kept rows, then the compact weight images.  exact (host, may be null): the
+// exact buffer size, which synchronizes s; with query_only nothing is written to buf.
+nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, int H,
+                        void* buf, int64_t buf_bytes, int64_t* exact, bool query_only, cudaStream_t s) {
+    using namespace tcs;
+    const SpGeom g = sp_geom(n, k, N, M, L, tf, H);
+    const int64_t units = static_cast<int64_t>(g.ntiles) * g.nchunks;
+    void* scr = nullptr;
+    nm_status st = scratch_alloc(&scr, sp_scratch_bytes(g), s);
+    if (st) return st;
+    uint8_t* sb = static_cast<uint8_t*>(scr);
+    int* qk = reinterpret_cast<int*>(sb);
+    sb += al256(units * g.KC * 4);
+    int* tsl = reinterpret_cast<int*>(sb);
+    uint8_t* tty = sb + units * (2 * g.KC + 4) * 4;
+    sb += al256(units * (2 * g.KC + 4) * 5);
+    int* ccnt = reinterpret_cast<int*>(sb);
+    sb += al256(units * 4);
+    int* slots = reinterpret_cast<int*>(sb);
+    sb += al256(g.ntiles * g.smax * 4);
+    uint8_t* stype = sb;
+    sb += al256(g.ntiles * g.smax);
+    int* nst = reinterpret_cast<int*>(sb);
+    sb += al256(g.ntiles * 4);
+    int4* tinfo = reinterpret_cast<int4*>(sb);
+    sb += al256(g.ntiles * 16);
+    int64_t* header = reinterpret_cast<int64_t*>(sb);
+    cudaError_t e = cudaSuccess;
+    auto done = [&](nm_status r) {
+        cudaFreeAsync(scr, s);
+        return r;
+    };
     const char* seq = std::getenv("NM_SP_PACK_SEQ");
     if (seq && seq[0] == '1')
         sp_pack_kernel<<<static_cast<unsigned>(ceil_div(units, 32)), 32, 0, s>>>(
-            D, reinterpret_cast<int*>(tsl), tty, ccnt, qk, static_cast<int>(n), static_cast<int>(k), N, M, L,
-            sp_halves(L, N, M), nchunks, tf ? El<true>::PG : El<false>::PG);
+            D, tsl, tty, ccnt, qk, static_cast<int>(n), static_cast<int>(k), N, M, L, g.H, g.nchunks, g.PG);
     else
-        sp_pack_warp_kernel<<<static_cast<unsigned>(units), 32, 0, s>>>(
-            D, reinterpret_cast<int*>(tsl), tty, ccnt, static_cast<int>(n), static_cast<int>(k), N, M, L,
-            sp_halves(L, N, M), nchunks, tf ? El<true>::PG : El<false>::PG);
+        sp_pack_warp_kernel<<<static_cast<unsigned>(units), 32, 0, s>>>(D, tsl, tty, ccnt, static_cast<int>(n),
+                                                                      static_cast<int>(k), N, M, L, g.H, g.nchunks, g.PG);
     note_launch();
-    NM_LAUNCH_CHECK("sp_pack_kernel");
-    sp_compact_kernel<<<static_cast<unsigned>(ntiles), 256, 0, s>>>(reinterpret_cast<const int*>(tsl), tty, ccnt,
-                                                                   reinterpret_cast<int*>(b + os), b + ot,
-                                                                   reinterpret_cast<int*>(b + on),
-                                                                   static_cast<int>(k), M, nchunks, smax,
-                                                                   tf ? El<true>::SLOTS : El<false>::SLOTS);
+    if ((e = cudaGetLastError()) != cudaSuccess) return done(cuda_fail(e, "sp_pack_kernel"));
+    sp_compact_kernel<<<static_cast<unsigned>(g.ntiles), 256, 0, s>>>(tsl, tty, ccnt, slots, stype, nst,
+                                                                     static_cast<int>(k), M, g.nchunks,
+                                                                     static_cast<int>(g.smax), g.SLOTS);
     note_launch();
-    NM_LAUNCH_CHECK("sp_compact_kernel");
-    // the pack scratch is dead from here on: clear it so a prepacked buffer is a pure function of
-    // the weight (the tests compare the warp-parallel and the sequential packer byte for byte)
-    NM_CUDA_TRY(cudaMemsetAsync(b + oq, 0, oi - oq, s));
-    const int64_t threads = static_cast<int64_t>(ntiles) * mst * mc;
+    sp_layout_kernel<<<1, 32, 0, s>>>(nst, tinfo, header, g.ntiles, g.H, g.SLOTS, g.slots_off);
+    note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return done(cuda_fail(e, "sp_layout_kernel"));
+    int64_t need = -1;
+    if (exact || query_only) {
+        if ((e = cudaMemcpyAsync(&need, header, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(s)) != cudaSuccess)
+            return done(cuda_fail(e, "nm_prepack size"));
+        if (exact) *exact = need;
+        if (query_only) return done(NM_OK);
+        if (buf_bytes < need) return done(fail(NM_ERR_NULL, "nm_prepack: buffer smaller than the prepacked weight (" +
+                                                                std::to_string(need) + " bytes, nm_prepack_size)"));
+    }
+    uint8_t* b = static_cast<uint8_t*>(buf);
+    // header + tinfo, then the slot region zeroed (so alignment gaps are deterministic) and filled
+    const int64_t zero_to = std::min<int64_t>(buf_bytes, g.slots_off + g.ntiles * g.smax * 4);
+    if ((e = cudaMemsetAsync(b, 0, static_cast<size_t>(zero_to), s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(b, header, 24, cudaMemcpyDeviceToDevice, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(b + 256, tinfo, static_cast<size_t>(g.ntiles) * 16, cudaMemcpyDeviceToDevice, s)) !=
+            cudaSuccess)
+        return done(cuda_fail(e, "nm_prepack layout"));
+    sp_slots_copy_kernel<<<static_cast<unsigned>(g.ntiles), 256, 0, s>>>(slots, tinfo, reinterpret_cast<int*>(b + g.slots_off),
+                                                                        static_cast<int>(g.smax), g.SLOTS);
+    note_launch();
+    const int max_pairs = static_cast<int>((g.max_stages + 1) / 2);
+    sp_meta_zero_kernel<<<static_cast<unsigned>(static_cast<int64_t>(g.ntiles) * max_pairs), 128, 0, s>>>(tinfo, b, g.H,
+                                                                                                          max_pairs);
+    note_launch();
+    const int64_t threads = static_cast<int64_t>(g.ntiles) * g.max_stages * 128 * g.H;
     auto img = tf ? sp_image_kernel<true> : sp_image_kernel<false>;
     img<<<static_cast<unsigned>(ceil_div(threads, 128)), 128, 0, s>>>(
-        Bv, D, reinterpret_cast<const int*>(b + os), b + ot, reinterpret_cast<const int*>(b + on), b + oi,
-        static_cast<int>(n), static_cast<int>(k), N, M, L, smax, mst, sp_halves(L, N, M));
+        Bv, D, slots, stype, nst, tinfo, b, static_cast<int>(n), static_cast<int>(k), N, M, L, static_cast<int>(g.smax),
+        static_cast<int>(g.max_stages), g.H);
     note_launch();
-    NM_LAUNCH_CHECK("sp_image_kernel");
-    return NM_OK;
+    if ((e = cudaGetLastError()) != cudaSuccess) return done(cuda_fail(e, "sp_image_kernel"));
+    return done(NM_OK);
 }
 
 template <int H, int NT, bool TF>
-static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n, cudaStream_t s) {
+static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n, int est_stages, cudaStream_t s) {
     using namespace tcs;
     using CF = Cfg<H, NT, TF>;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr_mask{0};
+    if (!attr_once(attr_mask)) {
         NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false, TF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, true, TF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false, TF, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
-        attr = true;
+        attr_done(attr_mask);
     }
     // C through TMA stores when its rows are 16-B aligned (the staged tile, NT/32 chunks of
     // 32 x MC elements, must fit in the stage ring it reuses)
@@ -1127,19 +1264,38 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     if (mc) p.n_tok += p.n_tok & 1;
     const int64_t tiles = ceil_div(n, CF::MC) * p.n_tok;
     const int64_t sms = num_sms();
-    const int64_t tail = tiles % sms;
+    // Split stage ranges (pair-aligned) over several CTAs per tile, partials added in a fixed order:
+    //  * a grid below one wave (small problems, column shards of a multi-GPU layer): every tile in
+    //    S = sms / tiles parts (<= 8, >= 4 stage pairs per part, est_stages = the host's estimate);
+    //  * a partial last wave that at most half fills the SMs: its tiles in 2 parts ("tail split").
+    // NM_SP_SPLIT=S forces S for those tiles; NM_SP_TAIL=0 disables splitting.
     const char* te2 = std::getenv("NM_SP_TAIL");
-    const bool split = !mc && p.tma_c && !(te2 && te2[0] == '0') && tail > 0 && 2 * tail <= sms;
-    p.full_ctas = static_cast<int>(split ? tiles - tail : tiles);
-    p.ws = nullptr;
-    p.flags = nullptr;
-    if (split) {
-        nm_status st = scratch_alloc(reinterpret_cast<void**>(&p.ws), static_cast<size_t>(tail) * CF::MC * NT * 4, s);
-        if (!st) st = scratch_alloc(reinterpret_cast<void**>(&p.flags), static_cast<size_t>(tail) * 4, s);
-        if (st) return st;
-        NM_CUDA_TRY(cudaMemsetAsync(p.flags, 0, static_cast<size_t>(tail) * 4, s));
+    const char* se = std::getenv("NM_SP_SPLIT");
+    const bool can_split = !mc && p.tma_c && !(te2 && te2[0] == '0');
+    int64_t split_tiles = 0;
+    int S = 1;
+    if (can_split && tiles < sms) {
+        split_tiles = tiles;
+        S = static_cast<int>(std::min<int64_t>(8, sms / tiles));
+        S = std::max(1, std::min(S, est_stages / 8));
+    } else if (can_split && tiles % sms > 0 && 2 * (tiles % sms) <= sms) {
+        split_tiles = tiles % sms;
+        S = 2;
     }
-    const unsigned grid = static_cast<unsigned>(split ? tiles + tail : tiles);
+    if (se && split_tiles > 0) S = std::max(1, std::min(16, std::atoi(se)));
+    if (S <= 1) split_tiles = 0, S = 1;
+    p.full_ctas = static_cast<int>(tiles - split_tiles);
+    p.split = S;
+    p.ws = nullptr;
+    p.counters = nullptr;
+    if (split_tiles > 0) {
+        nm_status st = scratch_alloc(reinterpret_cast<void**>(&p.ws),
+                                     static_cast<size_t>(split_tiles) * S * CF::MC * NT * 4, s);
+        if (!st) st = scratch_alloc(reinterpret_cast<void**>(&p.counters), static_cast<size_t>(split_tiles) * 8, s);
+        if (st) return st;
+        NM_CUDA_TRY(cudaMemsetAsync(p.counters, 0, static_cast<size_t>(split_tiles) * 8, s));
+    }
+    const unsigned grid = static_cast<unsigned>(p.full_ctas + split_tiles * S);
     prof_begin(s);
     if (mc) {
         cudaLaunchConfig_t lc = {};
@@ -1164,44 +1320,53 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     note_launch();
     const cudaError_t e = cudaGetLastError();
     if (p.ws) cudaFreeAsync(p.ws, s);
-    if (p.flags) cudaFreeAsync(p.flags, s);
+    if (p.counters) cudaFreeAsync(p.counters, s);
     if (e != cudaSuccess) return cuda_fail(e, "spmm_tc_sp_kernel");
     return NM_OK;
 }
 
 template <bool TF>
-static nm_status sp_dispatch(int H, int nt, const void* at, const tcs::Params& p, int64_t m, int64_t n, cudaStream_t s) {
+static nm_status sp_dispatch(int H, int nt, const void* at, const tcs::Params& p, int64_t m, int64_t n, int est,
+                             cudaStream_t s) {
     switch (H * 1000 + nt) {
-        case 2192: return sp_launch_h<2, 192, TF>(at, p, m, n, s);
-        case 2128: return sp_launch_h<2, 128, TF>(at, p, m, n, s);
-        case 2160: return sp_launch_h<2, 160, TF>(at, p, m, n, s);
-        case 2224: return sp_launch_h<2, 224, TF>(at, p, m, n, s);
-        case 2176: return sp_launch_h<2, 176, TF>(at, p, m, n, s);
-        case 2208: return sp_launch_h<2, 208, TF>(at, p, m, n, s);
-        case 1256: return sp_launch_h<1, 256, TF>(at, p, m, n, s);
-        case 1128: return sp_launch_h<1, 128, TF>(at, p, m, n, s);
-        case 1192: return sp_launch_h<1, 192, TF>(at, p, m, n, s);
+        case 2192: return sp_launch_h<2, 192, TF>(at, p, m, n, est, s);
+        case 2128: return sp_launch_h<2, 128, TF>(at, p, m, n, est, s);
+        case 2160: return sp_launch_h<2, 160, TF>(at, p, m, n, est, s);
+        case 2224: return sp_launch_h<2, 224, TF>(at, p, m, n, est, s);
+        case 2176: return sp_launch_h<2, 176, TF>(at, p, m, n, est, s);
+        case 2208: return sp_launch_h<2, 208, TF>(at, p, m, n, est, s);
+        case 1256: return sp_launch_h<1, 256, TF>(at, p, m, n, est, s);
+        case 1128: return sp_launch_h<1, 128, TF>(at, p, m, n, est, s);
+        case 1192: return sp_launch_h<1, 192, TF>(at, p, m, n, est, s);
         default: return fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: unsupported (H, NT)");
     }
 }
 
-nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N, int M, int L,
-                    bool tf, cudaStream_t s, const PeerOut* po, float alpha) {
+// Stages per tile the selector expects (host, no data): the tile's kept-row union
+// k (1 - (1 - N/M)^G) over its G = 128 H / L groups, at least 2 w (two rows per quad / one per
+// pair), + 10 % packing slack.
+static int sp_est_stages(int64_t k, int N, int M, int L, int H, bool tf) {
+    const int G = 128 * H / L;
+    const double keep = static_cast<double>(N) / M;
+    const double uni = 1.0 - std::pow(1.0 - keep, G);
+    const double slots = 1.1 * static_cast<double>(k) * std::max(uni, std::min(1.0, 2.0 * keep));
+    return static_cast<int>(slots / (tf ? tcs::El<true>::SLOTS : tcs::El<false>::SLOTS)) + 1;
+}
+
+// One SpMM on a prepacked weight (buf from tc_sp_prepack with H column halves per tile).
+nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
+                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha) {
     using namespace tcs;
-    size_t os, ot, on, oq, oi, tot;
-    int smax, mst;
-    tc_sp_sizes(n, k, N, M, L, tf, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
+    const SpGeom g = sp_geom(n, k, N, M, L, tf, H);
     const uint8_t* b = static_cast<const uint8_t*>(buf);
     const int64_t mp = (m + 7) / 8 * 8;
     const int eb = tf ? 4 : 2;
     void* at = nullptr;
+    if (static_cast<uint64_t>(k + 1) * static_cast<uint64_t>(mp) * static_cast<uint64_t>(eb) >= (1ull << 32))
+        return fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: A^T larger than 4 GiB (32-bit row offsets)");
     // k + 1 rows: row k is zero, the source of the padding slots (kappa = k)
     nm_status st = scratch_alloc(&at, static_cast<size_t>((k + 1) * mp) * eb, s);
     if (st) return st;
-    if (static_cast<uint64_t>(k + 1) * static_cast<uint64_t>(mp) * static_cast<uint64_t>(eb) >= (1ull << 32)) {
-        cudaFreeAsync(at, s);
-        return fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: A^T larger than 4 GiB (32-bit row offsets)");
-    }
     const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(mp, 64)));
     cudaError_t e = cudaSuccess;
     if (tf) {
@@ -1221,16 +1386,14 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
     if (e != cudaSuccess) st = cuda_fail(e, "spmm_tc_sp transpose");
     if (!st) {
         Params p{};
-        p.wimg = b + oi;
-        p.slots = reinterpret_cast<const int*>(b + os);
-        p.nstages = reinterpret_cast<const int*>(b + on);
+        p.base = b;
+        p.tinfo = reinterpret_cast<const int4*>(b + 256);
+        p.slots_off = g.slots_off;
         p.C = C;
         p.m = static_cast<int>(m);
         p.n = static_cast<int>(n);
         p.k = static_cast<int>(k);
         p.mp = static_cast<int>(mp);
-        p.smax = smax;
-        p.max_stages = mst;
         p.c_bf16 = c_bf16 ? 1 : 0;
         const char* dbg = std::getenv("NM_SP_DBG");
         p.dbg = dbg ? std::atoi(dbg) : 0;
@@ -1242,9 +1405,9 @@ nm_status tc_sp_run(const void* A, const void* buf, void* C, bool c_bf16, int64_
             p.col_off = po->col_off;
             p.n_valid = static_cast<int>(po->n_valid);
         }
-
-        const int H = sp_halves(L, N, M), nt = sp_tokens(H, m, n);
-        st = tf ? sp_dispatch<true>(H, nt, at, p, m, n, s) : sp_dispatch<false>(H, nt, at, p, m, n, s);
+        const int nt = sp_tokens(g.H, m, n);
+        const int est = sp_est_stages(k, N, M, L, g.H, tf);
+        st = tf ? sp_dispatch<true>(g.H, nt, at, p, m, n, est, s) : sp_dispatch<false>(g.H, nt, at, p, m, n, est, s);
     }
     e = cudaFreeAsync(at, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
@@ -1256,21 +1419,19 @@ void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int*
     *tokens = tcs::sp_tokens(*halves, m, n);
 }
 
-size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf) {
-    size_t os, ot, on, oq, oi, tot;
-    int smax, mst;
-    tc_sp_sizes(n, k, N, M, L, tf, &os, &ot, &on, &oq, &oi, &tot, &smax, &mst);
-    return tot;
-}
+int tc_sp_halves(int N, int M, int L) { return tcs::sp_halves(L, N, M); }
 
-// nm_spmm without a prepacked weight: prepack into pooled scratch, run, release.
+// nm_spmm without a prepacked weight: prepack into pooled scratch (the size bound, no sync), run,
+// release.
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
                        int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha) {
     void* buf = nullptr;
-    nm_status st = scratch_alloc(&buf, tc_sp_prepack_bytes(n, k, N, M, L, tf), s);
+    const size_t bytes = tc_sp_prepack_bytes(n, k, N, M, L, tf);
+    const int H = tcs::sp_halves(L, N, M);
+    nm_status st = scratch_alloc(&buf, bytes, s);
     if (st) return st;
-    st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, buf, s);
-    if (!st) st = tc_sp_run(A, buf, C, c_bf16, m, n, k, N, M, L, tf, s, nullptr, alpha);
+    st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, H, buf, static_cast<int64_t>(bytes), nullptr, false, s);
+    if (!st) st = tc_sp_run(A, buf, H, C, c_bf16, m, n, k, N, M, L, tf, s, nullptr, alpha);
     const cudaError_t e = cudaFreeAsync(buf, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;

@@ -28,7 +28,7 @@ EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_
            "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
            "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked",
            "nm_prepack_bytes_ex", "nm_prepack_ex", "nm_ipc_get_handle", "nm_ipc_open_handle", "nm_ipc_close",
-           "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled"]
+           "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled", "nm_prepack_size"]
 
 
 class NmError(RuntimeError):
@@ -90,6 +90,7 @@ def lib():
         L.nm_prepack_bytes_ex.argtypes = [I64, I64, I, I, I, I, I]
         L.nm_prepack_bytes_ex.restype = I64
         L.nm_prepack_ex.argtypes = [P, P, I64, I64, I, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
+        L.nm_prepack_size.argtypes = [P, P, I64, I64, I, I, I, I, I, ctypes.POINTER(I64), P]
         L.nm_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.nm_ipc_get_handle.argtypes = [P, P, ctypes.POINTER(I64)]
         L.nm_ipc_open_handle.argtypes = [P, I64, ctypes.POINTER(P)]
@@ -129,6 +130,17 @@ def _dev(t: torch.Tensor, name: str):
         raise ValueError(f"{name} must be a CUDA tensor")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous (row-major)")
+
+
+def _check_out(out: torch.Tensor, A: torch.Tensor, m: int, n: int):
+    '''A caller-supplied C: a contiguous CUDA tensor on A's device with shape (m, n) (the kernels
+    write m x n elements of out's dtype at its data pointer).'''
+    _dev(out, "out")
+    if out.device != A.device:
+        raise ValueError(f"out is on {out.device}, A on {A.device}")
+    if tuple(out.shape) != (m, n):
+        raise ValueError(f"out has shape {tuple(out.shape)}, expected {(m, n)}")
+    _dt(out)
 
 
 def version() -> str:
@@ -204,7 +216,7 @@ def nm_spmm(A: torch.Tensor, W: NmWeight, out: torch.Tensor | None = None, out_d
     if out is None:
         out = torch.empty((m, W.n), dtype=cdt, device=A.device)
     else:
-        _dev(out, "out")
+        _check_out(out, A, m, W.n)
     if alpha == 1.0:
         _check(lib().nm_spmm(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), out.data_ptr(), m, W.n, k, W.N,
                              W.M, W.L, _dt(A), _dt(out), MATH[math], _stream(A, stream)), "nm_spmm")
@@ -222,9 +234,13 @@ class PrepackedWeight:
     def __init__(self, W: NmWeight, stream=None, math: str = "auto"):
         self.W = W
         dt = _dt(W.values)
-        nbytes = lib().nm_prepack_bytes_ex(W.n, W.k, W.N, W.M, W.L, dt, MATH[math])
-        if nbytes < 0:
+        if lib().nm_prepack_bytes_ex(W.n, W.k, W.N, W.M, W.L, dt, MATH[math]) < 0:
             raise NmError(2, "nm_prepack_bytes", "bad shape")
+        # the exact size of the compact slot images (one packing pass; synchronizes the stream)
+        nb = ctypes.c_int64(0)
+        _check(lib().nm_prepack_size(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt, MATH[math],
+                                     ctypes.byref(nb), _stream(W.values, stream)), "nm_prepack_size")
+        nbytes = int(nb.value)
         self.buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=W.values.device)
         self.desc = Prepacked()
         _check(lib().nm_prepack_ex(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt, MATH[math],
@@ -250,9 +266,13 @@ def nm_spmm_prepacked(A: torch.Tensor, PW: PrepackedWeight, out: torch.Tensor | 
     m, k = A.shape
     if k != PW.W.k:
         raise NmError(2, "nm_spmm_prepacked", f"A has k={k}, weight has k={PW.W.k}")
+    if A.dtype != PW.W.values.dtype:  # the kernels read A's bytes as the weight's element type
+        raise TypeError(f"A is {A.dtype}, the prepacked weight is {PW.W.values.dtype}")
     cdt = out_dtype or A.dtype
     if out is None:
         out = torch.empty((m, PW.W.n), dtype=cdt, device=A.device)
+    else:
+        _check_out(out, A, m, PW.W.n)
     _check(lib().nm_spmm_prepacked(A.data_ptr(), ctypes.byref(PW.desc), out.data_ptr(), m, _dt(out),
                                    _stream(A, stream)), "nm_spmm_prepacked")
     return out
@@ -339,6 +359,8 @@ def nm_spmm_peers(A: torch.Tensor, W: NmWeight, c_ptrs, ldc: int, col_off: int, 
     every buffer in c_ptrs (own or IPC-mapped device addresses, row pitch ldc)."""
     _dev(A, "A")
     m, k = A.shape
+    if A.dtype != torch.float32 or W.values.dtype != torch.float32:
+        raise TypeError("nm_spmm_peers is the fp32 SIMT peer path: A and values must be float32")
     _check(lib().nm_spmm_peers(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), _ptr_array(c_ptrs), len(c_ptrs),
                                ldc, col_off, n_valid, m, W.n, k, W.N, W.M, W.L, _stream(A, stream)), "nm_spmm_peers")
 
@@ -353,6 +375,8 @@ def nm_spmm_prepacked_peers(A: torch.Tensor, PW: "PrepackedWeight", c_ptrs, ldc:
                             out_dtype=None, stream=None) -> None:
     """nm_spmm_peers for a prepacked shard (bf16 / tf32 slot kernels, or kind 0 -> the SIMT path)."""
     _dev(A, "A")
+    if A.dtype != PW.W.values.dtype:
+        raise TypeError(f"A is {A.dtype}, the prepacked weight is {PW.W.values.dtype}")
     cdt = _dt_of(out_dtype or A.dtype)
     _check(lib().nm_spmm_prepacked_peers(A.data_ptr(), ctypes.byref(PW.desc), _ptr_array(c_ptrs), len(c_ptrs), ldc,
                                          col_off, n_valid, A.shape[0], cdt, _stream(A, stream)),

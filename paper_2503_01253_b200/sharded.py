@@ -23,6 +23,14 @@ import torch
 import torch.distributed as dist
 
 
+def host_staged_all_gather(out: torch.Tensor, inp: torch.Tensor, group=None):
+    """all_gather_into_tensor through host memory (for backends without device collectives, e.g.
+    gloo): out[r] = rank r's inp."""
+    parts = [torch.empty(inp.shape, dtype=inp.dtype) for _ in range(dist.get_world_size(group))]
+    dist.all_gather(parts, inp.cpu(), group=group)
+    out.copy_(torch.stack(parts))
+
+
 def shard_ranges(q: int, G: int):
     """[(g0, g1)] per rank: rank r owns groups [floor(r*q/G), floor((r+1)*q/G))."""
     return [(r * q // G, (r + 1) * q // G) for r in range(G)]
@@ -88,7 +96,7 @@ class ShardedNmLinear:
     (all-gather + unshard kernel) or "p2p" (fused peer-store epilogue: fp32 SIMT kernel, or the bf16
     sparse-tensor-core kernel's direct-store epilogue)."""
 
-    def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl"):
+    def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl", all_gather=None):
         from . import nmspmm
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' or 'p2p'")
@@ -102,13 +110,23 @@ class ShardedNmLinear:
         self.n = n
         self.nr = local_weight.n
         self.exchange = exchange
+        # exchange="nccl": the collective that fills [G][m][nr] from every rank's [m][nr] block
+        # (default torch.distributed.all_gather_into_tensor over the group, i.e. NCCL on GPUs;
+        # injectable so the same branch runs with other backends, e.g. gloo with host staging)
+        self.all_gather = all_gather or (lambda out, inp, group: dist.all_gather_into_tensor(out, inp, group=group))
         self.peers = None
         q = n // local_weight.L
         g0, g1 = shard_ranges(q, self.G)[self.rank]
         self.col_off, self.n_valid = g0 * local_weight.L, (g1 - g0) * local_weight.L
+        # the fused exchange has two epilogues: the bf16 / tf32 slot kernels (prepack kind 2 / 3) and
+        # the fp32 SIMT kernel; any other weight (e.g. bf16 with L outside {16, 32, 64, 128}) has none
+        if exchange == "p2p" and local_weight.values.dtype != torch.float32 and (
+                self.PW is None or self.PW.kind not in (2, 3)):
+            raise ValueError("exchange='p2p' needs an fp32 weight or a bf16 weight the slot kernel takes "
+                             "(L in {16, 32, 64, 128}); use exchange='nccl'")
 
     @classmethod
-    def from_dense(cls, B: torch.Tensor, N: int, M: int, L: int, group=None, exchange: str = "nccl"):
+    def from_dense(cls, B: torch.Tensor, N: int, M: int, L: int, group=None, exchange: str = "nccl", all_gather=None):
         """Compress only this rank's columns (compression is per column group, so
         the shard of compress(B) equals compress of the shard)."""
         from . import nmspmm
@@ -121,7 +139,7 @@ class ShardedNmLinear:
         Bs[:, :(g1 - g0) * L] = B[:, g0 * L:g1 * L]
         # padding groups are all-zero: compress gives zero values and the pattern 0..N-1
         W = nmspmm.nm_compress(Bs.contiguous(), N, M, L)
-        return cls(W, n, group, exchange)
+        return cls(W, n, group, exchange, all_gather)
 
     def local(self, A: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         from . import nmspmm
@@ -155,7 +173,7 @@ class ShardedNmLinear:
         if self.G == 1 and self.nr == self.n:  # a single shard is already C (no exchange step)
             return c_local
         gathered = torch.empty((self.G, m, self.nr), dtype=c_local.dtype, device=A.device)
-        dist.all_gather_into_tensor(gathered, c_local, group=self.group)
+        self.all_gather(gathered, c_local, self.group)
         C = torch.empty((m, self.n), dtype=c_local.dtype, device=A.device)
         nmspmm.nm_unshard_columns(gathered, C, self.G, m, self.nr, self.n, self.W.L)
         return C

@@ -272,19 +272,18 @@ TC_CASES = [
 ]
 
 
-TC_PATHS = {"sp": ("1", "1", 4), "pair": ("0", "1", 2), "plain": ("0", "0", 2)}  # NM_TC_SP, NM_TC_PAIR, kernel id
+TC_PATHS = {"sp": ("1", 4), "generic": ("0", 0)}  # NM_TC_SP, kernel id (0: the generic correctness kernel)
 
 
 def use_tc_path(monkeypatch, path):
-    sp, pair, kid = TC_PATHS[path]
+    sp, kid = TC_PATHS[path]
     monkeypatch.setenv("NM_TC_SP", sp)
-    monkeypatch.setenv("NM_TC_PAIR", pair)
     return kid
 
 
 @pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
 @pytest.mark.parametrize("cdt", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("path", ["sp", "pair"])
+@pytest.mark.parametrize("path", ["sp", "generic"])
 def test_spmm_tc_bf16_vs_oracle(nm, oracle, monkeypatch, m, n, k, N, M, L, cdt, path):
     kid = use_tc_path(monkeypatch, path)
     A = synth.bf16grid((m, k), 51, synth.TID_A)
@@ -299,7 +298,7 @@ def test_spmm_tc_bf16_vs_oracle(nm, oracle, monkeypatch, m, n, k, N, M, L, cdt, 
 
 
 @pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
-@pytest.mark.parametrize("path", ["sp", "pair"])
+@pytest.mark.parametrize("path", ["sp", "generic"])
 def test_spmm_tc_bf16_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L, path):
     """Integer inputs: every partial sum is exact in fp32 -> bit-exact C (fp32 out)."""
     use_tc_path(monkeypatch, path)
@@ -318,7 +317,7 @@ def test_spmm_tc_bf16_deterministic(nm):
 
 
 @pytest.mark.parametrize("cfg", ["cfg2", "cfg3_62", "cfg3_75", "cfg4_65b"])
-@pytest.mark.parametrize("path", ["sp", "pair"])
+@pytest.mark.parametrize("path", ["sp"])
 def test_spmm_tc_bf16_full_size_sampled(nm, oracle, monkeypatch, cfg, path):
     use_tc_path(monkeypatch, path)
     m, n, k, N, M, L = {"cfg2": (4096, 4096, 4096, 16, 32, 32), "cfg3_62": (2048, 11008, 4096, 12, 32, 32),
@@ -371,7 +370,7 @@ def test_spmm_f32_split_tail(nm, oracle, monkeypatch, split):
 
 # --------------------------------------------------------------- prepacked weights (P:470-475 offline step)
 @pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
-@pytest.mark.parametrize("path", ["sp", "pair", "plain"])
+@pytest.mark.parametrize("path", ["sp", "generic"])
 def test_spmm_tc_prepacked_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M, L, path):
     use_tc_path(monkeypatch, path)
     A = synth.integer((m, k), 81, synth.TID_A)
@@ -381,7 +380,7 @@ def test_spmm_tc_prepacked_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M,
     PW = nm.nm_prepack(W)
     C = nm.nm_spmm_prepacked(dev(A, torch.bfloat16), PW, out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L))
-    assert PW.kind == {"sp": 2, "pair": 1}.get(path, PW.kind)
+    assert PW.kind == {"sp": 2, "generic": 0}[path]
     C2 = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=torch.float32).cpu().numpy()
     assert np.array_equal(C, C2)
 
@@ -691,7 +690,7 @@ SCALED_PATHS = [  # (name, ab dtype, math, env, expected kernel id)
     ("simt", torch.float32, "f32_simt", {}, 1),
     ("generic", torch.float32, "f32_simt", {}, 0),          # L = 3 -> generic kernel + scaling pass
     ("sp_bf16", torch.bfloat16, "bf16_tc", {}, 4),
-    ("pair_bf16", torch.bfloat16, "bf16_tc", {"NM_TC_SP": "0"}, 2),
+    ("generic_bf16", torch.bfloat16, "bf16_tc", {"NM_TC_SP": "0"}, 0),
     ("tf32", torch.float32, "tf32_tc", {}, 3),
 ]
 
