@@ -42,13 +42,20 @@ CONFIGS = {
     "cfg3_62": (2048, 11008, 4096, 12, 32, 32),
     "cfg3_75": (2048, 11008, 4096, 8, 32, 32),
     "cfg4_13b": (2048, 13824, 5120, 4, 32, 32),
+    "cfg4_13b_sq": (2048, 5120, 5120, 4, 32, 32),
+    "cfg4_65b_sq": (2048, 8192, 8192, 4, 32, 32),
     "cfg4_65b": (2048, 22016, 8192, 4, 32, 32),
+    # m = 256 tokens is the bf16 HBM-bound point of the 87.5 % regime
+    "cfg4_65b_m256": (256, 22016, 8192, 4, 32, 32),
+    "cfg4_13b_m256": (256, 13824, 5120, 4, 32, 32),
 }
 HEADLINE = "cfg2"
 # one metric string for both arms (the driver pairs the lines by it)
 METRIC = "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M"
-VARIANTS = ["cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_13b:f32", "cfg4_65b:f32", "cfg3_62:bf16",
-            "cfg3_75:bf16", "cfg4_13b:bf16", "cfg4_65b:bf16", "cfg2:tf32", "cfg3_62:tf32", "cfg3_75:tf32",
+VARIANTS = ["cfg1:f32", "cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_13b:f32", "cfg4_13b_sq:f32",
+            "cfg4_65b_sq:f32", "cfg4_65b:f32", "cfg4_65b_m256:f32", "cfg3_62:bf16", "cfg3_75:bf16",
+            "cfg4_13b:bf16", "cfg4_13b_sq:bf16", "cfg4_65b_sq:bf16", "cfg4_65b:bf16", "cfg4_65b_m256:bf16",
+            "cfg4_13b_m256:bf16", "cfg2:tf32", "cfg3_62:tf32", "cfg3_75:tf32",
             "cfg4_65b:tf32"]  # tf32 = fp32 operands on the tf32 sparse tensor cores (opt-in math)
 
 
@@ -435,11 +442,18 @@ def run_ours(args):
             # tf32 dense peak = the measured bf16 peak x the nominal tf32/bf16 ratio 1/2
             peak_v = (fp32_alu_peak_tflops(sm_mhz) if vdt == "f32" else
                       peaks.get("bf16_tflops", 1590.0) / (2.0 if vdt == "tf32" else 1.0))
+            # the relevant roofline: the slower of compute (FLOPs / peak) and HBM (algorithmic bytes /
+            # measured copy bandwidth); frac = that time / the kernel's time
+            e_v = 2 if vdt == "bf16" else 4
+            t_c = flop_count(vcfg) / (peak_v * 1e12)
+            t_m = alg_bytes(vcfg, e_v) / (peaks.get("hbm_gbs", 6650.0) * 1e9)
+            t_k = r["kernel_ms"] * 1e-3
             variants.append({"config": name, "dtype": vdt, "m_n_k": vcfg[:3], "N:M": f"{vcfg[3]}:{vcfg[4]}",
                              "L": vcfg[5], "tflops": round(r["tflops"], 3), "ms": round(r["ms"], 4),
                              "kernel_tflops": round(r["kernel_tflops"], 3),
-                             "roofline_frac": round(r["kernel_tflops"] / peak_v, 4),
-                             "roofline_bound": "alu" if vdt == "f32" else "tensor",
+                             "roofline_frac": round(max(t_c, t_m) / t_k, 4),
+                             "roofline_bound": ("hbm" if t_m > t_c else "alu" if vdt == "f32" else "tensor"),
+                             "hbm_gbs_achieved": round(alg_bytes(vcfg, e_v) / t_k / 1e9, 1),
                              "cublas_dense_tflops": round(r["cublas_dense_tflops"], 3),
                              "speedup_vs_cublas": round(r["speedup_vs_cublas"], 3),
                              "target_speedup": round(r["target_speedup"], 3)}
@@ -469,7 +483,8 @@ def run_sharded(args):
     dtype = torch.float32 if args.dtype == "f32" else torch.bfloat16
     m, n, k, N, M, L = cfg
     A, Bd, _ = make_inputs(cfg, dtype, "cuda")  # A replicated (column-parallel input), B generated identically
-    layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD, exchange=args.exchange)
+    chunks = args.chunks if args.chunks > 0 else (4 if m >= 1024 else 1)
+    layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD, exchange=args.exchange, chunks=chunks)
     del Bd
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     flush = (lambda: flush_buf.fill_(1.0)) if not args.no_flush else None
@@ -514,7 +529,7 @@ def run_sharded(args):
                 "warmup": args.warmup, "ms_per_step": round(t_step, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
                 "config": config_dict(cfg, args.dtype, {"parallelism": f"col{world} (column groups sharded, " + (
-                    "NCCL all-gather of C)" if args.exchange == "nccl" else
+                    f"NCCL all-gather of C, {chunks} overlapped row slices)" if args.exchange == "nccl" else
                     "fused peer-store epilogue over CUDA IPC / NVLink + flag barrier)")}),
                 "gpu_launches": int(launches), "clocks": sampler.summary(),
                 "roofline": {"bound": "alu" if dtype == torch.float32 else "tensor", "achieved": round(ach, 3),
@@ -581,6 +596,8 @@ def main():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="column-sharded path even at one rank (testing)")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
+    ap.add_argument("--chunks", type=int, default=0,
+                    help="sharded NCCL path: row slices whose all-gather overlaps the next slice (0 = auto)")
     ap.add_argument("--launch-check", action="store_true",
                     help="start the ranks, all-reduce a count over gloo, rank 0 prints it (no GPU needed)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],

@@ -209,6 +209,8 @@ nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, i
  * weights + sparse-MMA metadata per 64- (bf16) / 32-slot (tf32) stage.  The buffer is compact:
  *   [header 256 B | per tile {stages, first slot, image offset, image size} | slot lists |
  *    stage images (even stages: H x (8 KB weights + 2 KB metadata of the stage pair), odd: H x 8 KB)]
+ * fp32 weights on the SIMT kernel with 128 % L == 0 get kind 4: the index matrix bit-packed and
+ * tile-major (nm_index_pack below), read by the kernel instead of D.
  * Other weights keep using `values` / `idx` directly (kind 0, no buffer).
  *   nm_prepack_bytes[_ex]: a data-independent UPPER BOUND of the buffer (0 for kind 0; -1 on bad
  *                      args).  Host only.
@@ -225,7 +227,9 @@ typedef struct {
     int32_t magic;   /* 0x4B504D4E ("NMPK") once filled */
     int32_t kind;    /* 0 = plain (values/idx used directly),
                         2 = sparse-tensor-core slot prepack, bf16 (whole buffer at `bperm`),
-                        3 = the same for tf32 (fp32 weights, nm_prepack_ex with NM_MATH_TF32_TC) */
+                        3 = the same for tf32 (fp32 weights, nm_prepack_ex with NM_MATH_TF32_TC),
+                        4 = fp32 SIMT weight with bit-packed tile-major indices (nm_index_pack
+                            words at `tbl`; 128 % L == 0) */
     int32_t dtype, N, M, L;
     int64_t n, k;
     int32_t bn;      /* kind 2/3: output columns per tile (128 H) */
@@ -234,7 +238,7 @@ typedef struct {
     const void* values;
     const uint8_t* idx;
     void* perm;      /* reserved (NULL) */
-    void* tbl;       /* reserved (NULL) */
+    void* tbl;       /* kind 4: the packed index words */
     void* bperm;     /* kind 2/3: the prepacked buffer */
 } nm_prepacked;
 
@@ -252,6 +256,22 @@ nm_status nm_prepack_size(const void* values, const uint8_t* idx, int64_t n, int
                           nm_dtype dt, nm_math math, int64_t* bytes, void* stream);
 nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
                         nm_math math, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
+
+/*
+ * Bit-packed indices (an index needs only ceil(log2 M) bits) in the tile-major layout of
+ * the paper's transformLayout (Listing 3: fewer global memory transactions): b =
+ * max(1, ceil(log2 M)) bits per entry, e = floor(32 / b) entries per 32-bit word; the q column
+ * groups are cut into tiles of T = 128 / L groups (needs 128 % L == 0; one SIMT CTA tile of 128
+ * output columns); a tile's entries x = u*T + t (row u < w, group t < T) form Wt = ceil(w*T / e)
+ * consecutive words, entry x in word tile*Wt + x / e at bit (x % e) * b (groups >= q and unused
+ * bits are 0).  Bit-exact with the oracle's index_pack (R28).
+ *   nm_index_packed_words : words of the packed form (-1 on bad args / 128 % L != 0).  Host only.
+ *   nm_index_pack / unpack: D (w x q uint8, device) <-> words (device).  Asynchronous.
+ */
+int64_t nm_index_packed_words(int64_t k, int64_t n, int N, int M, int L);
+nm_status nm_index_pack(const uint8_t* idx, int64_t k, int64_t n, int N, int M, int L, uint32_t* words, void* stream);
+nm_status nm_index_unpack(const uint32_t* words, int64_t k, int64_t n, int N, int M, int L, uint8_t* idx,
+                          void* stream);
 
 /*
  * Fused multi-GPU exchange of the column-sharded layer.  Column j of C

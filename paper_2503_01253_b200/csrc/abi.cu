@@ -226,12 +226,15 @@ nm_status validate_launch(const uint8_t* idx, int64_t k, int64_t n, int N, int M
                           cudaStream_t s);
 nm_status unshard_launch(const void* src, void* dst, int64_t G, int64_t m, int64_t nr, int64_t q, int L,
                          int elem_bytes, cudaStream_t s);
+int64_t index_packed_words(int64_t k, int64_t n, int N, int M, int L);
+nm_status index_pack_launch(const uint8_t* D, uint32_t* P, int64_t k, int64_t n, int N, int M, int L, bool unpack,
+                            cudaStream_t s);
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
-                          float alpha = 1.f);
+                          float alpha = 1.f, const uint32_t* Dw = nullptr);
 bool simt_pipe_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 nm_status simt_pipe_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                            int N, int M, int L, cudaStream_t s);
@@ -700,10 +703,18 @@ static bool prepack_kind2(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt
     static const float dummy[4] = {0, 0, 0, 0};
     return dt == NM_BF16 && k > 0 && tc_sp_ok(dummy, dummy, 1, n, k, N, M, L);
 }
-// 2 / 3 = slot images (bf16 / tf32), 0 = none (values / idx used directly)
+// kind 4 iff the fp32 SIMT kernel runs the weight and its tiles hold whole groups (128 % L == 0):
+// the bit-packed tile-major index words replace D on the hot path
+static bool prepack_kind4(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
+    static const float dummy[4] = {0, 0, 0, 0};
+    return dt == NM_F32 && (math == NM_MATH_AUTO || math == NM_MATH_F32_SIMT) && k > 0 && 128 % L == 0 &&
+           simt_f32_applicable(dummy, dummy, dummy, 1, n, k, N, M, L);
+}
+// 2 / 3 = slot images (bf16 / tf32), 4 = packed indices (fp32 SIMT), 0 = none (values / idx directly)
 static int prepack_kind(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
     if (prepack_kind3(n, k, N, M, L, dt, math)) return 3;
     if (prepack_kind2(n, k, N, M, L, dt)) return 2;
+    if (prepack_kind4(n, k, N, M, L, dt, math)) return 4;
     return 0;
 }
 }  // namespace nm
@@ -712,6 +723,7 @@ extern "C" {
 int64_t nm_prepack_bytes_ex(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt, nm_math math) {
     if (check_common(0, n, k, N, M, L) != NM_OK || dt > NM_BF16 || math > NM_MATH_BF16_TC) return -1;
     const int kind = prepack_kind(n, k, N, M, L, dt, math);
+    if (kind == 4) return 4 * index_packed_words(k, n, N, M, L);
     return kind ? static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, kind == 3)) : 0;
 }
 
@@ -727,7 +739,8 @@ nm_status nm_prepack_size(const void* values, const uint8_t* idx, int64_t n, int
     if (dt > NM_BF16 || math > NM_MATH_BF16_TC) return fail(NM_ERR_UNSUPPORTED, "dtype/math");
     const int kind = prepack_kind(n, k, N, M, L, dt, math);
     *bytes = 0;
-    if (!kind) return NM_OK;
+    if (kind == 4) *bytes = 4 * index_packed_words(k, n, N, M, L);
+    if (kind == 0 || kind == 4) return NM_OK;
     if ((st = require_device())) return st;
     return tc_sp_prepack(values, idx, n, k, N, M, L, kind == 3, tc_sp_halves(N, M, L), nullptr, 0, bytes, true,
                          static_cast<cudaStream_t>(stream));
@@ -749,7 +762,16 @@ nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64
     out->values = values;
     out->idx = idx;
     const int kind = prepack_kind(n, k, N, M, L, dt, math);
-    if (kind) {
+    if (kind == 4) {
+        const int64_t need = 4 * index_packed_words(k, n, N, M, L);
+        if (!buf || buf_bytes < need) return fail(NM_ERR_NULL, "nm_prepack: buffer missing or below nm_prepack_size");
+        if ((st = require_device())) return st;
+        if ((st = index_pack_launch(idx, static_cast<uint32_t*>(buf), k, n, N, M, L, false,
+                                    static_cast<cudaStream_t>(stream))))
+            return st;
+        out->kind = 4;
+        out->tbl = buf;  // the packed index words
+    } else if (kind) {
         if (!buf) return fail(NM_ERR_NULL, "nm_prepack: buffer missing (size: nm_prepack_size)");
         if ((st = require_device())) return st;
         const int H = tc_sp_halves(N, M, L);
@@ -788,6 +810,20 @@ nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64
                              static_cast<cudaStream_t>(stream));
         if (tf) return fail(NM_ERR_UNSUPPORTED, "tf32 sparse-tensor-core path needs A 16-B and C 4-B aligned");
     }
+    if (w->kind == 4) {  // fp32 SIMT kernel on the bit-packed tile-major indices
+        nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
+        if (st) return st;
+        if (c_dt != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
+        if (m == 0 || w->n == 0) return NM_OK;
+        if (!A || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked: NULL pointer");
+        if ((st = require_device())) return st;
+        const int mode = simt_mode(m, w->n, w->k, w->N, w->M, w->L);
+        if (mode != 3 && simt_f32_applicable(A, w->values, C, m, w->n, w->k, w->N, w->M, w->L))
+            return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(w->values), w->idx,
+                                   static_cast<float*>(C), m, w->n, w->k, w->N, w->M, w->L, mode,
+                                   static_cast<cudaStream_t>(stream), nullptr, 1.f,
+                                   static_cast<const uint32_t*>(w->tbl));
+    }
     return nm_spmm(A, w->values, w->idx, C, m, w->n, w->k, w->N, w->M, w->L, static_cast<nm_dtype>(w->dtype), c_dt,
                    NM_MATH_AUTO, stream);
 }
@@ -818,6 +854,29 @@ nm_status nm_profile_end(double* kernel_ms, int64_t* kernel_count, int64_t* laun
     if (kernel_count) *kernel_count = cnt;
     if (launches) *launches = g_prof.launches;
     return NM_OK;
+}
+
+int64_t nm_index_packed_words(int64_t k, int64_t n, int N, int M, int L) {
+    if (check_common(0, n, k, N, M, L) != NM_OK) return -1;
+    return index_packed_words(k, n, N, M, L);
+}
+
+nm_status nm_index_pack(const uint8_t* idx, int64_t k, int64_t n, int N, int M, int L, uint32_t* words, void* stream) {
+    nm_status st = check_common(0, n, k, N, M, L);
+    if (st) return st;
+    if (128 % L) return fail(NM_ERR_UNSUPPORTED, "nm_index_pack: tiles of 128 columns need 128 % L == 0");
+    if (k * n > 0 && (!idx || !words)) return fail(NM_ERR_NULL, "nm_index_pack: NULL pointer");
+    if ((st = require_device())) return st;
+    return index_pack_launch(idx, words, k, n, N, M, L, false, static_cast<cudaStream_t>(stream));
+}
+
+nm_status nm_index_unpack(const uint32_t* words, int64_t k, int64_t n, int N, int M, int L, uint8_t* idx, void* stream) {
+    nm_status st = check_common(0, n, k, N, M, L);
+    if (st) return st;
+    if (128 % L) return fail(NM_ERR_UNSUPPORTED, "nm_index_unpack: tiles of 128 columns need 128 % L == 0");
+    if (k * n > 0 && (!idx || !words)) return fail(NM_ERR_NULL, "nm_index_unpack: NULL pointer");
+    if ((st = require_device())) return st;
+    return index_pack_launch(idx, const_cast<uint32_t*>(words), k, n, N, M, L, true, static_cast<cudaStream_t>(stream));
 }
 
 nm_status nm_unshard_columns(const void* src, void* dst, int64_t G, int64_t m, int64_t nr, int64_t n, int L,

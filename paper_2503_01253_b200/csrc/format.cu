@@ -210,4 +210,68 @@ nm_status unshard_launch(const void* src, void* dst, int64_t G, int64_t m, int64
     return NM_OK;
 }
 
+// ------------------------------------------------------------ bit-packed indices
+// The index matrix D with ceil(log2 M) bits per entry in a tile-major layout
+// (transformLayout, P:419 / Listing 3): per column tile of T = 128 / L groups (one SIMT CTA tile of
+// 128 output columns) its entries x = u * T + t (row u, group t of the tile) are a contiguous
+// stream of 32-bit words, floor(32 / b) entries per word, entry x at word x / e, bit (x % e) * b.
+// A CTA's whole index stream is one coalesced run (R28).
+struct IdxPack {
+    int b, e, T;
+    int64_t w, q, Wt, ntiles;
+};
+static IdxPack idx_pack_geom(int64_t k, int64_t n, int N, int M, int L) {
+    IdxPack g{};
+    g.b = 1;
+    while ((1 << g.b) < M) ++g.b;
+    g.e = 32 / g.b;
+    g.T = 128 / L;
+    g.w = k / M * N;
+    g.q = n / L;
+    g.ntiles = (g.q + g.T - 1) / g.T;
+    g.Wt = (g.w * g.T + g.e - 1) / g.e;
+    return g;
+}
+
+__global__ void index_pack_kernel(const uint8_t* __restrict__ D, uint32_t* __restrict__ P, IdxPack g) {
+    const int64_t wi = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // one word
+    if (wi >= g.ntiles * g.Wt) return;
+    const int64_t tile = wi / g.Wt, x0 = (wi % g.Wt) * g.e;
+    uint32_t word = 0;
+    for (int i = 0; i < g.e; ++i) {
+        const int64_t x = x0 + i, u = x / g.T, gg = tile * g.T + x % g.T;
+        if (u < g.w && gg < g.q) word |= static_cast<uint32_t>(D[u * g.q + gg]) << (i * g.b);
+    }
+    P[wi] = word;
+}
+
+__global__ void index_unpack_kernel(const uint32_t* __restrict__ P, uint8_t* __restrict__ D, IdxPack g) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // one entry of D
+    if (e >= g.w * g.q) return;
+    const int64_t u = e / g.q, gg = e % g.q, x = u * g.T + gg % g.T;
+    const uint32_t word = P[(gg / g.T) * g.Wt + x / g.e];
+    D[e] = static_cast<uint8_t>((word >> ((x % g.e) * g.b)) & ((1u << g.b) - 1u));
+}
+
+int64_t index_packed_words(int64_t k, int64_t n, int N, int M, int L) {
+    if (L < 1 || 128 % L || M < 1 || k % M || n % L) return -1;
+    const IdxPack g = idx_pack_geom(k, n, N, M, L);
+    return g.ntiles * g.Wt;
+}
+
+nm_status index_pack_launch(const uint8_t* D, uint32_t* P, int64_t k, int64_t n, int N, int M, int L, bool unpack,
+                            cudaStream_t s) {
+    const IdxPack g = idx_pack_geom(k, n, N, M, L);
+    const int64_t total = unpack ? g.w * g.q : g.ntiles * g.Wt;
+    if (total == 0) return NM_OK;
+    const unsigned blocks = static_cast<unsigned>(ceil_div(total, 256));
+    if (unpack)
+        index_unpack_kernel<<<blocks, 256, 0, s>>>(P, const_cast<uint8_t*>(D), g);
+    else
+        index_pack_kernel<<<blocks, 256, 0, s>>>(D, P, g);
+    note_launch();
+    NM_LAUNCH_CHECK("index_pack_kernel");
+    return NM_OK;
+}
+
 }  // namespace nm

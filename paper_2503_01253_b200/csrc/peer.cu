@@ -12,7 +12,7 @@
 namespace nm {
 
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha);
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha, const uint32_t* Dw);
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 nm_status require_device();
@@ -160,13 +160,13 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
     const int mode = m % 4 == 0 ? 1 : 0;  // A^T staging needs m % 4 == 0 (as in the selector)
     return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
                            static_cast<float*>(po.c[0]), m, nr, k, N, M, L, mode, static_cast<cudaStream_t>(stream), &po,
-                           1.f);
+                           1.f, nullptr);
 }
 
 nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* const* C_peers, int G, int64_t ldc,
                                   int64_t col_off, int64_t n_valid, int64_t m, nm_dtype c_dt, void* stream) {
     if (!w || w->magic != 0x4B504D4E) return fail(NM_ERR_NULL, "nm_spmm_prepacked_peers: descriptor not filled by nm_prepack");
-    if (w->kind == 0) {  // fp32 weights: the SIMT kernel's peer epilogue (fp32 A, B' and C only)
+    if (w->kind == 0 || w->kind == 4) {  // fp32 weights: the SIMT kernel's peer epilogue (fp32 A, B', C)
         if (w->dtype != NM_F32 || c_dt != NM_F32)
             return fail(NM_ERR_UNSUPPORTED, "nm_spmm_prepacked_peers: a weight without slot images (prepack kind 0) "
                                             "takes the fp32 SIMT peer path, which needs fp32 values and an fp32 C");

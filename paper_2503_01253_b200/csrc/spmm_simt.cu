@@ -45,11 +45,12 @@ struct Params {
     int m, n, k, N, M, L;
     int q, wp, bk, bkw, npanels, nboxA;
     int at_ld;
-    // tile schedule (1-D grid, n fastest so column tiles sharing an A panel run together);
+    // tile schedule (1-D grid, grouped raster: `gm` row tiles x all column tiles per group);
     // the last, partial wave is split along k ("stream-K lite"): tiles >= full_tiles are
     // done by `split` CTAs each, whose partial sums meet in ws and are added in a fixed
     // order by whichever CTA finishes last (deterministic, no atomics on data).
     int ntn, full_tiles, split;
+    int ntm, gm;  // row tiles; rows per raster group
     float* ws;
     int* counters;
     // peer-store epilogue (nm_spmm_peers): the C tile goes to cpeer[0 .. npeer) at
@@ -59,6 +60,11 @@ struct Params {
     int npeer, n_valid;
     int64_t ldc, col_off;
     float alpha;  // C = alpha . A B~ (1: the product; M/N: Eq. 1 as printed, nm_spmm_scaled)
+    // bit-packed tile-major indices (nm_index_pack, P:288 / P:419) instead of D when non-null:
+    // column tile ct's stream at Dw + ct * dwt, entry x = u * dT + t at word x / de, bit (x % de) * db
+    const uint32_t* Dw;
+    int db, de, dT;
+    int64_t dwt;
 };
 
 // Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
@@ -102,7 +108,17 @@ __global__ void __launch_bounds__(THREADS, 2)
         tile = p.full_tiles + (tile - p.full_tiles) / p.split;
         nparts = p.split;
     }
-    const int m0 = (tile / p.ntn) * BM, n0 = (tile % p.ntn) * BN;
+    // grouped raster: groups of `gm` row tiles sweep the column tiles with the row index fastest, so
+    // the group's A^T panels stay in L2 and each B' panel is read from DRAM once per group (an
+    // n-fastest order re-streamed all of B' every ~2 row tiles: 3.3x the algorithmic DRAM bytes)
+    int tm, tn;
+    {
+        const int per = p.gm * p.ntn, grp = tile / per, r = tile - grp * per;
+        const int first = grp * p.gm, gsz = min(p.gm, p.ntm - first);
+        tm = first + r % gsz;
+        tn = r / gsz;
+    }
+    const int m0 = tm * BM, n0 = tn * BN;
     const int p_begin = part * p.npanels / nparts, p_end = (part + 1) * p.npanels / nparts;
     const int g_first = n0 / p.L;
     const int nslots = min((n0 + BN - 1) / p.L, p.q - 1) - g_first + 1;
@@ -115,7 +131,7 @@ __global__ void __launch_bounds__(THREADS, 2)
         fence_mbar_init();
     }
     if (PK)
-        for (int i = tid; i < p.npanels; i += THREADS) smask[i] = p.masks[static_cast<int64_t>(tile % p.ntn) * p.npanels + i];
+        for (int i = tid; i < p.npanels; i += THREADS) smask[i] = p.masks[static_cast<int64_t>(tn) * p.npanels + i];
     __syncthreads();
 
     const uint32_t stage_tx =
@@ -174,8 +190,20 @@ __global__ void __launch_bounds__(THREADS, 2)
     const int wtot = (p.k / p.M) * p.N;
     auto load_d = [&](int panel) {
         const int u0 = panel * p.bkw;
-        const uint8_t* Dp = p.D + static_cast<int64_t>(u0) * p.q + g_first;
         const int ulim = wtot - u0;  // rows of D left (last panel may be partial)
+        if (p.Dw) {  // packed: this column tile's contiguous word stream (g_first = tile * dT)
+            const uint32_t* Dt = p.Dw + static_cast<int64_t>(tn) * p.dwt;
+            const uint32_t mask = (1u << p.db) - 1u;
+#pragma unroll
+            for (int r = 0; r < D_PER_THREAD; ++r) {
+                if (r >= nd) break;
+                const int u = d_us[r] >> 8, sl = d_us[r] & 255;
+                const int64_t x = static_cast<int64_t>(u0 + u) * p.dT + sl;
+                dreg[r] = (u < ulim) ? static_cast<int>((__ldg(Dt + x / p.de) >> ((x % p.de) * p.db)) & mask) : 0;
+            }
+            return;
+        }
+        const uint8_t* Dp = p.D + static_cast<int64_t>(u0) * p.q + g_first;
 #pragma unroll
         for (int r = 0; r < D_PER_THREAD; ++r) {
             if (r >= nd) break;
@@ -260,16 +288,18 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
                 for (int i = 0; i < 8; ++i) a1[i] = a0[i];
             }
+            // the 8 x 8 outer product as 32 paired FMAs (FFMA2, sm_100: two fp32 FMAs with the A
+            // element broadcast, each rounded exactly as fmaf -- the same bits, half the issue slots)
+            const float2 b01 = make_float2(b0.x, b0.y), b23 = make_float2(b0.z, b0.w);
+            const float2 b45 = make_float2(b1.x, b1.y), b67 = make_float2(b1.z, b1.w);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                acc[i][0] = fmaf(a0[i], b0.x, acc[i][0]);
-                acc[i][1] = fmaf(a0[i], b0.y, acc[i][1]);
-                acc[i][2] = fmaf(a0[i], b0.z, acc[i][2]);
-                acc[i][3] = fmaf(a0[i], b0.w, acc[i][3]);
-                acc[i][4] = fmaf(a1[i], b1.x, acc[i][4]);
-                acc[i][5] = fmaf(a1[i], b1.y, acc[i][5]);
-                acc[i][6] = fmaf(a1[i], b1.z, acc[i][6]);
-                acc[i][7] = fmaf(a1[i], b1.w, acc[i][7]);
+                const float2 x0 = make_float2(a0[i], a0[i]), x1 = make_float2(a1[i], a1[i]);
+                float2 c;
+                c = __ffma2_rn(x0, b01, make_float2(acc[i][0], acc[i][1])), acc[i][0] = c.x, acc[i][1] = c.y;
+                c = __ffma2_rn(x0, b23, make_float2(acc[i][2], acc[i][3])), acc[i][2] = c.x, acc[i][3] = c.y;
+                c = __ffma2_rn(x1, b45, make_float2(acc[i][4], acc[i][5])), acc[i][4] = c.x, acc[i][5] = c.y;
+                c = __ffma2_rn(x1, b67, make_float2(acc[i][6], acc[i][7])), acc[i][6] = c.x, acc[i][7] = c.y;
             }
         }
         if (panel + 1 < p_end) store_d(panel + 1);
@@ -448,10 +478,20 @@ static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, con
 // mode: 0 = A panels straight from A (swizzled [m][k] boxes), 1 = A^T staged (tile TMA),
 // 2 = A^T staged + packed col_info loads (high sparsity).  The selector decides.
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha) {
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha,
+                          const uint32_t* Dw) {
     using namespace simt;
     Params p{};
     p.D = D;
+    if (Dw) {  // bit-packed tile-major indices (needs 128 % L == 0: a CTA tile = whole groups)
+        p.Dw = Dw;
+        p.db = 1;
+        while ((1 << p.db) < M) ++p.db;
+        p.de = 32 / p.db;
+        p.dT = 128 / L;
+        p.dwt = ((k / M * N) * p.dT + p.de - 1) / p.de;
+        if (mode == 2) mode = 1;  // the packed col_info mode reads D itself
+    }
     p.C = C;
     p.alpha = alpha;
     if (po) {
@@ -509,6 +549,13 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
 
     // schedule: full waves of whole tiles, the partial last wave split along k
     p.ntn = ntiles_n;
+    p.ntm = static_cast<int>(ceil_div(m, BM));
+    {
+        const char* ge = getenv("NM_SIMT_GROUP");
+        p.gm = ge ? atoi(ge) : 8;
+        if (p.gm < 1) p.gm = 1;
+        if (p.gm > p.ntm) p.gm = p.ntm;
+    }
     const int ntiles = ntiles_n * static_cast<int>(ceil_div(m, BM));
     const int resident = 2 * num_sms();  // 2 CTAs per SM (launch bounds, ~105 KB smem)
     const int rem = ntiles % resident;

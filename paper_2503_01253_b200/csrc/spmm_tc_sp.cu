@@ -298,13 +298,13 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int npairs = (nst_all + 1) >> 1;
     const int sa = min(nst_all, 2 * (part * npairs / nparts));
     const int sb = min(nst_all, 2 * ((part + 1) * npairs / nparts));
-    const int nst = sb - sa;  // stages this CTA runs (ring index = st - sa)
+    const int nst = (p.dbg & 512) ? 0 : sb - sa;  // stages this CTA runs (ring index = st - sa); dbg 512: none
     const int tail_idx = tid_lin - p.full_ctas;
 
     if (warp == MMA_WARP) {
         if (lane == 0) {
             for (int s = 0; s < STAGES; ++s) {
-                mbar_init(&full[s], 1 + 32 * GATHER_WARPS);
+                mbar_init(&full[s], 1 + 2 * 32);  // two owner warps' copies + the weight copy
                 mbar_init(&empty[s], MCAST ? 2 : 1);
             }
             mbar_init(acc_full, 1);
@@ -321,23 +321,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t crank = MCAST ? cluster_rank() : 0u;
 
     if (warp < GATHER_WARPS) {
-        // ============ gather: one slot row (NT tokens) per warp instruction ============
-        // lane l copies tokens [8l, 8l+8) of the row: token atom l/8, 16-B chunk l%8 of the
-        // 128-B swizzled row (chunk ^= row % 8).  Warp wg owns RPW consecutive rows of a stage.
-        // Completion: cp.async.mbarrier.arrive.noinc per thread (no wait in the loop).
+        // ============ gather: stage-owning warp pairs ============
+        // Warps (g, g + 4) own the stages st == g (mod 4) of this CTA's range and copy half of the
+        // stage's slot rows each (bf16: 32 rows of NT tokens, one warp-wide 16-B cp.async per row;
+        // tf32: 16 rows x 2 token halves).  A warp thus walks every 4th stage with 32 independent
+        // copies per visit, instead of every stage with 8 -- measured on B200 (scripts/ubench_ring2,
+        // profiles/r02_ring_layouts.txt) the per-stage ring time drops from ~690 to ~420 clk when
+        // stage ownership replaces lock-step sharing.  4 owners <= STAGES, so a wait on empty[s]
+        // is never two ring laps behind (no parity aliasing).  Completion: one
+        // cp.async.mbarrier.arrive.noinc per thread (full count 2 x 32 + 1: the weight copy).
+        static_assert(STAGES >= 4, "four stage owners need a ring of at least four stages");
+        const int own = warp & 3, half = warp >> 2;
+        constexpr int ROWS = SLOTS / 2;          // slot rows per warp and owned stage (32 / 16)
+        constexpr int CPR = TF ? 2 : 1;          // 512-B copies per slot row (token halves for tf32)
+        constexpr int NCOPY = ROWS * CPR;        // 32 copies per warp and owned stage
+        static_assert(NCOPY == 32, "32 copies per warp and owned stage");
         const uint8_t* wsrc = p.base + static_cast<int64_t>(ti.z) * 1024;
-        const int* ssrc = reinterpret_cast<const int*>(p.base + p.slots_off) + ti.y + warp * RPW + (lane % RPW);
-        // per-lane constants: source = A^T row base + E (m0 + token) bytes (row k of A^T is a zero
-        // row, the padding slots' source); destination = stage + this lane's (atom, swizzled chunk)
-        // of each of the warp's rows.  Eight 512-B copies per warp and stage:
-        //   bf16: copy i = slot row i (NT <= 256 tokens), lane -> tokens [8 lane, +8): atom lane / 8,
-        //         16-B chunk lane % 8 ^ (row % 8 = i);
-        //   tf32: copy i = slot row i / 2, token half i % 2 (NT <= 256 tokens = 2 x 512 B), lane ->
-        //         tokens 128 (i % 2) + [4 lane, +4): atom 4 (i % 2) + lane / 8, 32-B chunk
-        //         (lane % 8) / 2 ^ (row % 4 = i / 2), 16-B half lane % 2.
-        // The row's swizzle phase equals its index inside the warp's rows, so every XOR is static.
-        static_assert(SLOTS * EL::E == 128, "eight 512-B copies per warp and stage");
-        constexpr int NCOPY = 8, CPR = NCOPY / RPW;  // copies per slot row
+        // this lane's slot row (lane < ROWS) of each owned stage: slot list + stage * SLOTS + half * ROWS + lane
+        const int* ssrc = reinterpret_cast<const int*>(p.base + p.slots_off) + ti.y + half * ROWS + (lane % ROWS);
+        // per-lane source (A^T + E (m0 + token)) and destination constants; the destination of copy i
+        // is dbase[i % 8] + (i / 8) * 8 rows (bf16) or dbase[i % 8] + (i / 8) * 4 rows (tf32)
         const char* src_c[CPR];
         uint32_t srcsz_c[CPR];
         bool on_c[CPR];
@@ -350,38 +353,41 @@ __global__ void __launch_bounds__(THREADS, 1)
             src_c[h2] = static_cast<const char*>(At) + EL::E * static_cast<int64_t>(ok ? m0 + tl : 0);
         }
         const uint32_t pitch = static_cast<uint32_t>(p.mp) * EL::E;
-        uint32_t dl[NCOPY];
+        uint32_t dl[8];
 #pragma unroll
-        for (int i = 0; i < NCOPY; ++i) {
-            if (TF) {
-                const uint32_t j = i / CPR, h2 = i % CPR;
-                dl[i] = static_cast<uint32_t>((4 * h2 + (lane >> 3)) * (SLOTS * 128) + (warp * RPW + j) * 128) +
+        for (int i = 0; i < 8; ++i) {
+            if (TF) {  // copy i: row half * 16 + i / 2, token half i % 2; swizzle phase row % 4 = (i / 2) % 4
+                const uint32_t j = i / 2, h2 = i % 2;
+                dl[i] = static_cast<uint32_t>((4 * h2 + (lane >> 3)) * (SLOTS * 128) + (half * ROWS + j) * 128) +
                         (((static_cast<uint32_t>(lane & 7) >> 1) ^ j) << 5) + ((static_cast<uint32_t>(lane) & 1u) << 4);
-            } else {
-                dl[i] = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128) + (warp * RPW + i) * 128) +
+            } else {   // copy i: row half * 32 + i; swizzle phase row % 8 = i % 8
+                dl[i] = static_cast<uint32_t>((lane >> 3) * (SLOTS * 128) + (half * ROWS + i) * 128) +
                         ((static_cast<uint32_t>(lane & 7) ^ static_cast<uint32_t>(i)) << 4);
             }
         }
-        // slot rows are prefetched PF stages ahead in rotating registers (loop unrolled by PF): a
-        // register is reloaded only after PF iterations, so the load latency (~1-2k clk under load)
-        // is not paid per stage -- at PF = 4 it was, and it paced the whole pipeline
-        constexpr int PF = 16;
-
+        constexpr uint32_t DSTEP = TF ? 4 * 128 : 8 * 128;  // 8 copies further = 4 (tf32) / 8 (bf16) rows
+        // slot rows of the next owned stages prefetched in a 4-deep register ring (loop unrolled by
+        // 4): a register is consumed 4 owned stages (16 stages) after its load was issued
+        constexpr int PF = 4;
         int kq[PF];
 #pragma unroll
-        for (int u = 0; u < PF; ++u) kq[u] = u < nst ? ssrc[(sa + u) * SLOTS] : 0;
-        for (int st0 = 0; st0 < nst; st0 += PF) {
+        for (int u = 0; u < PF; ++u) {
+            const int st = own + 4 * u;
+            kq[u] = st < nst ? ssrc[(sa + st) * SLOTS] : 0;
+        }
+        for (int v0 = 0; own + 4 * v0 < nst; v0 += PF) {
 #pragma unroll
             for (int u = 0; u < PF; ++u) {
-                const int st = st0 + u;  // local stage (global stage sa + st)
+                const int st = own + 4 * (v0 + u);  // local stage (global stage sa + st)
                 if (st >= nst) break;
                 const int s = st % STAGES;
                 const uint32_t off = static_cast<uint32_t>(kq[u]) * pitch;  // byte offset of this lane's row
-                if (st + PF < nst) kq[u] = ssrc[(sa + st + PF) * SLOTS];
-                if (warp == 0) SP_TS(st, 0);
+                {
+                    const int stn = st + 4 * PF;
+                    if (stn < nst) kq[u] = ssrc[(sa + stn) * SLOTS];
+                }
                 if (st >= STAGES) mbar_wait(&empty[s], ((st / STAGES) - 1) & 1);
-                if (warp == 0) SP_TS(st, 1);
-                if (warp == 0 && lane == 0) {
+                if (half == 0 && lane == 0) {
                     if (p.dbg & 16) {
                         mbar_arrive(&full[s]);
                     } else {
@@ -401,13 +407,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NCOPY; ++i) {
                         const uint32_t o = __shfl_sync(0xffffffffu, off, i / CPR);
-                        cp_async16_pred(bstage + dl[i], src_c[i % CPR] + o, srcsz_c[i % CPR], on_c[i % CPR]);
+                        cp_async16_pred(bstage + dl[i % 8] + (i / 8) * DSTEP, src_c[i % CPR] + o, srcsz_c[i % CPR],
+                                        on_c[i % CPR]);
                     }
                 }
                 // arrives on full[s] once this thread's copies have landed (counts as one of the
-                // barrier's expected arrivals: 32 x GATHER_WARPS + 1)
+                // barrier's expected arrivals: 2 x 32 + 1)
                 cp_async_arrive_noinc(&full[s]);
-                if (warp == 0) SP_TS(st, 2);
             }
         }
     } else if (warp == MMA_WARP) {

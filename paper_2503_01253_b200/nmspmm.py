@@ -28,7 +28,8 @@ EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_
            "nm_spmm", "nm_spmm_host_ws_bytes", "nm_spmm_host", "nm_plan_query", "nm_unshard_columns",
            "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked",
            "nm_prepack_bytes_ex", "nm_prepack_ex", "nm_ipc_get_handle", "nm_ipc_open_handle", "nm_ipc_close",
-           "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled", "nm_prepack_size"]
+           "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled", "nm_prepack_size",
+           "nm_index_packed_words", "nm_index_pack", "nm_index_unpack"]
 
 
 class NmError(RuntimeError):
@@ -91,6 +92,10 @@ def lib():
         L.nm_prepack_bytes_ex.restype = I64
         L.nm_prepack_ex.argtypes = [P, P, I64, I64, I, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
         L.nm_prepack_size.argtypes = [P, P, I64, I64, I, I, I, I, I, ctypes.POINTER(I64), P]
+        L.nm_index_packed_words.argtypes = [I64, I64, I, I, I]
+        L.nm_index_packed_words.restype = I64
+        L.nm_index_pack.argtypes = [P, I64, I64, I, I, I, P, P]
+        L.nm_index_unpack.argtypes = [P, I64, I64, I, I, I, P, P]
         L.nm_profile_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64), ctypes.POINTER(I64)]
         L.nm_ipc_get_handle.argtypes = [P, P, ctypes.POINTER(I64)]
         L.nm_ipc_open_handle.argtypes = [P, I64, ctypes.POINTER(P)]
@@ -100,7 +105,7 @@ def lib():
         L.nm_spmm_prepacked_peers.argtypes = [P, ctypes.POINTER(Prepacked), ctypes.POINTER(P), I, I64, I64, I64, I64, I,
                                               P]
         for name in EXPORTS[2:]:
-            if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes", "nm_prepack_bytes_ex"):
+            if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes", "nm_prepack_bytes_ex", "nm_index_packed_words"):
                 getattr(L, name).restype = I
         _lib = L
     return _lib
@@ -324,6 +329,26 @@ def nm_unshard_columns(src: torch.Tensor, dst: torch.Tensor, G: int, m: int, nr:
     _check(lib().nm_unshard_columns(src.data_ptr(), dst.data_ptr(), G, m, nr, n, L, src.element_size(),
                                     _stream(src, stream)), "nm_unshard_columns")
     return dst
+
+
+# ----------------------------------------------------------------------------- bit-packed indices
+def nm_index_pack(idx: torch.Tensor, k: int, n: int, N: int, M: int, L: int, stream=None) -> torch.Tensor:
+    """D (w x q uint8) -> ceil(log2 M)-bit tile-major words (P:288, P:419 transformLayout)."""
+    _dev(idx, "idx")
+    nw = lib().nm_index_packed_words(k, n, N, M, L)
+    if nw < 0:
+        raise NmError(5, "nm_index_pack", "needs 128 % L == 0 and a valid shape")
+    out = torch.empty(max(int(nw), 1), dtype=torch.int32, device=idx.device)
+    _check(lib().nm_index_pack(idx.data_ptr(), k, n, N, M, L, out.data_ptr(), _stream(idx, stream)), "nm_index_pack")
+    return out[:int(nw)]
+
+
+def nm_index_unpack(words: torch.Tensor, k: int, n: int, N: int, M: int, L: int, stream=None) -> torch.Tensor:
+    _dev(words, "words")
+    out = torch.empty((k // M * N, n // L), dtype=torch.uint8, device=words.device)
+    _check(lib().nm_index_unpack(words.data_ptr(), k, n, N, M, L, out.data_ptr(), _stream(words, stream)),
+           "nm_index_unpack")
+    return out
 
 
 # ----------------------------------------------------------------------------- fused peer exchange

@@ -23,12 +23,13 @@ import torch
 import torch.distributed as dist
 
 
-def host_staged_all_gather(out: torch.Tensor, inp: torch.Tensor, group=None):
+def host_staged_all_gather(out: torch.Tensor, inp: torch.Tensor, group=None, async_op=False):
     """all_gather_into_tensor through host memory (for backends without device collectives, e.g.
-    gloo): out[r] = rank r's inp."""
+    gloo): out[r] = rank r's inp.  Synchronous (returns no work handle)."""
     parts = [torch.empty(inp.shape, dtype=inp.dtype) for _ in range(dist.get_world_size(group))]
     dist.all_gather(parts, inp.cpu(), group=group)
     out.copy_(torch.stack(parts))
+    return None
 
 
 def shard_ranges(q: int, G: int):
@@ -96,7 +97,7 @@ class ShardedNmLinear:
     (all-gather + unshard kernel) or "p2p" (fused peer-store epilogue: fp32 SIMT kernel, or the bf16
     sparse-tensor-core kernel's direct-store epilogue)."""
 
-    def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl", all_gather=None):
+    def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl", all_gather=None, chunks: int = 1):
         from . import nmspmm
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' or 'p2p'")
@@ -113,7 +114,11 @@ class ShardedNmLinear:
         # exchange="nccl": the collective that fills [G][m][nr] from every rank's [m][nr] block
         # (default torch.distributed.all_gather_into_tensor over the group, i.e. NCCL on GPUs;
         # injectable so the same branch runs with other backends, e.g. gloo with host staging)
-        self.all_gather = all_gather or (lambda out, inp, group: dist.all_gather_into_tensor(out, inp, group=group))
+        self.all_gather = all_gather or (lambda out, inp, group, async_op=False: dist.all_gather_into_tensor(
+            out, inp, group=group, async_op=async_op))
+        # exchange="nccl" with chunks > 1: the rows of A go in `chunks` slices; the
+        # all-gather of slice c runs asynchronously (NCCL's stream) while slice c + 1 is computed
+        self.chunks = max(1, int(chunks))
         self.peers = None
         q = n // local_weight.L
         g0, g1 = shard_ranges(q, self.G)[self.rank]
@@ -126,7 +131,8 @@ class ShardedNmLinear:
                              "(L in {16, 32, 64, 128}); use exchange='nccl'")
 
     @classmethod
-    def from_dense(cls, B: torch.Tensor, N: int, M: int, L: int, group=None, exchange: str = "nccl", all_gather=None):
+    def from_dense(cls, B: torch.Tensor, N: int, M: int, L: int, group=None, exchange: str = "nccl", all_gather=None,
+                   chunks: int = 1):
         """Compress only this rank's columns (compression is per column group, so
         the shard of compress(B) equals compress of the shard)."""
         from . import nmspmm
@@ -139,7 +145,7 @@ class ShardedNmLinear:
         Bs[:, :(g1 - g0) * L] = B[:, g0 * L:g1 * L]
         # padding groups are all-zero: compress gives zero values and the pattern 0..N-1
         W = nmspmm.nm_compress(Bs.contiguous(), N, M, L)
-        return cls(W, n, group, exchange, all_gather)
+        return cls(W, n, group, exchange, all_gather, chunks)
 
     def local(self, A: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         from . import nmspmm
@@ -169,11 +175,21 @@ class ShardedNmLinear:
         if self.exchange == "p2p":
             return self._call_p2p(A)
         m = A.shape[0]
-        c_local = self.local(A)
         if self.G == 1 and self.nr == self.n:  # a single shard is already C (no exchange step)
-            return c_local
-        gathered = torch.empty((self.G, m, self.nr), dtype=c_local.dtype, device=A.device)
-        self.all_gather(gathered, c_local, self.group)
-        C = torch.empty((m, self.n), dtype=c_local.dtype, device=A.device)
-        nmspmm.nm_unshard_columns(gathered, C, self.G, m, self.nr, self.n, self.W.L)
+            return self.local(A)
+        # row slices of 128-multiples; slice c's all-gather overlaps slice c+1's SpMM
+        nch = min(self.chunks, max(1, m // 128))
+        rc = -(-m // nch)
+        rc = -(-rc // 128) * 128 if nch > 1 else m
+        pending = []
+        for r0 in range(0, m, rc):
+            r1 = min(m, r0 + rc)
+            c_local = self.local(A[r0:r1])
+            gathered = torch.empty((self.G, r1 - r0, self.nr), dtype=c_local.dtype, device=A.device)
+            pending.append((self.all_gather(gathered, c_local, self.group, async_op=nch > 1), gathered, r0, r1))
+        C = torch.empty((m, self.n), dtype=pending[0][1].dtype, device=A.device)
+        for work, gathered, r0, r1 in pending:
+            if work is not None:
+                work.wait()  # the current stream waits for this slice's collective
+            nmspmm.nm_unshard_columns(gathered, C[r0:r1], self.G, r1 - r0, self.nr, self.n, self.W.L)
         return C

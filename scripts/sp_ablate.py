@@ -15,7 +15,8 @@ flops = 2.0 * m * n * (k // M * N)
 names = {0: "full", 1: "no gather", 2: "no MMA", 3: "no gather, no MMA", 8: "no C stores",
          11: "no gather/MMA/stores", 16: "no weights", 27: "sync skeleton", 155: "skeleton, arrive not commit",
          131: "no gather/MMA, arrive", 19: "no gather/MMA/weights", 147: "no g/MMA/w, arrive",
-         283: "skeleton, warp arrivals", 411: "skel, warp arr, plain empty"}
+         283: "skeleton, warp arrivals", 411: "skel, warp arr, plain empty", 17: "MMA only (no gather/weights)",
+         512: "no stages (fixed costs)", 18: "no MMA, no weights", 9: "no gather, no C stores"}
 lib = nmspmm.lib()
 import ctypes
 for dbg in [int(x) for x in os.environ.get('SP_DBGS', '0 1 2 3 8 11 16 27 155 131').split()]:

@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(288, 1) kern(int layout, int ST, int cp, int i
     extern __shared__ __align__(1024) uint8_t buf[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NPW = layout == 0 ? 8 : layout == 3 ? 4 : 1;  // warps sharing one stage
+    const int OWN = layout == 2 ? 8 : layout == 4 ? 4 : layout == 5 ? 2 : 1;  // stage-owning warps (round robin)
     const int CPL = 64 / NPW;                                  // 512-B rows per warp and stage
     if (threadIdx.x == 0) {
         for (int s = 0; s < ST; ++s) {
@@ -45,9 +46,9 @@ __global__ void __launch_bounds__(288, 1) kern(int layout, int ST, int cp, int i
     }
     __syncthreads();
     long long t0 = clock64();
-    const bool producer = layout == 0 ? warp < 8 : layout == 1 ? warp == 0 : layout == 2 ? warp < 8 : warp < 4;
+    const bool producer = layout == 0 ? warp < 8 : layout == 1 ? warp == 0 : layout == 3 ? warp < 4 : warp < OWN;
     if (producer) {
-        const int first = layout == 2 ? warp : 0, step = layout == 2 ? 8 : 1;
+        const int first = OWN > 1 ? warp : 0, step = OWN;
         const int part = (layout == 0 || layout == 3) ? warp : 0;
         for (int st = first; st < iters; st += step) {
             const int s = st % ST;

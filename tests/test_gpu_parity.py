@@ -385,16 +385,46 @@ def test_spmm_tc_prepacked_integer_exact(nm, oracle, monkeypatch, m, n, k, N, M,
     assert np.array_equal(C, C2)
 
 
-def test_spmm_prepacked_fp32_plain(nm, oracle):
-    m, n, k, N, M, L = 200, 256, 256, 8, 32, 32
+@pytest.mark.parametrize("L,kind", [(32, 4), (12, 0)])
+def test_spmm_prepacked_fp32(nm, oracle, L, kind):
+    """fp32 prepack: kind 4 (SIMT on bit-packed tile-major indices) when 128 % L == 0, else kind 0;
+    the same bits as nm_spmm either way (the indices are the only difference)."""
+    m, n, k, N, M = 200, 24 * L, 256, 8, 32
     A = synth.uniform((m, k), 91, 1)
     B = synth.uniform((k, n), 92, 2)
     vals, D = oracle.compress(B, N, M, L)
     W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
     PW = nm.nm_prepack(W)
-    assert PW.kind == 0
+    assert PW.kind == kind
+    C = nm.nm_spmm_prepacked(dev(A), PW)
+    assert oracle.rel_frobenius(C.cpu().numpy(), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
+    assert torch.equal(C, nm.nm_spmm(dev(A), W))
+
+
+@pytest.mark.parametrize("N,M,L", [(2, 4, 4), (16, 32, 32), (4, 32, 8), (3, 8, 16), (1, 2, 64), (5, 64, 128),
+                                   (12, 32, 32), (7, 100, 4), (60, 256, 32)])
+def test_index_pack_bit_exact(nm, oracle, N, M, L):
+    """nm_index_pack == the oracle's index_pack word for word (ragged last tile included);
+    nm_index_unpack inverts it."""
+    k, n = 8 * M, 128 * 3 + 2 * L
+    _, D = oracle.compress(synth.uniform((k, n), 33, synth.TID_B), N, M, L)
+    words = nm.nm_index_pack(dev(D, torch.uint8), k, n, N, M, L)
+    torch.cuda.synchronize()
+    assert np.array_equal(words.cpu().numpy().view(np.uint32), oracle.index_pack(D, k, n, N, M, L))
+    assert np.array_equal(nm.nm_index_unpack(words, k, n, N, M, L).cpu().numpy(), D)
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", [(300, 384, 512, 16, 32, 32), (257, 640, 1024, 4, 32, 32),
+                                         (130, 256, 256, 2, 4, 4), (512, 1024, 2048, 8, 16, 16)])
+def test_spmm_prepacked_packed_indices_integer_exact(nm, oracle, m, n, k, N, M, L):
+    """kind 4: integer inputs, bit-exact vs the oracle through the packed-index loads."""
+    A = synth.integer((m, k), 95, 1)
+    vals, D = oracle.compress(synth.integer((k, n), 96, 2), N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    PW = nm.nm_prepack(W)
+    assert PW.kind == 4
     C = nm.nm_spmm_prepacked(dev(A), PW).cpu().numpy()
-    assert oracle.rel_frobenius(C, oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L))
 
 
 # --------------------------------------------------------------- sparse-tensor-core slot path edge cases
@@ -543,7 +573,7 @@ def test_spmm_tc_tf32_prepacked(nm, oracle, m, n, k, N, M, L):
     assert torch.equal(C, nm.nm_spmm(dev(A), W, math="tf32_tc"))
     ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)
     assert oracle.rel_frobenius(C.cpu().numpy(), ref) <= TOL_BF16
-    assert nm.nm_prepack(W).kind == 0  # AUTO on fp32 keeps the SIMT path
+    assert nm.nm_prepack(W).kind == 4  # AUTO on fp32 keeps the SIMT path (with packed indices)
 
 
 @pytest.mark.parametrize("dt", ["bf16", "tf32"])

@@ -31,13 +31,13 @@ def _worker(rank, world, port, case, errs):
         from oracle import oracle
         from paper_2503_01253_b200 import synth
         from paper_2503_01253_b200.sharded import ShardedNmLinear, host_staged_all_gather
-        m, n, k, N, M, L, dt, kind = case
+        m, n, k, N, M, L, dt, kind, chunks = case
         gen = synth.integer if kind == "integer" else (synth.uniform if dt == "f32" else synth.bf16grid)
         A = gen((m, k), 11, synth.TID_A)
         B = gen((k, n), 12, synth.TID_B)
         tdt = torch.float32 if dt == "f32" else torch.bfloat16
         layer = ShardedNmLinear.from_dense(torch.from_numpy(B).cuda().to(tdt), N, M, L,
-                                           all_gather=host_staged_all_gather)
+                                           all_gather=host_staged_all_gather, chunks=chunks)
         C = layer(torch.from_numpy(A).cuda().to(tdt)).float().cpu().numpy().astype(np.float64)
         Bo = B if dt == "f32" else synth.to_bf16_bits(B)
         Ao = A if dt == "f32" else synth.to_bf16_bits(A)
@@ -58,10 +58,12 @@ def _worker(rank, world, port, case, errs):
 
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("case", [
-    (256, 11 * 32, 512, 16, 32, 32, "f32", "uniform"),   # 11 groups: uneven shards, padding
-    (200, 8 * 32, 256, 8, 32, 32, "f32", "integer"),     # bit-exact through the exchange
-    (300, 12 * 32, 512, 12, 32, 32, "bf16", "uniform"),  # slot kernel (prepacked) shards
-    (128, 9 * 16, 256, 4, 16, 16, "bf16", "uniform"),
+    (256, 11 * 32, 512, 16, 32, 32, "f32", "uniform", 1),   # 11 groups: uneven shards, padding
+    (200, 8 * 32, 256, 8, 32, 32, "f32", "integer", 1),     # bit-exact through the exchange
+    (300, 12 * 32, 512, 12, 32, 32, "bf16", "uniform", 1),  # slot kernel (prepacked) shards
+    (128, 9 * 16, 256, 4, 16, 16, "bf16", "uniform", 1),
+    (700, 10 * 32, 512, 8, 32, 32, "f32", "integer", 3),    # row slices (overlapped exchange), ragged
+    (520, 12 * 32, 512, 12, 32, 32, "bf16", "uniform", 4),
 ])
 def test_sharded_nccl_branch_multi_rank_one_gpu(world, case):
     ctx = mp.get_context("spawn")
