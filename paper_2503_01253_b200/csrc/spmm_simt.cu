@@ -176,13 +176,14 @@ __global__ void __launch_bounds__(THREADS, 2)
     // D_s -> byte offsets koff[buf][u][slot] (index prefetch).  The (u, slot)
     // entries a thread handles, their D offsets and window bases are panel-invariant
     // (panels hold whole windows: (u0 + u) / N - t0 == u / N), so they are computed once.
-    int dreg[D_PER_THREAD], d_us[D_PER_THREAD], d_wb[D_PER_THREAD];  // d_us = u << 8 | slot (or -1)
+    // d_us = window base << 16 | u << 8 | slot (or -1): one register per entry (register pressure:
+    // the fragment double buffer of the inner loop needs the room)
+    int dreg[D_PER_THREAD], d_us[D_PER_THREAD];
 #pragma unroll
     for (int r = 0; r < D_PER_THREAD; ++r) {
         const int e = tid + r * THREADS;
         const int u = e / nslots, sl = e - u * nslots;
-        d_us[r] = (u < p.bkw && sl < nslots) ? (u << 8 | sl) : -1;
-        d_wb[r] = (u / p.N) * p.M;
+        d_us[r] = (u < p.bkw && sl < nslots) ? ((u / p.N) * p.M << 16 | u << 8 | sl) : -1;
     }
     // the valid entries are a prefix r < nd (e grows with r): the per-panel index loops stop
     // there -- at L >= 32 a panel has only BKW x (BN/L + 1) entries, most threads 0 or 1
@@ -197,7 +198,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
             for (int r = 0; r < D_PER_THREAD; ++r) {
                 if (r >= nd) break;
-                const int u = d_us[r] >> 8, sl = d_us[r] & 255;
+                const int u = (d_us[r] >> 8) & 255, sl = d_us[r] & 255;
                 const int64_t x = static_cast<int64_t>(u0 + u) * p.dT + sl;
                 dreg[r] = (u < ulim) ? static_cast<int>((__ldg(Dt + x / p.de) >> ((x % p.de) * p.db)) & mask) : 0;
             }
@@ -207,7 +208,7 @@ __global__ void __launch_bounds__(THREADS, 2)
 #pragma unroll
         for (int r = 0; r < D_PER_THREAD; ++r) {
             if (r >= nd) break;
-            const int u = d_us[r] >> 8, sl = d_us[r] & 255;
+            const int u = (d_us[r] >> 8) & 255, sl = d_us[r] & 255;
             dreg[r] = (u < ulim) ? Dp[u * p.q + sl] : 0;
         }
     };
@@ -218,9 +219,9 @@ __global__ void __launch_bounds__(THREADS, 2)
         for (int r = 0; r < D_PER_THREAD; ++r) {
             if (r >= nd) break;
             {
-                const int kk = d_wb[r] + dreg[r];  // dense column inside the panel
+                const int kk = (d_us[r] >> 16) + dreg[r];  // dense column inside the panel
                 const int row = PK ? __popcll(mk & ((1ull << kk) - 1ull)) : kk;  // packed position
-                kb[(d_us[r] >> 8) * MAX_SLOTS + (d_us[r] & 255)] = AT ? row * (BM * 4) : a_col_offset(kk);
+                kb[((d_us[r] >> 8) & 255) * MAX_SLOTS + (d_us[r] & 255)] = AT ? row * (BM * 4) : a_col_offset(kk);
             }
         }
     };
@@ -256,52 +257,54 @@ __global__ void __launch_bounds__(THREADS, 2)
         const float* bS = reinterpret_cast<const float*>(sB + s * B_STAGE_BYTES) + col0;
         const int* kS = koff + (rel & 1) * (BKW * MAX_SLOTS);
 
-        float a0[8], a1[8];
-        float4 b0, b1;
-#pragma unroll 2
-        for (int u = 0; u < bkw; ++u) {
-            const int* krow = kS + u * MAX_SLOTS;
-            const uint8_t* ap0 = aS + (krow[slot0] ^ tmx);
-            b0 = *reinterpret_cast<const float4*>(bS + u * BN);
-            b1 = *reinterpret_cast<const float4*>(bS + u * BN + 16);
+        // software pipeline: the gathered fragment(s) of row u + 1 (index LDS -> fragment LDS) are
+        // loaded while row u's FMAs run, so the index -> gather latency chain is off the FMA path
+        auto ld_frag = [&](const uint8_t* ap, float (&a)[8]) {
             if (AT) {
-                const float4 x0 = *reinterpret_cast<const float4*>(ap0);
-                const float4 x1 = *reinterpret_cast<const float4*>(ap0 + 128);
-                a0[0] = x0.x, a0[1] = x0.y, a0[2] = x0.z, a0[3] = x0.w;
-                a0[4] = x1.x, a0[5] = x1.y, a0[6] = x1.z, a0[7] = x1.w;
+                const float4 x0 = *reinterpret_cast<const float4*>(ap);
+                const float4 x1 = *reinterpret_cast<const float4*>(ap + 128);
+                a[0] = x0.x, a[1] = x0.y, a[2] = x0.z, a[3] = x0.w;
+                a[4] = x1.x, a[5] = x1.y, a[6] = x1.z, a[7] = x1.w;
             } else {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) a0[i] = *reinterpret_cast<const float*>(ap0 + i * 1024);
+                for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const float*>(ap + i * 1024);
             }
-            if (TWO) {
-                const uint8_t* ap1 = aS + (krow[slot1] ^ tmx);
-                if (AT) {
-                    const float4 x0 = *reinterpret_cast<const float4*>(ap1);
-                    const float4 x1 = *reinterpret_cast<const float4*>(ap1 + 128);
-                    a1[0] = x0.x, a1[1] = x0.y, a1[2] = x0.z, a1[3] = x0.w;
-                    a1[4] = x1.x, a1[5] = x1.y, a1[6] = x1.z, a1[7] = x1.w;
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) a1[i] = *reinterpret_cast<const float*>(ap1 + i * 1024);
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < 8; ++i) a1[i] = a0[i];
-            }
-            // the 8 x 8 outer product as 32 paired FMAs (FFMA2, sm_100: two fp32 FMAs with the A
-            // element broadcast, each rounded exactly as fmaf -- the same bits, half the issue slots)
+        };
+        // ping-pong fragment buffers (f*: even rows, g*: odd rows; *1: the second column group when TWO)
+        float fa0[8], fa1[8], ga0[8], ga1[8];
+        auto ld_row = [&](int u, float (&x0)[8], float (&x1)[8]) {
+            const int* krow = kS + u * MAX_SLOTS;
+            ld_frag(aS + (krow[slot0] ^ tmx), x0);
+            if (TWO) ld_frag(aS + (krow[slot1] ^ tmx), x1);
+        };
+        // the 8 x 8 outer product as 32 paired FMAs (FFMA2, sm_100: two fp32 FMAs with the A element
+        // broadcast, each rounded exactly as fmaf -- the same bits, half the issue slots)
+        auto fma_row = [&](int u, const float (&x0)[8], const float (&x1)[8]) {
+            const float4 b0 = *reinterpret_cast<const float4*>(bS + u * BN);
+            const float4 b1 = *reinterpret_cast<const float4*>(bS + u * BN + 16);
             const float2 b01 = make_float2(b0.x, b0.y), b23 = make_float2(b0.z, b0.w);
             const float2 b45 = make_float2(b1.x, b1.y), b67 = make_float2(b1.z, b1.w);
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                const float2 x0 = make_float2(a0[i], a0[i]), x1 = make_float2(a1[i], a1[i]);
+                const float2 y0 = make_float2(x0[i], x0[i]);
+                const float2 y1 = TWO ? make_float2(x1[i], x1[i]) : y0;
                 float2 c;
-                c = __ffma2_rn(x0, b01, make_float2(acc[i][0], acc[i][1])), acc[i][0] = c.x, acc[i][1] = c.y;
-                c = __ffma2_rn(x0, b23, make_float2(acc[i][2], acc[i][3])), acc[i][2] = c.x, acc[i][3] = c.y;
-                c = __ffma2_rn(x1, b45, make_float2(acc[i][4], acc[i][5])), acc[i][4] = c.x, acc[i][5] = c.y;
-                c = __ffma2_rn(x1, b67, make_float2(acc[i][6], acc[i][7])), acc[i][6] = c.x, acc[i][7] = c.y;
+                c = __ffma2_rn(y0, b01, make_float2(acc[i][0], acc[i][1])), acc[i][0] = c.x, acc[i][1] = c.y;
+                c = __ffma2_rn(y0, b23, make_float2(acc[i][2], acc[i][3])), acc[i][2] = c.x, acc[i][3] = c.y;
+                c = __ffma2_rn(y1, b45, make_float2(acc[i][4], acc[i][5])), acc[i][4] = c.x, acc[i][5] = c.y;
+                c = __ffma2_rn(y1, b67, make_float2(acc[i][6], acc[i][7])), acc[i][6] = c.x, acc[i][7] = c.y;
             }
+        };
+        ld_row(0, fa0, fa1);
+        int u = 0;
+#pragma unroll 1
+        for (; u + 1 < bkw; u += 2) {
+            ld_row(u + 1, ga0, ga1);
+            fma_row(u, fa0, fa1);
+            ld_row(min(u + 2, bkw - 1), fa0, fa1);  // the last pair reloads a valid row (unused)
+            fma_row(u + 1, ga0, ga1);
         }
+        if (u < bkw) fma_row(u, fa0, fa1);  // odd row count (odd N)
         if (panel + 1 < p_end) store_d(panel + 1);
         __syncthreads();
     }
