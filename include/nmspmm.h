@@ -73,6 +73,10 @@ typedef struct {
     double t_compute_us;  /* roofline estimates from the peaks passed in (or built-in nominal)   */
     double t_memory_us;
     int32_t bound;        /* 0 = compute (FMA or tensor), 1 = HBM                               */
+    int32_t split;        /* k-range parts per tile of the split tiles (the partial last wave, or  */
+                          /* every tile of a sub-wave grid); 1 = none                           */
+    int32_t split_tiles;  /* tiles run as `split` CTAs each                                    */
+    double waves;         /* CTAs launched / resident CTA slots (selector's wave model)          */
 } nm_plan;
 
 /* Library version string, e.g. "nmspmm 0.1 sm_100a". */

@@ -232,6 +232,7 @@ nm_status index_pack_launch(const uint8_t* D, uint32_t* P, int64_t k, int64_t n,
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
+int simt_split_factor(int ntiles, int64_t w, int npanels);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
                           float alpha = 1.f, const uint32_t* Dw = nullptr);
@@ -652,7 +653,14 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->bkw = bkw;
         out->stages = 2;
         out->threads = 256;
-        out->grid = static_cast<int32_t>(ceil_div(m, 128) * ceil_div(n, 128));
+        const int64_t tiles = ceil_div(m, 128) * ceil_div(n, 128);
+        const int npanels = static_cast<int>(ceil_div(k / M, wp));
+        const int sp = simt_split_factor(static_cast<int>(tiles), w, npanels);
+        const int64_t resident = 2 * static_cast<int64_t>(sms);
+        out->split = sp;
+        out->split_tiles = sp > 1 ? static_cast<int32_t>(tiles % resident) : 0;
+        out->grid = static_cast<int32_t>(tiles - out->split_tiles + out->split_tiles * static_cast<int64_t>(sp));
+        out->waves = double(out->grid) / double(resident);
         out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
     } else if (kernel == K_TC_SP || kernel == K_TC_TF32) {
         // tokens x output columns per CTA (MMA N x M per column half), 64 (bf16) / 32 (tf32) slots

@@ -17,6 +17,7 @@
 // tile 8 rows x 8 columns (two 4-column chunks 16 apart).  A panel: WP whole
 // windows (BK = WP*M <= 64 dense k, never straddling a window), i.e.
 // BKW = WP*N <= 32 compressed rows.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -478,6 +479,40 @@ static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, con
     return NM_OK;
 }
 
+// Split factor of the SIMT kernel's tile schedule (the selector's wave model): the
+// tiles of a partial last wave (multi-wave grids) or of a sub-wave grid (small problems, column
+// shards of a multi-GPU layer) run as S CTAs each over S k-ranges, partials added in a fixed
+// order by the last arriver.  R = 2 x SMs resident CTAs; with 2 CTAs on an SM each runs at about
+// 0.6x the speed of a lone CTA, so a split pays only when it leaves the split CTAs alone on their
+// SMs (or nearly) and each part keeps enough rows to amortise its fixed cost:
+//   * multi-wave, rem = tiles mod R with 0 < 2 rem <= SMs: S = min(3, SMs / rem);
+//   * sub-wave: the largest S <= 4 with tiles x S <= SMs and >= 256 compressed rows per part;
+//     else, when SMs < tiles, S = 2 if the CTAs beyond the first R fit half the SMs and each part
+//     keeps >= 512 rows;
+//   * else 1.
+// Measured on B200 (pipelined kernel, profiles/r02c_simt_streamk.txt table 1) this picks the
+// fastest S of {1, 2, 3, 4} at all 11 shapes timed (BASELINE tails, m = 256, the 8-GPU shards of
+// cfg2 / cfg3 / cfg4, 1024^3 and 2048^3).  NM_SIMT_SPLIT overrides (never for whole waves).
+int simt_split_factor(int ntiles, int64_t w, int npanels) {
+    const int sms = num_sms(), resident = 2 * sms;
+    if (ntiles <= 0 || npanels < 2 || (ntiles >= resident && ntiles % resident == 0)) return 1;
+    const char* e = getenv("NM_SIMT_SPLIT");  // timing studies / tests
+    if (e) return std::max(1, std::min(atoi(e), std::min(4, npanels / 2)));
+    int S = 1;
+    if (ntiles >= resident) {
+        const int rem = ntiles % resident;
+        if (rem > 0 && 2 * rem <= sms) S = std::min(3, sms / rem);
+    } else {
+        for (int c = 4; c >= 2; --c)
+            if (static_cast<int64_t>(ntiles) * c <= sms && w / c >= 256) {
+                S = c;
+                break;
+            }
+        if (S == 1 && ntiles > sms && 2 * ntiles - resident <= sms / 2 && w / 2 >= 512) S = 2;
+    }
+    return std::min(S, std::max(1, npanels / 2));
+}
+
 // mode: 0 = A panels straight from A (swizzled [m][k] boxes), 1 = A^T staged (tile TMA),
 // 2 = A^T staged + packed col_info loads (high sparsity).  The selector decides.
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
@@ -562,17 +597,7 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     const int ntiles = ntiles_n * static_cast<int>(ceil_div(m, BM));
     const int resident = 2 * num_sms();  // 2 CTAs per SM (launch bounds, ~105 KB smem)
     const int rem = ntiles % resident;
-    // Measured on B200 (cfg2-cfg4): splitting the partial wave of a multi-wave grid gains
-    // nothing -- CTAs do not retire in lock-step waves -- so it is off there unless
-    // NM_SIMT_SPLIT asks for it.  A grid below one wave (e.g. a column shard of a multi-GPU
-    // layer) is split so that it fills the resident CTA slots (up to 4 parts per tile).
-    int split = 1;
-    const char* env_split = getenv("NM_SIMT_SPLIT");
-    if (env_split) split = atoi(env_split);
-    else if (ntiles < resident) split = resident / ntiles;
-    split = split > 4 ? 4 : split;
-    if (split > p.npanels / 2) split = p.npanels / 2;
-    if (split < 2) split = 1;
+    const int split = simt_split_factor(ntiles, w, p.npanels);
     p.split = split;
     p.full_tiles = split > 1 ? ntiles - rem : ntiles;
     float* ws = nullptr;

@@ -15,7 +15,8 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnmspmm.so")
+# NM_LIB_PATH: an alternative build of the same library (A/B timing studies in scripts/ only)
+LIB_PATH = os.environ.get("NM_LIB_PATH") or os.path.join(_PKG, "libnmspmm.so")
 
 NM_OK = 0
 STATUS = {0: "NM_OK", 1: "NM_ERR_INVALID_CONFIG", 2: "NM_ERR_SHAPE", 3: "NM_ERR_ALIGNMENT",
@@ -52,7 +53,8 @@ class Plan(ctypes.Structure):
                 ("bn", ctypes.c_int32), ("bk", ctypes.c_int32), ("bkw", ctypes.c_int32),
                 ("stages", ctypes.c_int32), ("grid", ctypes.c_int32), ("threads", ctypes.c_int32),
                 ("smem_bytes", ctypes.c_int32), ("flops", ctypes.c_double), ("bytes", ctypes.c_double),
-                ("t_compute_us", ctypes.c_double), ("t_memory_us", ctypes.c_double), ("bound", ctypes.c_int32)]
+                ("t_compute_us", ctypes.c_double), ("t_memory_us", ctypes.c_double), ("bound", ctypes.c_int32),
+                ("split", ctypes.c_int32), ("split_tiles", ctypes.c_int32), ("waves", ctypes.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

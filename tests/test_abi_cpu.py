@@ -101,3 +101,35 @@ def test_plan_query_model(L):
     assert p["bound"] == 0  # FMA-bound
     q = nmspmm.nm_plan_query(256, 255, 256, 2, 4, 3, torch.float32)
     assert q["kernel"] == 0  # L % 4 != 0 -> generic
+
+
+# The SIMT kernel's split choice (nm_plan_query.split, simt_split_factor) pinned to the fastest
+# split factor measured on B200 for each shape (profiles/r02c_simt_streamk.txt, table 1: kernel
+# time under NM_SIMT_SPLIT = 1..4; 148 SMs, 296 resident CTAs).
+SPLIT_MEASURED = [
+    # (m, n, k, N, M, L), fastest S, why
+    ((2048, 5120, 5120, 4, 32, 32), 3),    # 640 tiles: a 48-tile tail -> 144 lone CTAs
+    ((256, 22016, 8192, 4, 32, 32), 3),    # 344 tiles: 48-tile tail
+    ((2048, 2752, 8192, 4, 32, 32), 2),    # cfg4-65B 8-GPU shard, 352 tiles: 56-tile tail
+    ((2048, 13824, 5120, 4, 32, 32), 1),   # 1728 tiles: 248-tile tail is most of a wave
+    ((4096, 4096, 4096, 16, 32, 32), 1),   # cfg2: 1024 tiles, 136-tile tail
+    ((256, 13824, 5120, 4, 32, 32), 1),    # 216 tiles, sub-wave: a split would double up SMs
+    ((4096, 512, 4096, 16, 32, 32), 1),    # cfg2 8-GPU shard: 128 tiles, one per SM already
+    ((2048, 1376, 4096, 8, 32, 32), 2),    # cfg3-75% 8-GPU shard: 176 tiles -> 296 + 56 lone
+    ((1024, 1024, 1024, 16, 32, 32), 2),   # 64 tiles x 2 = 128 lone CTAs, 256 rows each
+    ((1024, 1024, 1024, 4, 32, 32), 1),    # 64 tiles, 128 rows: too short to split
+    ((2048, 2048, 2048, 16, 32, 32), 1),   # 256 tiles, sub-wave
+]
+
+
+@pytest.mark.parametrize("cfg,best", SPLIT_MEASURED)
+def test_plan_simt_split_matches_measured_best(L, cfg, best):
+    from paper_2503_01253_b200 import nmspmm
+    import torch
+    p = nmspmm.nm_plan_query(*cfg, torch.float32)
+    assert p["kernel"] == 1
+    assert p["split"] == best, p
+    m, n = cfg[:2]
+    tiles = -(-m // 128) * -(-n // 128)
+    assert p["grid"] == tiles - p["split_tiles"] + p["split_tiles"] * p["split"]
+    assert abs(p["waves"] - p["grid"] / 296) < 1e-9

@@ -350,14 +350,25 @@ def test_spmm_f32_staging_modes(nm, oracle, monkeypatch, mode, m, n, k, N, M, L)
     assert oracle.rel_frobenius(C, oracle.spmm_sparse_f64(A, vals, D, k, N, M, L)) <= TOL_F32
 
 
-@pytest.mark.parametrize("split", ["1", "2", "3", "4"])
-def test_spmm_f32_split_tail(nm, oracle, monkeypatch, split):
-    """Stream-K-lite tail split: every split factor gives the same parity, and results
-    are bit-reproducible run to run (fixed reduction order)."""
-    monkeypatch.setenv("NM_SIMT_SPLIT", split)
-    m, n, k, N, M, L = 4096, 1280, 1024, 16, 32, 32  # 320 tiles > 296 resident -> a partial wave
+SK_CASES = [
+    (4096, 1280, 1024, 16, 32, 32),   # 320 tiles > 296 resident: a 24-tile partial wave
+    (1000, 640, 2048, 8, 32, 32),     # 40 tiles, ragged m: sub-wave grid
+    (384, 384, 4096, 4, 32, 32),      # 9 tiles, long k, 87.5 %
+    (256, 520, 1536, 3, 8, 8),        # odd N (odd row counts), n not a multiple of the tile
+    (300, 256, 512, 2, 4, 4),         # L = 4: two column groups per thread chunk (TWO)
+]
+
+
+@pytest.mark.parametrize("split", ["auto", "1", "2", "3", "4"])
+@pytest.mark.parametrize("m,n,k,N,M,L", SK_CASES)
+def test_spmm_f32_split(nm, oracle, monkeypatch, split, m, n, k, N, M, L):
+    """Split tiles (the partial last wave, or every tile of a sub-wave grid, as S k-range CTAs whose
+    partials the last arriver adds in part order): integer inputs bit-exact for every S, uniform
+    inputs within tolerance, and bit-reproducible run to run (fixed reduction order)."""
+    if split != "auto":
+        monkeypatch.setenv("NM_SIMT_SPLIT", split)
     A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L, kind="integer", seed=5)
-    rows = np.arange(0, m, 97)
+    rows = np.unique(np.concatenate([np.arange(0, m, 37), [m - 1]]))
     ref = oracle.spmm_sparse_f64(A, vals, D, k, N, M, L, rows=rows)
     assert np.array_equal(C[rows].astype(np.float64), ref)
     A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L, seed=6)
