@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     const int stn = st + 4 * PF;
                     if (stn < nst) kq[u] = ssrc[(sa + stn) * SLOTS];
                 }
-                if (st >= STAGES) mbar_wait(&empty[s], ((st / STAGES) - 1) & 1);
+                if (st >= STAGES) mbar_wait_dbg(&empty[s], ((st / STAGES) - 1) & 1, p.dbg, 2048, 8192);
                 if (half == 0 && lane == 0) {
                     if (p.dbg & 16) {
                         mbar_arrive(&full[s]);
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             uint32_t ph = 0;
             for (int st = 0; st < nst; ++st) {
                 const int gs = sa + st;  // stage index in the tile (pairs: 2i, 2i+1)
-                mbar_wait(&full[s], ph);
+                mbar_wait_dbg(&full[s], ph, p.dbg, 1024, 4096);
                 tc_fence_after();
                 if (elect_one()) {
                     if (!skip_mma) {

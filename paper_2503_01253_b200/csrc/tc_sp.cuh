@@ -74,6 +74,29 @@ struct Params {
     int n_units;  // CTA-pair kernel (spmm_tc_sp2.cu): work units = full tiles + split tiles x split
 };
 
+// mbarrier wait variants (timing studies of the stage hand-off, NM_SP_DBG 1024 / 2048 / 4096):
+// try_wait with an explicit suspend-time hint (ns), and a pure test_wait spin
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(ns)
+            : "memory");
+}
+__device__ __forceinline__ void mbar_wait_dbg(uint64_t* bar, uint32_t parity, int dbg, int hint_bit, int spin_bit) {
+    if (dbg & spin_bit) {
+        while (!mbar_test(bar, parity)) {
+        }
+    } else if (dbg & hint_bit) {
+        mbar_wait_hint(bar, parity, 32);
+    } else {
+        mbar_wait(bar, parity);
+    }
+}
+
 // 16-B global -> shared copy (L2 only); src_bytes = 0 zero-fills the destination
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
