@@ -48,7 +48,13 @@ CONFIGS = {
     # m = 256 tokens is the bf16 HBM-bound point of the 87.5 % regime
     "cfg4_65b_m256": (256, 22016, 8192, 4, 32, 32),
     "cfg4_13b_m256": (256, 13824, 5120, 4, 32, 32),
+    # one rank's column shard of the 8-GPU split (ceil(q/8) groups of L): kernel-only
+    # scaling = T_kernel(full) / (8 T_kernel(shard)), reported beside the full config's variant
+    "cfg2_shard8": (4096, 512, 4096, 16, 32, 32),
+    "cfg3_75_shard8": (2048, 1376, 4096, 8, 32, 32),
+    "cfg4_65b_shard8": (2048, 2752, 8192, 4, 32, 32),
 }
+SHARD_OF = {"cfg2_shard8": "cfg2", "cfg3_75_shard8": "cfg3_75", "cfg4_65b_shard8": "cfg4_65b"}
 HEADLINE = "cfg2"
 # one metric string for both arms (the driver pairs the lines by it)
 METRIC = "effective TFLOPS (kept MACs) of C = A . B~, vector-wise N:M"
@@ -56,7 +62,8 @@ VARIANTS = ["cfg1:f32", "cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_13b:f32
             "cfg4_65b_sq:f32", "cfg4_65b:f32", "cfg4_65b_m256:f32", "cfg3_62:bf16", "cfg3_75:bf16",
             "cfg4_13b:bf16", "cfg4_13b_sq:bf16", "cfg4_65b_sq:bf16", "cfg4_65b:bf16", "cfg4_65b_m256:bf16",
             "cfg4_13b_m256:bf16", "cfg2:tf32", "cfg3_62:tf32", "cfg3_75:tf32",
-            "cfg4_65b:tf32"]  # tf32 = fp32 operands on the tf32 sparse tensor cores (opt-in math)
+            "cfg4_65b:tf32", "cfg2_shard8:f32", "cfg3_75_shard8:f32", "cfg4_65b_shard8:f32",
+            "cfg2_shard8:bf16", "cfg3_75_shard8:bf16", "cfg4_65b_shard8:bf16"]  # tf32 = fp32 operands on the tf32 sparse tensor cores (opt-in math)
 
 
 def load_peaks():
@@ -450,7 +457,7 @@ def run_ours(args):
             t_k = r["kernel_ms"] * 1e-3
             variants.append({"config": name, "dtype": vdt, "m_n_k": vcfg[:3], "N:M": f"{vcfg[3]}:{vcfg[4]}",
                              "L": vcfg[5], "tflops": round(r["tflops"], 3), "ms": round(r["ms"], 4),
-                             "kernel_tflops": round(r["kernel_tflops"], 3),
+                             "kernel_tflops": round(r["kernel_tflops"], 3), "kernel_ms": round(r["kernel_ms"], 5),
                              "roofline_frac": round(max(t_c, t_m) / t_k, 4),
                              "roofline_bound": ("hbm" if t_m > t_c else "alu" if vdt == "f32" else "tensor"),
                              "hbm_gbs_achieved": round(alg_bytes(vcfg, e_v) / t_k / 1e9, 1),
@@ -461,6 +468,15 @@ def run_ours(args):
                                 "speedup_vs_cublas_tf32": round(r["speedup_vs_cublas_tf32"], 3)}
                                if "cublas_tf32_dense_tflops" in r else {}))
             torch.cuda.empty_cache()
+        # kernel-only 8-GPU scaling of the column-sharded layer from one GPU: the full config's kernel
+        # time over 8 x one shard's (the all-gather is not included; SURVEY 8(e) reporting (i))
+        kms = {(u["config"], u["dtype"]): u["kernel_ms"] for u in variants}
+        if roof.get("kernel_ms_per_launch"):
+            kms.setdefault((args.config, args.dtype), roof["kernel_ms_per_launch"])
+        for v in variants:
+            full = kms.get((SHARD_OF.get(v["config"]), v["dtype"]))
+            if full:
+                v["kernel_only_scaling_8gpu"] = round(full / (8 * v["kernel_ms"]), 4)
         line["variants"] = variants
     print(json.dumps(line), flush=True)
     return 0

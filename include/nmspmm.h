@@ -157,8 +157,8 @@ nm_status nm_spmm(const void* A, const void* values, const uint8_t* idx, void* C
  * paper's approximation C' of the unpruned product being alpha = M/N (R1 reads the product
  * path unscaled: nm_spmm == nm_spmm_scaled with alpha = 1).  alpha is applied in fp32 to the
  * fp32 accumulators inside the epilogue of the SIMT and sparse-tensor-core kernels (after any
- * split-k / tail-split addition, before the bf16 rounding); the other kernels (generic,
- * pipelined SIMT mode 3) are followed by one in-place scaling pass over C (for a bf16
+ * split-k / tail-split addition, before the bf16 rounding); the generic kernel is followed by
+ * one in-place scaling pass over C (for a bf16
  * C: a second rounding, exact when alpha is a power of two).  Otherwise as nm_spmm.
  */
 nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,

@@ -236,9 +236,6 @@ int simt_split_factor(int ntiles, int64_t w, int npanels);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
                           float alpha = 1.f, const uint32_t* Dw = nullptr);
-bool simt_pipe_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
-nm_status simt_pipe_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                           int N, int M, int L, cudaStream_t s);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 // tf: fp32 operands on the tf32 sparse tensor cores (1:2 slot pairs), else bf16 (2:4 slot quads)
 size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf);  // bound (no data)
@@ -333,10 +330,9 @@ static bool simt_use_at(int64_t m, int64_t n, int64_t k, int N, int M) {
 // NM_SIMT_MODE=0/1/2 overrides (ablation).
 static int simt_mode(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     const char* e = getenv("NM_SIMT_MODE");
-    if (e && e[0] >= '0' && e[0] <= '3') {
+    if (e && e[0] >= '0' && e[0] <= '2') {
         int mode = e[0] - '0';
         if (mode >= 1 && m % 4 != 0) mode = 0;
-        if (mode == 3 && !simt_pipe_applicable(m, n, k, N, M, L)) mode = 1;
         return mode;
     }
     if (!simt_use_at(m, n, k, N, M)) return 0;
@@ -472,19 +468,14 @@ nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, 
     int kernel = K_GENERIC;
     nm_math used = NM_MATH_AUTO;
     if ((st = select(A, values, C, m, n, k, N, M, L, ab_dt, c_dt, math, &kernel, &used))) return st;
-    // alpha is fused into the epilogues of the SIMT (modes 0-2) and sparse-tensor-core kernels; the
+    // alpha is fused into the epilogues of the SIMT and sparse-tensor-core kernels; the
     // others are followed by one scaling pass over C when alpha != 1
     bool fused = false;
     if (kernel == K_SIMT_F32) {
         const int mode = simt_mode(m, n, k, N, M, L);
-        if (mode == 3) {
-            st = simt_pipe_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
-                                  static_cast<float*>(C), m, n, k, N, M, L, s);
-        } else {
-            st = simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
-                                 static_cast<float*>(C), m, n, k, N, M, L, mode, s, nullptr, alpha);
-            fused = true;
-        }
+        st = simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
+                             static_cast<float*>(C), m, n, k, N, M, L, mode, s, nullptr, alpha);
+        fused = true;
     } else if (kernel == K_TC_SP || kernel == K_TC_TF32) {
         st = tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, kernel == K_TC_TF32, s, alpha);
         fused = true;

@@ -74,6 +74,10 @@ struct Params {
     int n_units;  // CTA-pair kernel (spmm_tc_sp2.cu): work units = full tiles + split tiles x split
 };
 
+// bulk L2 prefetch of global bytes (size a multiple of 16)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // mbarrier wait variants (timing studies of the stage hand-off, NM_SP_DBG 1024 / 2048 / 4096):
 // try_wait with an explicit suspend-time hint (ns), and a pure test_wait spin
 __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {

@@ -5,11 +5,11 @@
                    sparsity-aware footprint reduction, only the tile's col_info rows of A^T loaded
                    (mode 2); V3 = + latency hiding, the software-pipelined index -> gather ->
                    FFMA2 chain on the TMA-staged A^T panel (mode 1, the default; Listing 4, P:540-546);
-                   plus the 128x256 deep-ring kernel (mode 3) and cuBLAS SGEMM (dense, all sparsities);
+                   and cuBLAS SGEMM (dense, all sparsities);
                    bf16: the slot kernel vs cuBLAS bf16 at the same points;
   * study=af    -- the blocking study (P:646-660 Table matrix_sizes): matrices A-F x the
-                   same 5 sparsities x kernel variants: fp32 'selector' (default schedule),
-                   'no-split' (one CTA per tile), 'large' (mode 3, 128x256 tiles); bf16 'selector',
+                   same 5 sparsities x kernel variants: fp32 'selector' (default schedule with the
+                   wave-model split), 'no-split' (one CTA per tile), mode 0; bf16 'selector',
                    H = 1 / H = 2 column halves, token tiles NT = 128 / 192 / 256; cuBLAS at 0 %.
 Kernel time = nm_profile CUDA events around the SpMM launch (median of 10, L2 flushed between
 steps); efficiency = kernel TFLOP/s (kept MACs) / the path's peak (FP32 FFMA 74.45, bf16 measured).
@@ -47,12 +47,12 @@ print("study,matrix,dtype,m,n,k,N,M,variant,kernel_us,kernel_tflops,efficiency,c
 if study == "v123":
     mats = {"4096^3": (4096, 4096, 4096)}
     F32V = {"V1 (mode 0)": {"NM_SIMT_MODE": "0"}, "V2 (mode 2, packed)": {"NM_SIMT_MODE": "2"},
-            "V3 (mode 1, default)": {}, "deep ring (mode 3)": {"NM_SIMT_MODE": "3"}}
+            "V3 (mode 1, default)": {}}
     BF16V = {"slot kernel (default)": {}}
 else:
     mats = {"A": (512, 512, 512), "B": (512, 1024, 1024), "C": (512, 2048, 2048), "D": (1024, 2048, 2048),
             "E": (2048, 4096, 4096), "F": (4096, 4096, 4096)}
-    F32V = {"selector": {}, "no-split": {"NM_SIMT_SPLIT": "1"}, "large (mode 3, 128x256)": {"NM_SIMT_MODE": "3"}}
+    F32V = {"selector": {}, "no-split": {"NM_SIMT_SPLIT": "1"}, "A straight from [m][k] panels (mode 0)": {"NM_SIMT_MODE": "0"}}
     BF16V = {"selector": {}, "H=1": {"NM_SP_H": "1"}, "H=2": {"NM_SP_H": "2"}, "H=2 NT=128": {"NM_SP_H": "2", "NM_SP_NT": "128"},
              "H=1 NT=128": {"NM_SP_H": "1", "NM_SP_NT": "128"}, "H=1 NT=192": {"NM_SP_H": "1", "NM_SP_NT": "192"}}
 for label, (m, n, k) in mats.items():
