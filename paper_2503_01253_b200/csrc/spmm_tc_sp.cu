@@ -1125,7 +1125,8 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     const int64_t sms = num_sms();
     // Split stage ranges (pair-aligned) over several CTAs per tile, partials added in a fixed order:
     //  * a grid below one wave (small problems, column shards of a multi-GPU layer): every tile in
-    //    S = sms / tiles parts (<= 8, >= 4 stage pairs per part, est_stages = the host's estimate);
+    //    S = sms / tiles parts (<= 8, >= MIN_PART_STAGES stages per part, est_stages = the host's
+    //    estimate);
     //  * a partial last wave that at most half fills the SMs: its tiles in 2 parts ("tail split").
     // NM_SP_SPLIT=S forces S for those tiles; NM_SP_TAIL=0 disables splitting.
     const char* te2 = std::getenv("NM_SP_TAIL");
@@ -1133,15 +1134,20 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     const bool can_split = !mc && p.tma_c && !(te2 && te2[0] == '0');
     int64_t split_tiles = 0;
     int S = 1;
+    // Every part must keep >= 24 stages: measured on B200 (profiles/r02f_sp_split_probe.txt) shorter
+    // parts lose to their fixed costs (1024^3 16:32 in 2 parts of ~8 stages: 25.6 vs 18.4 us unsplit;
+    // 2048x5120x5120 4:32 tail in parts of ~18: 56.6 vs 53.5 us), longer ones gain 1-4 % (cfg2 tail,
+    // the 8-GPU column shards of cfg2 / cfg3).
+    constexpr int MIN_PART_STAGES = 24;
     if (can_split && tiles < sms) {
         split_tiles = tiles;
         S = static_cast<int>(std::min<int64_t>(8, sms / tiles));
-        S = std::max(1, std::min(S, est_stages / 8));
+        S = std::max(1, std::min(S, est_stages / MIN_PART_STAGES));
     } else if (can_split && tiles % sms > 0 && 2 * (tiles % sms) <= sms) {
         split_tiles = tiles % sms;
-        S = 2;
+        S = est_stages / 2 >= MIN_PART_STAGES ? 2 : 1;
     }
-    if (se && split_tiles > 0) S = std::max(1, std::min(16, std::atoi(se)));
+    if (se && split_tiles > 0) S = std::max(1, std::min(16, std::atoi(se)));  // forced (tests, studies)
     if (S <= 1) split_tiles = 0, S = 1;
     p.full_ctas = static_cast<int>(tiles - split_tiles);
     p.split = S;

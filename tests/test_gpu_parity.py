@@ -495,6 +495,7 @@ def test_spmm_tc_sp_tail_split_on_off(nm, oracle, monkeypatch, tail, m, n, k, N,
     use_tc_path(monkeypatch, "sp")
     monkeypatch.setenv("NM_SP_PAIR", "0")  # the one-CTA kernel's tail split (pairs: test_gpu_pair.py)
     monkeypatch.setenv("NM_SP_TAIL", tail)
+    monkeypatch.setenv("NM_SP_SPLIT", "2")  # these tiles are too short for the selector to split them
     A = synth.integer((m, k), 131, synth.TID_A)
     B = synth.integer((k, n), 132, synth.TID_B)
     vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
@@ -545,6 +546,7 @@ def test_spmm_tc_tf32_token_tiles_all_rows(nm, oracle, monkeypatch, nt):
 @pytest.mark.parametrize("m,n,k,N,M,L", [(700, 768, 512, 16, 32, 32), (300, 640, 1024, 4, 32, 32)])
 def test_spmm_tc_tf32_tail_split_on_off(nm, oracle, monkeypatch, tail, m, n, k, N, M, L):
     monkeypatch.setenv("NM_SP_TAIL", tail)
+    monkeypatch.setenv("NM_SP_SPLIT", "2")  # forced: these tiles are too short for the selector's split
     C, ref = run_tf32(nm, oracle, m, n, k, N, M, L, "integer", 3)
     assert np.array_equal(C.astype(np.float64), ref)
 
