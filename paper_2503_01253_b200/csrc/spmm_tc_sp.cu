@@ -66,36 +66,58 @@ struct Cfg {
     static_assert(SMEM_BYTES <= 232448, "shared memory budget");
 };
 
-// Tokens per CTA (MMA N); NM_SP_NT overrides (ablation).  H = 1: 256 (a full 512-B row per
-// warp-wide cp.async).  H = 2: the fewest waves of CTAs over the SMs, ties in the order
-// 192, 208, 176, 224, 160 -- measured on B200 (profiles/r01f_sp_nt_sweep.txt): at equal wave
-// counts the kernel time is flat within +-4 % in NT, 192 lowest (TMEM caps N at 224 with two
-// accumulators and the metadata ring).
+// Tokens per CTA (MMA N); NM_SP_NT overrides (ablation).  Choice by a wave model: a tile's time
+// ~ its stages x (hand-off floor + MMA work), the MMA work growing with NT, so over the candidate
+// token tiles minimise rounds(tiles) x (NT + 64): rounds = full waves of tiles over the SMs plus
+// the last partial wave (half a round when it at most half fills the SMs and may be split).  The
+// +64 is the per-tile fixed cost in token-equivalents (fit on the A-F study: on small grids NT = 128
+// wins at H = 1, profiles/r02e_protocol_summary.txt); at equal cost the earlier candidate wins
+// (the order is the measured preference, profiles/r01f_sp_nt_sweep.txt; TMEM caps N at 224 with two
+// accumulators and the metadata ring at H = 2).
 static int sp_tokens(int H, int64_t m, int64_t n) {
     const char* e = std::getenv("NM_SP_NT");
     if (e) return std::atoi(e);
-    if (H == 1) return 256;
-    const int64_t sms = num_sms(), col_tiles = (n + 255) / 256;
-    int best = 192;
+    const int64_t sms = num_sms(), col_tiles = (n + 128 * H - 1) / (128 * H);
+    static const int c1[] = {256, 192, 128};
+    static const int c2[] = {192, 208, 176, 224, 160, 128};
+    const int* cand = H == 1 ? c1 : c2;
+    const int nc = H == 1 ? 3 : 6;
+    int best = cand[0];
     int64_t best_cost = -1;
-    for (const int nt : {192, 208, 176, 224, 160}) {
+    for (int i = 0; i < nc; ++i) {
+        const int nt = cand[i];
         const int64_t tiles = col_tiles * ((m + nt - 1) / nt), tail = tiles % sms;
-        // waves x 2; a tail that at most half fills the SMs is split in two (half a wave)
-        const int64_t cost = 2 * (tiles / sms) + (tail == 0 ? 0 : 2 * tail <= sms ? 1 : 2);
+        const int64_t rounds2 = 2 * (tiles / sms) + (tail == 0 ? 0 : 2 * tail <= sms ? 1 : 2);  // rounds x 2
+        const int64_t cost = rounds2 * (nt + 64);
         if (best_cost < 0 || cost < best_cost) best_cost = cost, best = nt;
     }
     return best;
 }
 
 // Column halves per CTA (NM_SP_H=1/2 overrides, ablation).  H = 2 halves the gathered bytes per
-// MAC but packs 8 groups per slot sequence instead of 4; measured on B200 it wins
-// at N/M >= 1/4 and loses at 87.5 % sparsity, where the 8-group union (66 % of k) needs 1.6x the
-// slots of the 4-group one -- so H = 2 iff L >= 32 and 4N >= M.
+// MAC but packs 8 groups per slot sequence instead of 4, whose union needs more slots as the
+// sparsity grows: measured on B200 (the A-F study, profiles/r02e_protocol_summary.txt, and the
+// BASELINE shapes, profiles/r02g_sp_tmem_weights_ab.txt tw=0 rows) H = 2 wins at 50 % (cfg2 104.5 vs
+// 115.2 us, 8192^3 583 vs 755) and 62.5 % (cfg3 109 vs 124), ties at 75 % on cfg3 (103 vs 105) and
+// loses there on 4096^3 / 2048x4096x4096 (95 vs 86, 64 vs 46 us), loses at 87.5 % -- so H = 2 iff
+// L >= 32 and 3N >= M.
 static int sp_halves(int L, int N, int M) {
     const char* e = std::getenv("NM_SP_H");
     if (e && e[0] == '1') return 1;
     if (e && e[0] == '2' && L >= 32) return 2;
-    return (L >= 32 && 4 * N >= M) ? 2 : 1;
+    return (L >= 32 && 3 * N >= M) ? 2 : 1;
+}
+
+// With the token count known (a per-call prepack: nm_spmm, nm_spmm_host) small grids take H = 1
+// below 100 % density: H = 2 then leaves the grid under two waves, and the 2x tiles of H = 1 buy
+// more parallelism than its larger unions cost (A-F study: 2048x4096x4096 62.5 % 53 vs 64 us,
+// 1024x2048x2048 50 % 20 vs 23 us; profiles/r02e_protocol_summary.txt).
+static int sp_halves_m(int L, int N, int M, int64_t m, int64_t n) {
+    const int H = sp_halves(L, N, M);
+    if (H != 2 || N == M || std::getenv("NM_SP_H")) return H;
+    const int nt = sp_tokens(2, m, n);
+    const int64_t tiles = ((n + 255) / 256) * ((m + nt - 1) / nt);
+    return tiles >= 2 * static_cast<int64_t>(num_sms()) ? 2 : 1;
 }
 
 
@@ -1283,12 +1305,15 @@ nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16,
     return st;
 }
 
+// nm_plan_query: the geometry nm_spmm (a per-call prepack) would use; nm_spmm_prepacked keeps the
+// H of its prepack (tcs::sp_halves, chosen without m)
 void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int* tokens) {
-    *halves = tcs::sp_halves(L, N, M);
+    *halves = tcs::sp_halves_m(L, N, M, m, n);
     *tokens = tcs::sp_tokens(*halves, m, n);
 }
 
 int tc_sp_halves(int N, int M, int L) { return tcs::sp_halves(L, N, M); }
+int tc_sp_halves_m(int N, int M, int L, int64_t m, int64_t n) { return tcs::sp_halves_m(L, N, M, m, n); }
 
 // nm_spmm without a prepacked weight: prepack into pooled scratch (the size bound, no sync), run,
 // release.
@@ -1296,7 +1321,7 @@ nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C,
                        int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha) {
     void* buf = nullptr;
     const size_t bytes = tc_sp_prepack_bytes(n, k, N, M, L, tf);
-    const int H = tcs::sp_halves(L, N, M);
+    const int H = tcs::sp_halves_m(L, N, M, m, n);  // per-call prepack: the token count is known
     nm_status st = scratch_alloc(&buf, bytes, s);
     if (st) return st;
     st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, H, buf, static_cast<int64_t>(bytes), nullptr, false, s);

@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def pair_on(monkeypatch):
     monkeypatch.setenv("NM_SP_PAIR", "1")
+    monkeypatch.setenv("NM_SP_H", "2")  # the pair kernel runs on the H = 2 prepack (also at 75 %)
 
 
 @pytest.fixture(scope="module")
