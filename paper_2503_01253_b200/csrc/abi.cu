@@ -240,8 +240,8 @@ bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 // tf: fp32 operands on the tf32 sparse tensor cores (1:2 slot pairs), else bf16 (2:4 slot quads)
 size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf);  // bound (no data)
 int tc_sp_halves(int N, int M, int L);
-int tc_sp_halves_m(int N, int M, int L, int64_t m, int64_t n);  // per-call prepack (m known)
-void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int* tokens);
+int tc_sp_halves_m(int N, int M, int L, int64_t m, int64_t n, int64_t k);  // per-call prepack (m known)
+void tc_sp_geometry(int64_t m, int64_t n, int64_t k, int N, int M, int L, int* halves, int* tokens);
 nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, int H,
                         void* buf, int64_t buf_bytes, int64_t* exact, bool query_only, cudaStream_t s);
 nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
@@ -564,7 +564,7 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     const int64_t rc = ceil_div(ceil_div(m, nch), 128) * 128;
     // slot kernels: prepack the weight once (the paper's offline step, here per call) on s
     const bool slot = kernel == K_TC_SP || kernel == K_TC_TF32, tf = kernel == K_TC_TF32;
-    const int hsp = tc_sp_halves_m(N, M, L, rc, n);  // the chunk's token count
+    const int hsp = tc_sp_halves_m(N, M, L, rc, n, k);  // the chunk's token count
     void* pbuf = nullptr;
     if (slot) {
         const size_t pb = tc_sp_prepack_bytes(n, k, N, M, L, tf);
@@ -658,7 +658,7 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         // tokens x output columns per CTA (MMA N x M per column half), 64 (bf16) / 32 (tf32) slots
         // per stage, the same bytes per stage
         int hh = 1, nt = 256;
-        tc_sp_geometry(m, n, N, M, L, &hh, &nt);
+        tc_sp_geometry(m, n, k, N, M, L, &hh, &nt);
         out->bm = nt;
         out->bn = 128 * hh;
         out->bk = kernel == K_TC_SP ? 64 : 32;

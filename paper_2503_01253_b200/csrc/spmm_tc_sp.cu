@@ -74,7 +74,8 @@ struct Cfg {
 // wins at H = 1, profiles/r02e_protocol_summary.txt); at equal cost the earlier candidate wins
 // (the order is the measured preference, profiles/r01f_sp_nt_sweep.txt; TMEM caps N at 224 with two
 // accumulators and the metadata ring at H = 2).
-static int sp_tokens(int H, int64_t m, int64_t n) {
+constexpr int MIN_PART_STAGES = 24;  // a split part keeps >= 24 stages (sp_launch_h, profiles/r02f_sp_split_probe.txt)
+static int sp_tokens(int H, int64_t m, int64_t n, int est_stages) {
     const char* e = std::getenv("NM_SP_NT");
     if (e) return std::atoi(e);
     const int64_t sms = num_sms(), col_tiles = (n + 128 * H - 1) / (128 * H);
@@ -83,13 +84,20 @@ static int sp_tokens(int H, int64_t m, int64_t n) {
     const int* cand = H == 1 ? c1 : c2;
     const int nc = H == 1 ? 3 : 6;
     int best = cand[0];
-    int64_t best_cost = -1;
+    double best_cost = -1;
     for (int i = 0; i < nc; ++i) {
         const int nt = cand[i];
         const int64_t tiles = col_tiles * ((m + nt - 1) / nt), tail = tiles % sms;
-        const int64_t rounds2 = 2 * (tiles / sms) + (tail == 0 ? 0 : 2 * tail <= sms ? 1 : 2);  // rounds x 2
-        const int64_t cost = rounds2 * (nt + 64);
-        if (best_cost < 0 || cost < best_cost) best_cost = cost, best = nt;
+        double rounds;
+        if (tiles <= sms) {  // one round, shortened by a sub-wave split into S parts
+            const int64_t S = std::max<int64_t>(1, std::min<int64_t>({8, sms / tiles, est_stages / MIN_PART_STAGES}));
+            rounds = 1.0 / static_cast<double>(S);
+        } else {  // full waves + the last partial wave (half a round when it is split in two)
+            const bool half = 2 * tail <= sms && est_stages / 2 >= MIN_PART_STAGES;
+            rounds = static_cast<double>(tiles / sms) + (tail == 0 ? 0.0 : half ? 0.5 : 1.0);
+        }
+        const double cost = rounds * (nt + 64);
+        if (best_cost < 0 || cost < best_cost - 1e-9) best_cost = cost, best = nt;
     }
     return best;
 }
@@ -112,10 +120,21 @@ static int sp_halves(int L, int N, int M) {
 // below 100 % density: H = 2 then leaves the grid under two waves, and the 2x tiles of H = 1 buy
 // more parallelism than its larger unions cost (A-F study: 2048x4096x4096 62.5 % 53 vs 64 us,
 // 1024x2048x2048 50 % 20 vs 23 us; profiles/r02e_protocol_summary.txt).
-static int sp_halves_m(int L, int N, int M, int64_t m, int64_t n) {
+// Stages per tile the selector expects (host, no data): the tile's kept-row union
+// k (1 - (1 - N/M)^G) over its G = 128 H / L groups, at least 2 w (two rows per quad / one per
+// pair), + 10 % packing slack.
+static int sp_est_stages(int64_t k, int N, int M, int L, int H, bool tf) {
+    const int G = 128 * H / L;
+    const double keep = static_cast<double>(N) / M;
+    const double uni = 1.0 - std::pow(1.0 - keep, G);
+    const double slots = 1.1 * static_cast<double>(k) * std::max(uni, std::min(1.0, 2.0 * keep));
+    return static_cast<int>(slots / (tf ? El<true>::SLOTS : El<false>::SLOTS)) + 1;
+}
+
+static int sp_halves_m(int L, int N, int M, int64_t m, int64_t n, int64_t k) {
     const int H = sp_halves(L, N, M);
     if (H != 2 || N == M || std::getenv("NM_SP_H")) return H;
-    const int nt = sp_tokens(2, m, n);
+    const int nt = sp_tokens(2, m, n, sp_est_stages(k, N, M, L, 2, false));
     const int64_t tiles = ((n + 255) / 256) * ((m + nt - 1) / nt);
     return tiles >= 2 * static_cast<int64_t>(num_sms()) ? 2 : 1;
 }
@@ -1160,7 +1179,6 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     // parts lose to their fixed costs (1024^3 16:32 in 2 parts of ~8 stages: 25.6 vs 18.4 us unsplit;
     // 2048x5120x5120 4:32 tail in parts of ~18: 56.6 vs 53.5 us), longer ones gain 1-4 % (cfg2 tail,
     // the 8-GPU column shards of cfg2 / cfg3).
-    constexpr int MIN_PART_STAGES = 24;
     if (can_split && tiles < sms) {
         split_tiles = tiles;
         S = static_cast<int>(std::min<int64_t>(8, sms / tiles));
@@ -1229,16 +1247,6 @@ static nm_status sp_dispatch(int H, int nt, const void* at, const tcs::Params& p
     }
 }
 
-// Stages per tile the selector expects (host, no data): the tile's kept-row union
-// k (1 - (1 - N/M)^G) over its G = 128 H / L groups, at least 2 w (two rows per quad / one per
-// pair), + 10 % packing slack.
-static int sp_est_stages(int64_t k, int N, int M, int L, int H, bool tf) {
-    const int G = 128 * H / L;
-    const double keep = static_cast<double>(N) / M;
-    const double uni = 1.0 - std::pow(1.0 - keep, G);
-    const double slots = 1.1 * static_cast<double>(k) * std::max(uni, std::min(1.0, 2.0 * keep));
-    return static_cast<int>(slots / (tf ? tcs::El<true>::SLOTS : tcs::El<false>::SLOTS)) + 1;
-}
 
 // One SpMM on a prepacked weight (buf from tc_sp_prepack with H column halves per tile).
 nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
@@ -1292,11 +1300,11 @@ nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16,
             p.col_off = po->col_off;
             p.n_valid = static_cast<int>(po->n_valid);
         }
-        const int est = sp_est_stages(k, N, M, L, g.H, tf);
+        const int est = tcs::sp_est_stages(k, N, M, L, g.H, tf);
         if (!po && tc_sp2_enabled(tf, g.H)) {
             st = tc_sp2_launch(at, p, m, n, est, s);  // CTA pairs (spmm_tc_sp2.cu)
         } else {
-            const int nt = sp_tokens(g.H, m, n);
+            const int nt = sp_tokens(g.H, m, n, est);
             st = tf ? sp_dispatch<true>(g.H, nt, at, p, m, n, est, s) : sp_dispatch<false>(g.H, nt, at, p, m, n, est, s);
         }
     }
@@ -1307,13 +1315,13 @@ nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16,
 
 // nm_plan_query: the geometry nm_spmm (a per-call prepack) would use; nm_spmm_prepacked keeps the
 // H of its prepack (tcs::sp_halves, chosen without m)
-void tc_sp_geometry(int64_t m, int64_t n, int N, int M, int L, int* halves, int* tokens) {
-    *halves = tcs::sp_halves_m(L, N, M, m, n);
-    *tokens = tcs::sp_tokens(*halves, m, n);
+void tc_sp_geometry(int64_t m, int64_t n, int64_t k, int N, int M, int L, int* halves, int* tokens) {
+    *halves = tcs::sp_halves_m(L, N, M, m, n, k);
+    *tokens = tcs::sp_tokens(*halves, m, n, tcs::sp_est_stages(k, N, M, L, *halves, false));
 }
 
 int tc_sp_halves(int N, int M, int L) { return tcs::sp_halves(L, N, M); }
-int tc_sp_halves_m(int N, int M, int L, int64_t m, int64_t n) { return tcs::sp_halves_m(L, N, M, m, n); }
+int tc_sp_halves_m(int N, int M, int L, int64_t m, int64_t n, int64_t k) { return tcs::sp_halves_m(L, N, M, m, n, k); }
 
 // nm_spmm without a prepacked weight: prepack into pooled scratch (the size bound, no sync), run,
 // release.
@@ -1321,7 +1329,7 @@ nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C,
                        int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha) {
     void* buf = nullptr;
     const size_t bytes = tc_sp_prepack_bytes(n, k, N, M, L, tf);
-    const int H = tcs::sp_halves_m(L, N, M, m, n);  // per-call prepack: the token count is known
+    const int H = tcs::sp_halves_m(L, N, M, m, n, k);  // per-call prepack: the token count is known
     nm_status st = scratch_alloc(&buf, bytes, s);
     if (st) return st;
     st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, H, buf, static_cast<int64_t>(bytes), nullptr, false, s);

@@ -133,3 +133,28 @@ def test_plan_simt_split_matches_measured_best(L, cfg, best):
     tiles = -(-m // 128) * -(-n // 128)
     assert p["grid"] == tiles - p["split_tiles"] + p["split_tiles"] * p["split"]
     assert abs(p["waves"] - p["grid"] / 296) < 1e-9
+
+
+# The bf16 slot kernel's geometry for nm_spmm (per-call prepack: m known) pinned to the choices the
+# A-F study and the BASELINE timings support (profiles/r02e_protocol_summary.txt,
+# profiles/r02g_protocol_af_after_retune.csv, profiles/r02g_sp_tmem_weights_ab.txt): bn = 128 H output
+# columns per CTA, bm = NT tokens.
+SLOT_GEOMETRY = [
+    ((4096, 4096, 4096, 16, 32, 32), 256, 192),    # cfg2: H = 2 (50 %), 352 tiles
+    ((2048, 11008, 4096, 12, 32, 32), 256, 208),   # cfg3 62.5 %: H = 2 (109 vs 124 us); 430 tiles
+    ((256, 22016, 8192, 4, 32, 32), 128, 256),     # cfg4 m = 256: H = 1, one token tile
+    ((2048, 11008, 4096, 8, 32, 32), 128, 256),    # cfg3 75 %: H = 1
+    ((2048, 22016, 8192, 4, 32, 32), 128, 256),    # cfg4 87.5 %: H = 1
+    ((2048, 4096, 4096, 12, 32, 32), 128, 256),    # A-F "E" 62.5 %: H = 2 would be < 2 waves -> H = 1
+    ((1024, 2048, 2048, 16, 32, 32), 128, 128),    # A-F "D" 50 %: small grid -> H = 1, NT = 128
+    ((512, 512, 512, 32, 32, 32), 256, 128),       # N = M: H = 2 always; 8 tiles -> the smallest NT
+]
+
+
+@pytest.mark.parametrize("cfg,bn,bm", SLOT_GEOMETRY)
+def test_plan_slot_geometry(L, cfg, bn, bm):
+    from paper_2503_01253_b200 import nmspmm
+    import torch
+    p = nmspmm.nm_plan_query(*cfg, torch.bfloat16)
+    assert p["kernel"] == 4
+    assert (p["bn"], p["bm"]) == (bn, bm), p
