@@ -320,6 +320,43 @@ nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* co
                                   int64_t col_off, int64_t n_valid, int64_t m, nm_dtype c_dt, void* stream);
 
 /*
+ * NVLS multicast C ("an NVLS multicast epilogue (multimem.st into a symmetric-memory
+ * C) so tiles land on all peers as they retire"; the assembly of the column-sharded layer, north
+ * star).  A multicast object spans the G ranks' devices; each rank binds its own physical C buffer
+ * to it and maps two views of it: the multicast address (a store through it reaches every bound
+ * buffer, replicated by the NVSwitch) and the unicast address of its own replica.
+ *   nm_mc_supported  : *supported = 1 iff the current device supports multicast objects and this
+ *                      process can create one (a trial object; with one visible GPU of a multi-GPU
+ *                      node the driver refuses: CUDA_ERROR_INVALID_VALUE).
+ *   nm_mc_create     : rank 0 (or a single process): a multicast object of >= bytes per device for
+ *                      num_devices devices (1..8); *mc = its handle, *mc_bytes = the size rounded up to
+ *                      the recommended granularity (use it everywhere below).  Exportable as a fabric
+ *                      handle when num_devices > 1.
+ *   nm_mc_export / nm_mc_import : the 64-byte fabric handle of the object (rank 0 exports, the other
+ *                      ranks import; the bytes travel over any channel, e.g. torch.distributed).
+ *   nm_mc_add_device : add the current device (every rank, before any rank binds).
+ *   nm_mc_bind_map   : allocate this device's buffer (mc_bytes), bind it, map *uc_ptr (this replica)
+ *                      and *mc_ptr (the multicast view); *mem = the physical allocation's handle.
+ *   nm_mc_free       : unmap, unbind and release everything nm_mc_* created here (synchronizes).
+ *   nm_spmm_mc       : nm_spmm_peers with one destination, the multicast address: the SIMT kernel's
+ *                      epilogue writes each float4 of its [m x n_valid] shard once with multimem.st
+ *                      at C_mc[i][col_off + j] (row pitch ldc floats); every rank's replica receives
+ *                      it.  Same geometry requirements as nm_spmm_peers.  Completion across ranks:
+ *                      nm_peer_barrier.  Asynchronous.
+ * Errors: NM_ERR_UNSUPPORTED without multicast support or driver entry points; NM_ERR_CUDA with the
+ * driver's CUresult in nm_last_error().
+ */
+nm_status nm_mc_supported(int* supported);
+nm_status nm_mc_create(int64_t bytes, int num_devices, uint64_t* mc, int64_t* mc_bytes);
+nm_status nm_mc_export(uint64_t mc, void* fabric_handle);
+nm_status nm_mc_import(const void* fabric_handle, uint64_t* mc);
+nm_status nm_mc_add_device(uint64_t mc);
+nm_status nm_mc_bind_map(uint64_t mc, int64_t mc_bytes, uint64_t* mem, void** uc_ptr, void** mc_ptr);
+nm_status nm_mc_free(uint64_t mc, uint64_t mem, void* uc_ptr, void* mc_ptr, int64_t mc_bytes);
+nm_status nm_spmm_mc(const void* A, const void* values, const uint8_t* idx, void* C_mc, int64_t ldc, int64_t col_off,
+                     int64_t n_valid, int64_t m, int64_t nr, int64_t k, int N, int M, int L, void* stream);
+
+/*
  * nm_profile_begin / nm_profile_end -- launch accounting for measurement
  * (bench.py).  Between the two calls the library counts every kernel it
  * launches and records a CUDA event pair on the launching stream around each

@@ -33,6 +33,7 @@ nm_status cuda_fail(cudaError_t e, const char* what);
 
 int num_sms();         // SM count of the current device (cached per device; 148 on B200)
 int current_device();  // cudaGetDevice, -1 on error
+nm_status require_device();  // NM_OK iff a device of compute capability 10.0 is current
 // Once-per-device guards for cudaFuncSetAttribute (MaxDynamicSharedMemorySize is a per-device
 // setting): attr_once(mask) is true once attr_done(mask) ran on the current device.  Racing
 // threads may both set the attribute, which is idempotent.
@@ -55,6 +56,7 @@ struct PeerOut {
     void* c[8];
     int np;
     int64_t ldc, col_off, n_valid;
+    int mc = 0;  // 1: c[0] is a multicast (NVLS) address, written once with multimem.st (nm_spmm_mc)
 };
 
 // TMA descriptor encoding (cuTensorMapEncodeTiled fetched via cudaGetDriverEntryPoint).

@@ -163,6 +163,34 @@ nm_status nm_spmm_peers(const void* A, const void* values, const uint8_t* idx, v
                            1.f, nullptr);
 }
 
+nm_status nm_spmm_mc(const void* A, const void* values, const uint8_t* idx, void* C_mc, int64_t ldc, int64_t col_off,
+                     int64_t n_valid, int64_t m, int64_t nr, int64_t k, int N, int M, int L, void* stream) {
+    if (N < 1 || M < N || M > 256 || L < 1) return fail(NM_ERR_INVALID_CONFIG, "invalid N:M/L");
+    if (m < 0 || nr < 0 || k < 0 || k % M || nr % L) return fail(NM_ERR_SHAPE, "nm_spmm_mc: shape");
+    if (col_off < 0 || n_valid < 0 || n_valid > nr || col_off + n_valid > ldc || n_valid % 4)
+        return fail(NM_ERR_SHAPE, "nm_spmm_mc: columns [col_off, col_off + n_valid) outside ldc, n_valid > nr or "
+                                  "n_valid % 4 != 0");
+    if (m == 0 || nr == 0 || n_valid == 0) return NM_OK;
+    if (!A || !C_mc || (k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_spmm_mc: NULL pointer");
+    PeerOut po{};
+    po.np = 1;
+    po.mc = 1;
+    po.ldc = ldc;
+    po.col_off = col_off;
+    po.n_valid = n_valid;
+    po.c[0] = C_mc;
+    const uintptr_t al = static_cast<uintptr_t>(ldc | col_off) * 4u | reinterpret_cast<uintptr_t>(C_mc);
+    if (k == 0 || (al & 15) || !simt_f32_applicable(A, values, C_mc, m, nr, k, N, M, L))
+        return fail(NM_ERR_UNSUPPORTED, "nm_spmm_mc: needs the fp32 SIMT kernel's geometry (L % 4 == 0, M <= 64, "
+                                        "N <= 32, k > 0, 16-B aligned operands, ldc and col_off multiples of 4)");
+    nm_status st = require_device();
+    if (st) return st;
+    const int mode = m % 4 == 0 ? 1 : 0;
+    return simt_f32_launch(static_cast<const float*>(A), static_cast<const float*>(values), idx,
+                           static_cast<float*>(C_mc), m, nr, k, N, M, L, mode, static_cast<cudaStream_t>(stream), &po,
+                           1.f, nullptr);
+}
+
 nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* const* C_peers, int G, int64_t ldc,
                                   int64_t col_off, int64_t n_valid, int64_t m, nm_dtype c_dt, void* stream) {
     if (!w || w->magic != 0x4B504D4E) return fail(NM_ERR_NULL, "nm_spmm_prepacked_peers: descriptor not filled by nm_prepack");

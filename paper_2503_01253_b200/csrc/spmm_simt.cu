@@ -59,6 +59,7 @@ struct Params {
     // sharded layer fused into the SpMM's stores over NVLink peer memory.  npeer = 0: C.
     float* cpeer[8];
     int npeer, n_valid;
+    int mc;  // 1: cpeer[0] is a multicast (NVLS) address: one multimem.st per float4 reaches every rank
     int64_t ldc, col_off;
     float alpha;  // C = alpha . A B~ (1: the product; M/N: Eq. 1 as printed, nm_spmm_scaled)
     // bit-packed tile-major indices (nm_index_pack, P:288 / P:419) instead of D when non-null:
@@ -67,6 +68,13 @@ struct Params {
     int db, de, dT;
     int64_t dwt;
 };
+
+// 16-B store through a multicast (NVLS) address: one instruction, replicated to every bound buffer
+__device__ __forceinline__ void mc_store4(float* addr, float a, float b, float c, float d) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c),
+                 "f"(d)
+                 : "memory");
+}
 
 // Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
 // box kk/32, 16-byte chunk (kk%32)/4, word kk%4.
@@ -356,6 +364,12 @@ __global__ void __launch_bounds__(THREADS, 2)
         for (int i = 0; i < 8; ++i) {
             const int row = m0 + wm * 64 + (AT ? (i & 3) + 4 * t_m + 32 * (i >> 2) : 8 * i + t_m);
             if (row >= p.m) continue;
+            if (p.mc) {  // NVLS: the switch replicates each store into every rank's bound C buffer
+                float* crow = p.cpeer[0] + static_cast<int64_t>(row) * p.ldc + p.col_off;
+                if (gc0 < p.n_valid) mc_store4(crow + gc0, acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+                if (gc0 + 16 < p.n_valid) mc_store4(crow + gc0 + 16, acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+                continue;
+            }
             for (int pi = 0; pi < p.npeer; ++pi) {
                 float* crow = p.cpeer[pi] + static_cast<int64_t>(row) * p.ldc + p.col_off;
                 if (gc0 < p.n_valid)
@@ -538,6 +552,7 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
         p.ldc = po->ldc;
         p.col_off = po->col_off;
         p.n_valid = static_cast<int>(po->n_valid);
+        p.mc = po->mc;
     }
     p.m = static_cast<int>(m);
     p.n = static_cast<int>(n);

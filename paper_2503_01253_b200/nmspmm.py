@@ -30,7 +30,8 @@ EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_
            "nm_profile_begin", "nm_profile_end", "nm_prepack_bytes", "nm_prepack", "nm_spmm_prepacked",
            "nm_prepack_bytes_ex", "nm_prepack_ex", "nm_ipc_get_handle", "nm_ipc_open_handle", "nm_ipc_close",
            "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled", "nm_prepack_size",
-           "nm_index_packed_words", "nm_index_pack", "nm_index_unpack"]
+           "nm_index_packed_words", "nm_index_pack", "nm_index_unpack", "nm_mc_supported", "nm_mc_create",
+           "nm_mc_export", "nm_mc_import", "nm_mc_add_device", "nm_mc_bind_map", "nm_mc_free", "nm_spmm_mc"]
 
 
 class NmError(RuntimeError):
@@ -106,6 +107,15 @@ def lib():
         L.nm_peer_barrier.argtypes = [ctypes.POINTER(P), I, I, I, P]
         L.nm_spmm_prepacked_peers.argtypes = [P, ctypes.POINTER(Prepacked), ctypes.POINTER(P), I, I64, I64, I64, I64, I,
                                               P]
+        U64 = ctypes.c_uint64
+        L.nm_mc_supported.argtypes = [ctypes.POINTER(I)]
+        L.nm_mc_create.argtypes = [I64, I, ctypes.POINTER(U64), ctypes.POINTER(I64)]
+        L.nm_mc_export.argtypes = [U64, P]
+        L.nm_mc_import.argtypes = [P, ctypes.POINTER(U64)]
+        L.nm_mc_add_device.argtypes = [U64]
+        L.nm_mc_bind_map.argtypes = [U64, I64, ctypes.POINTER(U64), ctypes.POINTER(P), ctypes.POINTER(P)]
+        L.nm_mc_free.argtypes = [U64, U64, P, P, I64]
+        L.nm_spmm_mc.argtypes = [P, P, P, P, I64, I64, I64, I64, I64, I64, I, I, I, P]
         for name in EXPORTS[2:]:
             if name not in ("nm_spmm_host_ws_bytes", "nm_prepack_bytes", "nm_prepack_bytes_ex", "nm_index_packed_words"):
                 getattr(L, name).restype = I
@@ -416,3 +426,57 @@ def _dt_of(dtype) -> int:
     if dtype == torch.bfloat16:
         return NM_BF16
     raise TypeError(f"unsupported dtype {dtype}")
+
+
+# ----------------------------------------------------------------------------- NVLS multicast C
+class McBuffer:
+    """A multicast (NVLS) buffer of this process's device (nm_mc_*): `mc_ptr` is the multicast
+    view (stores through it reach every bound rank's replica), `uc_ptr` this device's replica.
+    Single-process form (num_devices = 1); the collective multi-rank setup is the same calls with
+    the fabric handle exchanged (MulticastExchange in sharded.py)."""
+
+    def __init__(self, nbytes: int, num_devices: int = 1, fabric_handle: bytes | None = None):
+        L = lib()
+        self.mc, self.mem = ctypes.c_uint64(), ctypes.c_uint64()
+        self.bytes = ctypes.c_int64()
+        self.uc_ptr, self.mc_ptr = ctypes.c_void_p(), ctypes.c_void_p()
+        if fabric_handle is None:
+            _check(L.nm_mc_create(int(nbytes), num_devices, ctypes.byref(self.mc), ctypes.byref(self.bytes)),
+                   "nm_mc_create")
+        else:
+            buf = ctypes.create_string_buffer(bytes(fabric_handle), 64)
+            _check(L.nm_mc_import(buf, ctypes.byref(self.mc)), "nm_mc_import")
+            self.bytes.value = int(nbytes)
+
+    def export(self) -> bytes:
+        buf = ctypes.create_string_buffer(64)
+        _check(lib().nm_mc_export(self.mc, buf), "nm_mc_export")
+        return buf.raw
+
+    def add_device(self):
+        _check(lib().nm_mc_add_device(self.mc), "nm_mc_add_device")
+
+    def bind_map(self):
+        _check(lib().nm_mc_bind_map(self.mc, self.bytes, ctypes.byref(self.mem), ctypes.byref(self.uc_ptr),
+                                    ctypes.byref(self.mc_ptr)), "nm_mc_bind_map")
+
+    def free(self):
+        if self.mc.value:
+            _check(lib().nm_mc_free(self.mc, self.mem, self.uc_ptr, self.mc_ptr, self.bytes), "nm_mc_free")
+            self.mc.value = 0
+
+
+def nm_mc_supported() -> bool:
+    v = ctypes.c_int(0)
+    _check(lib().nm_mc_supported(ctypes.byref(v)), "nm_mc_supported")
+    return bool(v.value)
+
+
+def nm_spmm_mc(A: torch.Tensor, W: "NmWeight", c_mc: int, ldc: int, col_off: int, n_valid: int, stream=None) -> None:
+    """C_mc[i][col_off + j] = (A . B~)[i][j] through a multicast address (nm_spmm_mc, fp32 SIMT)."""
+    _dev(A, "A")
+    if A.dtype != torch.float32 or W.values.dtype != torch.float32:
+        raise TypeError("nm_spmm_mc: fp32 A and values (the SIMT kernel's multicast epilogue)")
+    m, k = A.shape
+    _check(lib().nm_spmm_mc(A.data_ptr(), W.values.data_ptr(), W.idx.data_ptr(), ctypes.c_void_p(c_mc), ldc, col_off,
+                            n_valid, m, W.n, k, W.N, W.M, W.L, _stream(A, stream)), "nm_spmm_mc")
