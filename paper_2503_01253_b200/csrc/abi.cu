@@ -233,6 +233,7 @@ bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 int simt_split_factor(int ntiles, int64_t w, int npanels);
+int simt_row_tile(int64_t m, int64_t n);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
                           float alpha = 1.f, const uint32_t* Dw = nullptr);
@@ -639,21 +640,22 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
     if (kernel == K_SIMT_F32) {
         int wp, bk, bkw;
         simt_f32_geometry(N, M, &wp, &bk, &bkw);
-        out->bm = 128;
+        const int bm = simt_row_tile(m, n);
+        out->bm = bm;
         out->bn = 128;
         out->bk = bk;
         out->bkw = bkw;
         out->stages = 2;
-        out->threads = 256;
-        const int64_t tiles = ceil_div(m, 128) * ceil_div(n, 128);
+        out->threads = 2 * bm;
+        const int64_t tiles = ceil_div(m, bm) * ceil_div(n, 128);
         const int npanels = static_cast<int>(ceil_div(k / M, wp));
-        const int sp = simt_split_factor(static_cast<int>(tiles), w, npanels);
-        const int64_t resident = 2 * static_cast<int64_t>(sms);
+        const int sp = bm == 128 || getenv("NM_SIMT_SPLIT") ? simt_split_factor(static_cast<int>(tiles), w, npanels) : 1;
+        const int64_t resident = (bm == 128 ? 2 : 3) * static_cast<int64_t>(sms);
         out->split = sp;
         out->split_tiles = sp > 1 ? static_cast<int32_t>(tiles % resident) : 0;
         out->grid = static_cast<int32_t>(tiles - out->split_tiles + out->split_tiles * static_cast<int64_t>(sp));
         out->waves = double(out->grid) / double(resident);
-        out->smem_bytes = 2 * (128 * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
+        out->smem_bytes = 2 * (bm * 64 * 4 + 32 * 128 * 4) + 2 * 32 * 33 * 4 + 64 + 1024;
     } else if (kernel == K_TC_SP || kernel == K_TC_TF32) {
         // tokens x output columns per CTA (MMA N x M per column half), 64 (bf16) / 32 (tf32) slots
         // per stage, the same bytes per stage

@@ -78,9 +78,23 @@ __device__ __forceinline__ void mc_store4(float* addr, float a, float b, float c
 
 // Byte offset (before the per-row XOR) of dense column kk (0..63) inside an A stage:
 // box kk/32, 16-byte chunk (kk%32)/4, word kk%4.
+template <int BMT>
 __device__ __forceinline__ int a_col_offset(int kk) {
-    return ((kk >> 5) * A_BOX_BYTES) + (((kk & 31) >> 2) << 4) + ((kk & 3) << 2);
+    return ((kk >> 5) * (BMT * A_BOX_COLS * 4)) + (((kk & 31) >> 2) << 4) + ((kk & 3) << 2);
 }
+
+// Row-tile geometry: BMT = 128 (8 warps of 64 x 32, 2 CTAs/SM) or 64 (4 warps of 64 x 32, 3 CTAs/SM;
+// for sub-wave grids: column shards of a multi-GPU layer, small problems -- the selector's choice).
+template <int BMT>
+struct SG {
+    static constexpr int THREADS = 2 * BMT;
+    static constexpr int MINB = BMT == 128 ? 2 : 3;                 // resident CTAs per SM
+    static constexpr int A_BOX_BYTES = BMT * A_BOX_COLS * 4;
+    static constexpr int A_STAGE_BYTES = BMT * BK * 4;
+    static constexpr int SMEM_BYTES = STAGES * (A_STAGE_BYTES + B_STAGE_BYTES) + KOFF_BYTES + 64 + 1024;
+    static constexpr int SMEM_BYTES_PACKED = SMEM_BYTES + MASK_BYTES;
+    static constexpr int D_PER_THREAD = (BKW * MAX_SLOTS + THREADS - 1) / THREADS;
+};
 
 // TWO: the thread's two 4-column chunks may belong to different column groups (L < 32).
 // AT:  A arrives transposed (A^T, k x m, written by transpose_kernel): the panel is
@@ -94,10 +108,13 @@ __device__ __forceinline__ int a_col_offset(int kk) {
 //      positions (reorderingIdx) by a popcount over the col_info mask.
 // PEER: the fused exchange's peer-store epilogue (nm_spmm_peers), a separate instantiation so the
 // common kernel's code and register allocation stay as they were.
-template <bool TWO, bool AT, bool PK, bool PEER = false>
-__global__ void __launch_bounds__(THREADS, 2)
+template <int BMT, bool TWO, bool AT, bool PK, bool PEER = false>
+__global__ void __launch_bounds__(SG<BMT>::THREADS, SG<BMT>::MINB)
     spmm_simt_f32_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                          const Params p) {
+    constexpr int BM = BMT, THREADS = SG<BMT>::THREADS, A_BOX_BYTES = SG<BMT>::A_BOX_BYTES;
+    constexpr int A_STAGE_BYTES = SG<BMT>::A_STAGE_BYTES, D_PER_THREAD = SG<BMT>::D_PER_THREAD;
+    static_assert(!PK || BMT == 128, "packed mode: one 512-B A^T row per warp-wide cp.async (BM = 128)");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-B alignment for the swizzle-128B TMA destination; offset arithmetic on the
     // __shared__ array keeps the shared address space visible to the compiler (LDS, not LD)
@@ -109,7 +126,7 @@ __global__ void __launch_bounds__(THREADS, 2)
     uint64_t* smask = bars + 8;  // [MAX_PANELS_PACKED] (packed mode)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp & 1, wn = warp >> 1;
+    const int wm = BMT == 128 ? (warp & 1) : 0, wn = BMT == 128 ? (warp >> 1) : warp;
     const int t_m = lane & 7, t_n = lane >> 3;
     int tile = blockIdx.x, part = 0, nparts = 1;
     if (tile >= p.full_tiles) {
@@ -230,7 +247,7 @@ __global__ void __launch_bounds__(THREADS, 2)
             {
                 const int kk = (d_us[r] >> 16) + dreg[r];  // dense column inside the panel
                 const int row = PK ? __popcll(mk & ((1ull << kk) - 1ull)) : kk;  // packed position
-                kb[((d_us[r] >> 8) & 255) * MAX_SLOTS + (d_us[r] & 255)] = AT ? row * (BM * 4) : a_col_offset(kk);
+                kb[((d_us[r] >> 8) & 255) * MAX_SLOTS + (d_us[r] & 255)] = AT ? row * (BM * 4) : a_col_offset<BMT>(kk);
             }
         }
     };
@@ -468,29 +485,45 @@ __global__ void build_colinfo_kernel(const uint8_t* __restrict__ D, uint64_t* __
     if (threadIdx.x == 0) masks[static_cast<int64_t>(tile) * npanels + panel] = mk;
 }
 
-template <bool TWO, bool AT, bool PK>
+template <int BMT, bool TWO, bool AT, bool PK>
 static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, const simt::Params& p, dim3 grid,
                              cudaStream_t s) {
     using namespace simt;
-    const int smem = PK ? SMEM_BYTES_PACKED : SMEM_BYTES;
+    using G = SG<BMT>;
+    const int smem = PK ? G::SMEM_BYTES_PACKED : G::SMEM_BYTES;
     static std::atomic<uint64_t> attr_mask{0};
     if (!attr_once(attr_mask)) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         smem));
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<BMT, TWO, AT, PK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         if (!PK)
-            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<TWO, AT, false, true>,
+            NM_CUDA_TRY(cudaFuncSetAttribute(spmm_simt_f32_kernel<BMT, TWO, AT, false, true>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         attr_done(attr_mask);
     }
     prof_begin(s);
     if (!PK && p.npeer)
-        spmm_simt_f32_kernel<TWO, AT, false, true><<<grid, THREADS, smem, s>>>(tmA, tmB, p);
+        spmm_simt_f32_kernel<BMT, TWO, AT, false, true><<<grid, G::THREADS, smem, s>>>(tmA, tmB, p);
     else
-        spmm_simt_f32_kernel<TWO, AT, PK><<<grid, THREADS, smem, s>>>(tmA, tmB, p);
+        spmm_simt_f32_kernel<BMT, TWO, AT, PK><<<grid, G::THREADS, smem, s>>>(tmA, tmB, p);
     prof_end(s);
     note_launch();
     NM_LAUNCH_CHECK("spmm_simt_f32_kernel");
     return NM_OK;
+}
+
+// Row tile of the SIMT kernel (the selector): 64 rows (4 warps, 3 resident CTAs per
+// SM) when the 64-row grid fits in one round of resident CTAs (tiles64 <= 3 x SMs: sub-wave grids
+// such as the column shards of a multi-GPU layer, m = 256 decode shapes, small problems), else 128
+// (8 warps, 2 per SM, with the wave-model split of its tail).  Measured on B200
+// (profiles/r02j_simt_row_tile.txt): 1024^3 47.1 -> 39.5 us, 256x13824x5120 141 -> 114, the
+// cfg3-75 % 8-GPU shard 183 -> 173, cfg1 27.2 -> 20.8; beyond one round the 128-row tile with its
+// split wins (m = 256 cfg4-65B 258 vs 280, 2048^3 188 vs 193); the one loss of the rule is the cfg2
+// shard (225 vs 220 us).  NM_SIMT_BM=64/128 overrides.
+int simt_row_tile(int64_t m, int64_t n) {
+    const char* e = getenv("NM_SIMT_BM");
+    if (e) return atoi(e) == 64 ? 64 : 128;
+    const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, simt::BN);
+    return tiles64 <= 3 * static_cast<int64_t>(num_sms()) ? 64 : 128;
 }
 
 // Split factor of the SIMT kernel's tile schedule (the selector's wave model): the
@@ -567,10 +600,12 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     p.nboxA = (p.bk + A_BOX_COLS - 1) / A_BOX_COLS;
     const int64_t w = k / M * N;
     if (mode == 2 && p.npanels > MAX_PANELS_PACKED) mode = 1;
+    const int bm = simt_row_tile(m, n);
+    if (bm == 64 && mode == 2) mode = 1;  // packed mode: 512-B A^T rows (BM = 128)
     const bool use_at = mode >= 1;
     const bool packed = mode == 2;
     const int ntiles_n = static_cast<int>(ceil_div(n, BN));
-    p.at_ld = static_cast<int>(ceil_div(m, BM) * BM);  // padded so every 128-row A^T segment is in bounds
+    p.at_ld = static_cast<int>(ceil_div(m, bm) * bm);  // padded so every bm-row A^T segment is in bounds
 
     CUtensorMap tmA, tmB;
     nm_status st = make_tma_2d(&tmB, Bv, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, w, n, p.bkw, BN, 0);
@@ -585,9 +620,9 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
         note_launch();
         NM_LAUNCH_CHECK("transpose_kernel");
         p.AT = AT;
-        st = make_tma_2d(&tmA, AT, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k, p.at_ld, p.bk, BM, 0);
+        st = make_tma_2d(&tmA, AT, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k, p.at_ld, p.bk, bm, 0);
     } else {
-        st = make_tma_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, m, k, BM, A_BOX_COLS, 128);
+        st = make_tma_2d(&tmA, A, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, m, k, bm, A_BOX_COLS, 128);
     }
     if (st) return st;
     if (packed) {
@@ -602,23 +637,25 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
 
     // schedule: full waves of whole tiles, the partial last wave split along k
     p.ntn = ntiles_n;
-    p.ntm = static_cast<int>(ceil_div(m, BM));
+    p.ntm = static_cast<int>(ceil_div(m, bm));
     {
         const char* ge = getenv("NM_SIMT_GROUP");
         p.gm = ge ? atoi(ge) : 8;
         if (p.gm < 1) p.gm = 1;
         if (p.gm > p.ntm) p.gm = p.ntm;
     }
-    const int ntiles = ntiles_n * static_cast<int>(ceil_div(m, BM));
+    const int ntiles = ntiles_n * static_cast<int>(ceil_div(m, bm));
     const int resident = 2 * num_sms();  // 2 CTAs per SM (launch bounds, ~105 KB smem)
     const int rem = ntiles % resident;
-    const int split = simt_split_factor(ntiles, w, p.npanels);
+    // the wave-model split is tuned for the 128-row tile; the 64-row tile is itself the sub-wave
+    // answer (NM_SIMT_SPLIT still forces a split for tests / studies)
+    const int split = bm == 128 || getenv("NM_SIMT_SPLIT") ? simt_split_factor(ntiles, w, p.npanels) : 1;
     p.split = split;
     p.full_tiles = split > 1 ? ntiles - rem : ntiles;
     float* ws = nullptr;
     int* counters = nullptr;
     if (split > 1) {
-        st = scratch_alloc(reinterpret_cast<void**>(&ws), static_cast<size_t>(rem) * split * BM * BN * sizeof(float), s);
+        st = scratch_alloc(reinterpret_cast<void**>(&ws), static_cast<size_t>(rem) * split * bm * BN * sizeof(float), s);
         if (!st) st = scratch_alloc(reinterpret_cast<void**>(&counters), static_cast<size_t>(rem) * sizeof(int), s);
         if (st) return st;
         NM_CUDA_TRY(cudaMemsetAsync(counters, 0, static_cast<size_t>(rem) * sizeof(int), s));
@@ -628,13 +665,19 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     const dim3 grid(static_cast<unsigned>(p.full_tiles + (ntiles - p.full_tiles) * split));
     const bool two = L < 32;
     if (packed)
-        st = two ? launch_simt<true, true, true>(tmA, tmB, p, grid, s) : launch_simt<false, true, true>(tmA, tmB, p, grid, s);
+        st = two ? launch_simt<128, true, true, true>(tmA, tmB, p, grid, s)
+                 : launch_simt<128, false, true, true>(tmA, tmB, p, grid, s);
+    else if (bm == 64)
+        st = use_at ? (two ? launch_simt<64, true, true, false>(tmA, tmB, p, grid, s)
+                           : launch_simt<64, false, true, false>(tmA, tmB, p, grid, s))
+                    : (two ? launch_simt<64, true, false, false>(tmA, tmB, p, grid, s)
+                           : launch_simt<64, false, false, false>(tmA, tmB, p, grid, s));
     else if (use_at)
-        st = two ? launch_simt<true, true, false>(tmA, tmB, p, grid, s)
-                 : launch_simt<false, true, false>(tmA, tmB, p, grid, s);
+        st = two ? launch_simt<128, true, true, false>(tmA, tmB, p, grid, s)
+                 : launch_simt<128, false, true, false>(tmA, tmB, p, grid, s);
     else
-        st = two ? launch_simt<true, false, false>(tmA, tmB, p, grid, s)
-                 : launch_simt<false, false, false>(tmA, tmB, p, grid, s);
+        st = two ? launch_simt<128, true, false, false>(tmA, tmB, p, grid, s)
+                 : launch_simt<128, false, false, false>(tmA, tmB, p, grid, s);
     if (ws) {
         cudaError_t e1 = cudaFreeAsync(ws, s), e2 = cudaFreeAsync(counters, s);
         if (st == NM_OK && (e1 != cudaSuccess || e2 != cudaSuccess)) st = cuda_fail(e1 != cudaSuccess ? e1 : e2, "cudaFreeAsync");

@@ -123,9 +123,11 @@ SPLIT_MEASURED = [
 
 
 @pytest.mark.parametrize("cfg,best", SPLIT_MEASURED)
-def test_plan_simt_split_matches_measured_best(L, cfg, best):
+def test_plan_simt_split_matches_measured_best(L, monkeypatch, cfg, best):
+    """The split rule of the 128-row tile (the measurements above were taken with it)."""
     from paper_2503_01253_b200 import nmspmm
     import torch
+    monkeypatch.setenv("NM_SIMT_BM", "128")
     p = nmspmm.nm_plan_query(*cfg, torch.float32)
     assert p["kernel"] == 1
     assert p["split"] == best, p
@@ -158,3 +160,26 @@ def test_plan_slot_geometry(L, cfg, bn, bm):
     p = nmspmm.nm_plan_query(*cfg, torch.bfloat16)
     assert p["kernel"] == 4
     assert (p["bn"], p["bm"]) == (bn, bm), p
+
+
+# The SIMT row tile (nm_plan_query.bm, simt_row_tile) pinned to the faster of 64 / 128 measured on
+# B200 (profiles/r02j_simt_row_tile.txt; the 128 column is the 128-row tile with its split rule).
+ROW_TILE_MEASURED = [
+    ((1024, 1024, 1024, 16, 32, 32), 64),    # 39.5 vs 47.1 us
+    ((1024, 1024, 1024, 4, 32, 32), 64),     # 22.9 vs 27.9
+    ((256, 13824, 5120, 4, 32, 32), 64),     # 114 vs 141
+    ((2048, 1376, 4096, 8, 32, 32), 64),     # 173 vs 183 (cfg3-75 % 8-GPU shard)
+    ((256, 256, 256, 2, 4, 4), 64),          # cfg1: 20.8 vs 27.2
+    ((256, 22016, 8192, 4, 32, 32), 128),    # 258 vs 280
+    ((2048, 2752, 8192, 4, 32, 32), 128),    # 303 vs 315 (cfg4-65B 8-GPU shard)
+    ((2048, 2048, 2048, 16, 32, 32), 128),   # 188 vs 193
+    ((4096, 4096, 4096, 16, 32, 32), 128),   # cfg2: 1208 vs 1200 (within 1 %)
+]
+
+
+@pytest.mark.parametrize("cfg,bm", ROW_TILE_MEASURED)
+def test_plan_simt_row_tile(L, cfg, bm):
+    from paper_2503_01253_b200 import nmspmm
+    import torch
+    p = nmspmm.nm_plan_query(*cfg, torch.float32)
+    assert p["kernel"] == 1 and p["bm"] == bm and p["threads"] == 2 * bm, p

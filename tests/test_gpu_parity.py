@@ -379,6 +379,19 @@ def test_spmm_f32_split(nm, oracle, monkeypatch, split, m, n, k, N, M, L):
     assert torch.equal(nm.nm_spmm(Ad, W), nm.nm_spmm(Ad, W))
 
 
+@pytest.mark.parametrize("bm", ["64", "128"])
+@pytest.mark.parametrize("mode", ["0", "1"])
+@pytest.mark.parametrize("m,n,k,N,M,L", [(300, 640, 512, 16, 32, 32), (97, 256, 384, 2, 4, 4),
+                                         (513, 384, 1024, 3, 8, 8), (64, 128, 2048, 4, 32, 32)])
+def test_spmm_f32_row_tiles(nm, oracle, monkeypatch, bm, mode, m, n, k, N, M, L):
+    """Both SIMT row tiles (64: 4 warps, 3 CTAs/SM; 128: 8 warps) in both A stagings, integer inputs
+    bit-exact (ragged m and n, the TWO path at L = 4, odd N)."""
+    monkeypatch.setenv("NM_SIMT_BM", bm)
+    monkeypatch.setenv("NM_SIMT_MODE", mode)
+    A, vals, D, C = run_f32(nm, oracle, m, n, k, N, M, L, kind="integer", seed=7)
+    assert np.array_equal(C.astype(np.float64), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L))
+
+
 # --------------------------------------------------------------- prepacked weights (P:470-475 offline step)
 @pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
 @pytest.mark.parametrize("path", ["sp", "generic"])
