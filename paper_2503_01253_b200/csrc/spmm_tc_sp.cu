@@ -173,7 +173,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     unsigned long long t_start = 0;
-    if ((p.dbg & 256) && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    long long c_start = 0, c_acc = 0;
+    if ((p.dbg & 256) && threadIdx.x == 0) {
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+        c_start = clock64();
+    }
     // 1-D grid, token tiles fastest (the CTAs that share a column tile's weight stream run
     // together, so it is read from DRAM once and served from L2 to the others).  The last,
     // partial wave's tiles are split in two stage ranges ("tail split"): part 1 leaves an fp32
@@ -364,6 +368,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_wait(acc_full, 0);
         tc_fence_after();
         if (warp == 0) SP_TS(nst, 7);
+        if ((p.dbg & 256) && threadIdx.x == 0) c_acc = clock64();
         const int qw = warp & 3;
         // split tiles (nparts > 1): the first nparts - 1 CTAs of a tile to finish publish their fp32
         // partials in ws; the last one (by ticket) waits for them -- they hold tickets, so they are
@@ -541,16 +546,20 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
     }
-    if ((p.dbg & 256) && threadIdx.x == 0) {  // timeline study: [start ns, end ns, smid, stages]
+    if ((p.dbg & 256) && threadIdx.x == 0) {  // timeline study: [start ns, end ns, smid, stages, clk: start, accumulators done, end]
         unsigned long long t_end;
         uint32_t smid;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        long long* o = static_cast<long long*>(p.C) + 4 * static_cast<int64_t>(blockIdx.x);
+        long long* o = static_cast<long long*>(p.C) + 8 * static_cast<int64_t>(blockIdx.x);
         o[0] = static_cast<long long>(t_start);
         o[1] = static_cast<long long>(t_end);
         o[2] = smid;
         o[3] = nst;
+        o[4] = c_start;
+        o[5] = c_acc;
+        o[6] = clock64();
+        o[7] = 0;
     }
 }
 
