@@ -507,11 +507,11 @@ int64_t nm_spmm_host_ws_bytes(int64_t m, int64_t n, int64_t k, int N, int M, int
 
 }  // extern "C"
 namespace nm {
-// Row chunks for the host path's copy/compute overlap: fp32 SIMT only (the per-call prepack of
-// the tensor-core paths would be repeated per chunk); 4 chunks of whole 128-row tiles once m >=
-// 1024.  Measured on B200 (profiles/r01p_host_e2e_chunks.txt): 4 chunks beat 2 and 3 at cfg2
-// and cfg4-65B even where a chunk's grid ends in a partial wave -- the overlap gained exceeds
-// the quantization lost (6 / 8 chunks: no better at cfg2, +5 % at cfg4).  NM_HOST_CHUNKS=1..8
+// Row chunks for the host path's copy/compute overlap (nch + 1 chunks sized 1 : 2 : .. : 2 : 1, see
+// nm_spmm_host): nch = 4 once m >= 1024, 8 for the fp32 SIMT kernel once m >= 2048.  Measured on
+// B200 (profiles/r01p_host_e2e_chunks.txt with equal chunks: 4 beat 2 and 3 at cfg2 and cfg4-65B
+// even where a chunk's grid ends in a partial wave; profiles/r02l_host_e2e.txt with the 1:2:..:1
+// sizes: cfg2 3.04 -> 2.88 ms (4) / 2.79 ms (8), cfg4-65B 6.0 -> 5.73 / 5.58 ms).  NM_HOST_CHUNKS=1..8
 // overrides (ablation).
 // kernel: the selector's choice; the slot kernels (bf16 / tf32 sparse TC) chunk too, with the
 // weight prepacked once per call ahead of the chunks.
@@ -522,6 +522,7 @@ static int host_chunks(int64_t m, int kernel, nm_math math) {
     const bool simt = kernel == K_SIMT_F32 && (math == NM_MATH_AUTO || math == NM_MATH_F32_SIMT);
     if (!simt && kernel != K_TC_SP && kernel != K_TC_TF32) return 1;
     if (force) return force;
+    if (simt && m >= 2048) return 8;  // 1:2:..:2:1 sizing, fp32: 8 beats 4 by 3 % at cfg2 / cfg4-65B (r02l)
     return m >= 1024 ? 4 : 1;
 }
 }  // namespace nm
@@ -561,8 +562,18 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     // Row chunks of A / C, three-stage pipeline: H2D of chunk i+1 (copy stream) and D2H of chunk
     // i-1 (second copy stream) overlap the SpMM of chunk i (the caller's stream).  Every chunk
     // is the same product on a row range, so C is unchanged up to the k-split of sub-wave grids
-    // (fixed order).
-    const int64_t rc = ceil_div(ceil_div(m, nch), 128) * 128;
+    // (fixed order).  Chunk sizes 1 : 2 : ... : 2 : 1 (nch + 1 chunks, whole 128-row
+    // tiles): the first chunk is on the critical path behind the weight upload and the last
+    // chunk's D2H after the last SpMM, so both are half-size (CUPTI timeline at cfg2,
+    // profiles/r02l_host_timeline.txt: equal chunks leave ~0.3 ms of D2H and the first chunk's
+    // H2D exposed).
+    const int nck = nch + 1;
+    int64_t rb[10];
+    rb[0] = 0;
+    for (int i = 1; i < nck; ++i) rb[i] = std::min(m, ceil_div(m * (2 * i - 1), 2 * static_cast<int64_t>(nch) * 128) * 128);
+    rb[nck] = m;
+    int64_t rc = 0;  // the largest chunk (the slot kernels' H is chosen for it)
+    for (int i = 0; i < nck; ++i) rc = std::max(rc, rb[i + 1] - rb[i]);
     // slot kernels: prepack the weight once (the paper's offline step, here per call) on s
     const bool slot = kernel == K_TC_SP || kernel == K_TC_TF32, tf = kernel == K_TC_TF32;
     const int hsp = tc_sp_halves_m(N, M, L, rc, n, k);  // the chunk's token count
@@ -576,7 +587,7 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
         }
     }
     cudaStream_t hs = nullptr, ds = nullptr;
-    cudaEvent_t ev[2 * 8 + 1] = {};
+    cudaEvent_t ev[2 * 9 + 1] = {};
     auto cleanup = [&]() {
         for (cudaEvent_t x : ev)
             if (x) cudaEventDestroy(x);
@@ -586,10 +597,10 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
     };
     cudaError_t ce = cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking);
     if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking);
-    for (int i = 0; ce == cudaSuccess && i < 2 * nch + 1; ++i) ce = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
-    for (int i = 0; ce == cudaSuccess && i < nch; ++i) {
-        const int64_t r0 = i * rc, r1 = std::min(m, r0 + rc);
-        if (r0 >= r1) break;
+    for (int i = 0; ce == cudaSuccess && i < 2 * nck + 1; ++i) ce = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    for (int i = 0; ce == cudaSuccess && i < nck; ++i) {
+        const int64_t r0 = rb[i], r1 = rb[i + 1];
+        if (r0 >= r1) continue;
         ce = cudaMemcpyAsync(dA + r0 * k * e, static_cast<const uint8_t*>(A_host) + r0 * k * e,
                              static_cast<size_t>((r1 - r0) * k * e), cudaMemcpyHostToDevice, hs);
         if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i], hs);
@@ -609,8 +620,8 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
             ce = cudaMemcpyAsync(static_cast<uint8_t*>(C_host) + r0 * n * ec, dC + r0 * n * ec,
                                  static_cast<size_t>((r1 - r0) * n * ec), cudaMemcpyDeviceToHost, ds);
     }
-    if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * nch], ds);
-    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * nch], 0);  // the caller's stream sees C_host
+    if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * nck], ds);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * nck], 0);  // the caller's stream sees C_host
     const cudaError_t se = cudaStreamSynchronize(s);
     cudaStreamSynchronize(hs);
     cudaStreamSynchronize(ds);

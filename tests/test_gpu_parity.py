@@ -628,12 +628,13 @@ def test_sp_pack_warp_matches_sequential(nm, monkeypatch, dt, k, n, N, M, L):
     assert torch.equal(fast.buf, ref.buf)
 
 
-@pytest.mark.parametrize("chunks", ["1", "2", "3", "4"])
-def test_spmm_host_path_chunked(nm, oracle, monkeypatch, chunks):
-    """nm_spmm_host's copy/compute overlap (row chunks on separate copy streams) gives the
-    oracle's result for every chunk count, including a ragged last chunk."""
+@pytest.mark.parametrize("chunks,m", [("1", 700), ("2", 700), ("3", 700), ("4", 700), ("8", 700), ("0", 2100)])
+def test_spmm_host_path_chunked(nm, oracle, monkeypatch, chunks, m):
+    """nm_spmm_host's copy/compute overlap (row chunks 1 : 2 : .. : 2 : 1 on separate copy streams)
+    gives the oracle's result for every chunk count, including a ragged last chunk, empty chunks
+    (8 at m = 700) and the default (0: 9 chunks at m = 2100)."""
     monkeypatch.setenv("NM_HOST_CHUNKS", chunks)
-    m, n, k, N, M, L = 700, 512, 1024, 8, 32, 32
+    n, k, N, M, L = 512, 1024, 8, 32, 32
     A = synth.uniform((m, k), 43, 1)
     B = synth.uniform((k, n), 44, 2)
     vals, D = oracle.compress(B, N, M, L)
