@@ -428,62 +428,81 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int eb = p.c_bf16 ? 2 : 4;
             const int rowb = MC * eb;
             const uint32_t tbase = tmem + (static_cast<uint32_t>(qw * 32) << 16);
-#pragma unroll 1
-            for (int t0 = (warp >> 2) * 32; t0 < NT; t0 += 64) {
+            // (chunk, half) items j = 0 .. J - 1 of this warp: t0 = (warp / 4 + 2 (j / H)) 32, h = j % H.
+            // The TMEM load of item j + 1 is issued before item j is converted and staged, so its
+            // latency overlaps the stores (tcgen05.wait::ld then waits for it); two register sets.
+            const int J = H * (((NT + 31) / 32 - (warp >> 2) + 1) / 2);
+            auto item_t0 = [&](int j) { return ((warp >> 2) + 2 * (j / H)) * 32; };
+            auto stage = [&](uint32_t (&v)[32], int j) {
+                const int t0 = item_t0(j), h = j % H;
                 uint8_t* buf = smem + (t0 / 32) * 32 * rowb;
+                if (wpart) {  // sum of the parts in the order 0 .. nparts-1 (this CTA's own from TMEM)
+                    const int nv = NT - t0 < 32 ? NT - t0 : 32;
+                    float a[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) a[i] = 0.f;
 #pragma unroll 1
-                for (int h = 0; h < H; ++h) {
-                    uint32_t v[32];
-                    if (nst > 0) {
-                        tmem_ld32(tbase + h * NT + t0, v);
-                        tmem_wait_ld();
-                    } else {
+                    for (int q2 = 0; q2 < nparts; ++q2) {
+                        if (q2 == part) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = 0u;
-                    }
-                    if (wpart) {  // sum of the parts in the order 0 .. nparts-1 (this CTA's own from TMEM)
-                        const int nv = NT - t0 < 32 ? NT - t0 : 32;
-                        float a[32];
+                            for (int i = 0; i < 32; ++i) a[i] += __uint_as_float(v[i]);
+                        } else {
+                            const float* src = wpart + static_cast<int64_t>(q2) * MC * NT + static_cast<int64_t>(t0) * MC +
+                                               h * 128 + qw * 32 + lane;
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) a[i] = 0.f;
-#pragma unroll 1
-                        for (int q2 = 0; q2 < nparts; ++q2) {
-                            if (q2 == part) {
-#pragma unroll
-                                for (int i = 0; i < 32; ++i) a[i] += __uint_as_float(v[i]);
-                            } else {
-                                const float* src = wpart + static_cast<int64_t>(q2) * MC * NT + static_cast<int64_t>(t0) * MC +
-                                                   h * 128 + qw * 32 + lane;
-#pragma unroll
-                                for (int i = 0; i < 32; ++i)
-                                    if (i < nv) a[i] += __ldcg(src + static_cast<int64_t>(i) * MC);
-                            }
+                            for (int i = 0; i < 32; ++i)
+                                if (i < nv) a[i] += __ldcg(src + static_cast<int64_t>(i) * MC);
                         }
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(a[i]);
                     }
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.alpha);
-                    uint8_t* cb = buf + (h * 128 + qw * 32 + lane) * eb;
-                    // NT % 32 == 16 (176, 208 tokens): the last chunk holds 16 tokens of this tile
-                    const int rows = NT - t0 < 32 ? NT - t0 : 32;
-                    if (p.c_bf16) {
+                    for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(a[i]);
+                }
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i < rows)
-                                *reinterpret_cast<__nv_bfloat16*>(cb + i * rowb) = __float2bfloat16_rn(__uint_as_float(v[i]));
-                    } else {
+                for (int i = 0; i < 32; ++i) v[i] = __float_as_uint(__uint_as_float(v[i]) * p.alpha);
+                uint8_t* cb = buf + (h * 128 + qw * 32 + lane) * eb;
+                // NT % 32 == 16 (176, 208 tokens): the last chunk holds 16 tokens of this tile
+                const int rows = NT - t0 < 32 ? NT - t0 : 32;
+                if (p.c_bf16) {
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            if (i < rows) *reinterpret_cast<uint32_t*>(cb + i * rowb) = v[i];
+                    for (int i = 0; i < 32; ++i)
+                        if (i < rows)
+                            *reinterpret_cast<__nv_bfloat16*>(cb + i * rowb) = __float2bfloat16_rn(__uint_as_float(v[i]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (i < rows) *reinterpret_cast<uint32_t*>(cb + i * rowb) = v[i];
+                }
+                if (h == H - 1) {  // the chunk is complete in shared memory: one TMA store
+                    fence_proxy_async_smem();
+                    named_bar_sync(1 + (warp >> 2), 128);
+                    if (qw == 0 && lane == 0 && !(p.dbg & (8 | 64 | 256))) {
+                        tma_store_2d(NT - t0 < 32 ? &tmC16 : &tmC, buf, tile * MC, m0 + t0);
+                        bulk_commit();
                     }
                 }
-                fence_proxy_async_smem();
-                named_bar_sync(1 + (warp >> 2), 128);
-                if (qw == 0 && lane == 0 && !(p.dbg & (8 | 64 | 256))) {
-                    tma_store_2d(NT - t0 < 32 ? &tmC16 : &tmC, buf, tile * MC, m0 + t0);
-                    bulk_commit();
+            };
+            auto load = [&](uint32_t (&v)[32], int j) {
+                if (nst > 0) {
+                    tmem_ld32(tbase + (j % H) * NT + item_t0(j), v);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) v[i] = 0u;
                 }
+            };
+            uint32_t va[32], vb[32];
+            if (J > 0) {
+                load(va, 0);
+                tmem_wait_ld();
+            }
+#pragma unroll 1
+            for (int j = 0; j < J; j += 2) {
+                if (j + 1 < J) load(vb, j + 1);
+                stage(va, j);
+                tmem_wait_ld();
+                if (j + 1 >= J) break;
+                if (j + 2 < J) load(va, j + 2);
+                stage(vb, j + 1);
+                tmem_wait_ld();
             }
             if (qw == 0 && lane == 0) bulk_wait_read0();
         } else {
