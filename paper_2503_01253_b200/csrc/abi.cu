@@ -347,7 +347,78 @@ static int simt_mode(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
     return 1;
 }
 
-enum KernelId { K_GENERIC = 0, K_SIMT_F32 = 1, K_TC_BF16 = 2, K_TC_TF32 = 3, K_TC_SP = 4 };
+enum KernelId { K_GENERIC = 0, K_SIMT_F32 = 1, K_TC_BF16 = 2, K_TC_TF32 = 3, K_TC_SP = 4, K_SIMT_BF16 = 5 };
+
+// bf16 operands the slot kernel cannot take (L not in {16, 32, 64, 128}, k % 8 != 0, e.g. cfg5's
+// L = 4): the fp32 SIMT kernel on exact fp32 copies of A and B' (bf16 -> fp32 is exact, and so is
+// every product), C rounded to bf16 (RNE) after the fp32 accumulation when c_dt is bf16 -- instead
+// of the one-thread-per-element generic kernel.  NM_BF16_SIMT=0 disables (tests of the generic
+// kernel).  The shape conditions are the SIMT kernel's on 16-B-aligned scratch copies.
+static bool simt_bf16_ok(int64_t m, int64_t n, int64_t k, int N, int M, int L) {
+    const char* e = getenv("NM_BF16_SIMT");
+    if (e && e[0] == '0') return false;
+    alignas(16) static const float dummy[4] = {0, 0, 0, 0};
+    return simt_f32_applicable(dummy, dummy, dummy, m, n, k, N, M, L);
+}
+
+__global__ void widen_bf16_kernel(const __nv_bfloat16* __restrict__ in, float* __restrict__ out, int64_t count) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const int64_t nv = count / 8;  // 8 elements (16 B in, 32 B out) per step; the scratch / caller
+                                   // buffers are 16-B aligned (checked by the caller)
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < nv; i += stride) {
+        const uint4 v = reinterpret_cast<const uint4*>(in)[i];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        float4 a, b;
+        a.x = __uint_as_float(w[0] << 16), a.y = __uint_as_float(w[0] & 0xffff0000u);
+        a.z = __uint_as_float(w[1] << 16), a.w = __uint_as_float(w[1] & 0xffff0000u);
+        b.x = __uint_as_float(w[2] << 16), b.y = __uint_as_float(w[2] & 0xffff0000u);
+        b.z = __uint_as_float(w[3] << 16), b.w = __uint_as_float(w[3] & 0xffff0000u);
+        reinterpret_cast<float4*>(out)[2 * i] = a;
+        reinterpret_cast<float4*>(out)[2 * i + 1] = b;
+    }
+    for (int64_t i = nv * 8 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
+        out[i] = __bfloat162float(in[i]);
+}
+__global__ void narrow_f32_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out, int64_t count) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += stride)
+        out[i] = __float2bfloat16_rn(in[i]);
+}
+
+static nm_status simt_bf16_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m,
+                                  int64_t n, int64_t k, int N, int M, int L, int mode, float alpha, cudaStream_t s) {
+    const int64_t w = k / M * N;
+    if ((reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(Bv) & 15))
+        return fail(NM_ERR_ALIGNMENT, "bf16 SIMT path: A and values must be 16-B aligned");
+    float *fa = nullptr, *fb = nullptr, *fc = nullptr;
+    auto release = [&]() {
+        if (fa) cudaFreeAsync(fa, s);
+        if (fb) cudaFreeAsync(fb, s);
+        if (fc) cudaFreeAsync(fc, s);
+    };
+    nm_status st = scratch_alloc(reinterpret_cast<void**>(&fa), static_cast<size_t>(m * k) * 4, s);
+    if (!st) st = scratch_alloc(reinterpret_cast<void**>(&fb), static_cast<size_t>(w * n) * 4, s);
+    if (!st && c_bf16) st = scratch_alloc(reinterpret_cast<void**>(&fc), static_cast<size_t>(m * n) * 4, s);
+    if (st) {
+        release();
+        return st;
+    }
+    const unsigned blocks = static_cast<unsigned>(4 * num_sms());
+    widen_bf16_kernel<<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(A), fa, m * k);
+    note_launch();
+    widen_bf16_kernel<<<blocks, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(Bv), fb, w * n);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) st = cuda_fail(e, "widen_bf16_kernel");
+    if (!st) st = simt_f32_launch(fa, fb, D, c_bf16 ? fc : static_cast<float*>(C), m, n, k, N, M, L, mode, s, nullptr, alpha);
+    if (!st && c_bf16) {
+        narrow_f32_kernel<<<blocks, 256, 0, s>>>(fc, static_cast<__nv_bfloat16*>(C), m * n);
+        note_launch();
+        if ((e = cudaGetLastError()) != cudaSuccess) st = cuda_fail(e, "narrow_f32_kernel");
+    }
+    release();
+    return st;
+}
 
 static nm_status select(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                         int L, nm_dtype ab, nm_dtype cd, nm_math math, int* kernel, nm_math* used) {
@@ -371,7 +442,7 @@ static nm_status select(const void* A, const void* Bv, const void* C, int64_t m,
     }
     if (math == NM_MATH_AUTO || math == NM_MATH_BF16_TC) {
         *used = NM_MATH_BF16_TC;
-        *kernel = tc_sp_ok(A, C, m, n, k, N, M, L) ? K_TC_SP : K_GENERIC;
+        *kernel = tc_sp_ok(A, C, m, n, k, N, M, L) ? K_TC_SP : simt_bf16_ok(m, n, k, N, M, L) ? K_SIMT_BF16 : K_GENERIC;
         return NM_OK;
     }
     return fail(NM_ERR_UNSUPPORTED, "math mode not available for bf16 operands");
@@ -480,6 +551,9 @@ nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, 
         fused = true;
     } else if (kernel == K_TC_SP || kernel == K_TC_TF32) {
         st = tc_sp_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, kernel == K_TC_TF32, s, alpha);
+        fused = true;
+    } else if (kernel == K_SIMT_BF16) {
+        st = simt_bf16_launch(A, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, simt_mode(m, n, k, N, M, L), alpha, s);
         fused = true;
     } else if (ab_dt == NM_F32) {
         st = generic_launch<float, float>(A, values, idx, C, m, n, k, N, M, L, s);
@@ -648,7 +722,7 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
     out->math = used;
     out->kernel = kernel;
     const int sms = num_sms();
-    if (kernel == K_SIMT_F32) {
+    if (kernel == K_SIMT_F32 || kernel == K_SIMT_BF16) {
         int wp, bk, bkw;
         simt_f32_geometry(N, M, &wp, &bk, &bkw);
         const int bm = simt_row_tile(m, n);

@@ -162,6 +162,19 @@ def test_plan_slot_geometry(L, cfg, bn, bm):
     assert (p["bn"], p["bm"]) == (bn, bm), p
 
 
+@pytest.mark.parametrize("cfg,kid", [((1024, 1024, 1024, 8, 32, 4), 5),   # cfg5 L = 4: bf16 on the SIMT kernel
+                                     ((256, 256, 256, 2, 4, 4), 5),      # cfg1 pattern
+                                     ((64, 96, 192, 3, 8, 12), 5),       # L = 12
+                                     ((64, 99, 192, 3, 8, 3), 0),        # L % 4 != 0: generic
+                                     ((1024, 1024, 1024, 8, 32, 32), 4)])  # the slot kernel
+def test_plan_bf16_fallback(L, cfg, kid):
+    """bf16 shapes the slot kernel cannot take go to the fp32 SIMT kernel (exact fp32 copies),
+    not the one-thread-per-element generic kernel, unless the SIMT kernel's shape rules fail."""
+    from paper_2503_01253_b200 import nmspmm
+    import torch
+    assert nmspmm.nm_plan_query(*cfg, torch.bfloat16)["kernel"] == kid
+
+
 # The SIMT row tile (nm_plan_query.bm, simt_row_tile) pinned to the faster of 64 / 128 measured on
 # B200 (profiles/r02j_simt_row_tile.txt; the 128 column is the 128-row tile with its split rule).
 ROW_TILE_MEASURED = [

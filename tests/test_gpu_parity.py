@@ -272,18 +272,57 @@ TC_CASES = [
 ]
 
 
-TC_PATHS = {"sp": ("1", 4), "generic": ("0", 0)}  # NM_TC_SP, kernel id (0: the generic correctness kernel)
+# NM_TC_SP, NM_BF16_SIMT, kernel id (0: the generic correctness kernel, 5: bf16 on the fp32 SIMT kernel)
+TC_PATHS = {"sp": ("1", "1", 4), "generic": ("0", "0", 0), "simt": ("0", "1", 5)}
 
 
 def use_tc_path(monkeypatch, path):
-    sp, kid = TC_PATHS[path]
+    sp, simt, kid = TC_PATHS[path]
     monkeypatch.setenv("NM_TC_SP", sp)
+    monkeypatch.setenv("NM_BF16_SIMT", simt)
     return kid
+
+
+BF16_SIMT_CASES = [
+    # (m, n, k, N, M, L): L outside {16, 32, 64, 128} -> bf16 on the fp32 SIMT kernel by default
+    (256, 256, 256, 2, 4, 4),       # cfg1's pattern on bf16
+    (300, 512, 1024, 8, 32, 4),     # cfg5's L = 4, ragged m
+    (129, 264, 512, 4, 32, 8),      # L = 8, ragged m and n tile
+    (64, 96, 192, 3, 8, 12),        # L = 12, odd N
+]
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L", BF16_SIMT_CASES)
+@pytest.mark.parametrize("cdt", [torch.bfloat16, torch.float32])
+def test_spmm_bf16_simt_default_path(nm, oracle, monkeypatch, m, n, k, N, M, L, cdt):
+    """bf16 operands whose L the slot kernel cannot take run the fp32 SIMT kernel on exact fp32
+    copies (kernel id 5, AUTO and bf16_tc): uniform inputs within the bf16 bar, integer inputs
+    bit-exact with fp32 C, and bf16 C = RNE of the exact result."""
+    monkeypatch.delenv("NM_TC_SP", raising=False)
+    monkeypatch.delenv("NM_BF16_SIMT", raising=False)
+    for math in ("auto", "bf16_tc"):
+        assert nm.nm_plan_query(m, n, k, N, M, L, torch.bfloat16, math)["kernel"] == 5
+    A = synth.bf16grid((m, k), 61, synth.TID_A)
+    B = synth.bf16grid((k, n), 62, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A, torch.bfloat16), W, out_dtype=cdt).float().cpu().numpy()
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
+    assert oracle.rel_frobenius(C, ref) <= TOL_BF16
+    Ai = synth.integer((m, k), 63, synth.TID_A)
+    vi, Di = oracle.compress(synth.integer((k, n), 64, synth.TID_B), N, M, L)
+    Wi = nm.NmWeight(dev(vi, torch.bfloat16), dev(Di, torch.uint8), k, N, M, L)
+    Ci = nm.nm_spmm(dev(Ai, torch.bfloat16), Wi, out_dtype=cdt).float().cpu().numpy()
+    refi = oracle.spmm_sparse_f64(Ai, vi, Di, k, N, M, L)
+    if cdt == torch.float32:
+        assert np.array_equal(Ci.astype(np.float64), refi)
+    else:  # |C| <= 4 w < 2^24: exact in fp32, then one RNE to bf16 (torch's rounding of the exact value)
+        assert np.array_equal(Ci, torch.from_numpy(refi).float().bfloat16().float().numpy())
 
 
 @pytest.mark.parametrize("m,n,k,N,M,L", TC_CASES)
 @pytest.mark.parametrize("cdt", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("path", ["sp", "generic"])
+@pytest.mark.parametrize("path", ["sp", "generic", "simt"])
 def test_spmm_tc_bf16_vs_oracle(nm, oracle, monkeypatch, m, n, k, N, M, L, cdt, path):
     kid = use_tc_path(monkeypatch, path)
     A = synth.bf16grid((m, k), 51, synth.TID_A)
@@ -754,7 +793,8 @@ SCALED_PATHS = [  # (name, ab dtype, math, env, expected kernel id)
     ("simt", torch.float32, "f32_simt", {}, 1),
     ("generic", torch.float32, "f32_simt", {}, 0),          # L = 3 -> generic kernel + scaling pass
     ("sp_bf16", torch.bfloat16, "bf16_tc", {}, 4),
-    ("generic_bf16", torch.bfloat16, "bf16_tc", {"NM_TC_SP": "0"}, 0),
+    ("generic_bf16", torch.bfloat16, "bf16_tc", {"NM_TC_SP": "0", "NM_BF16_SIMT": "0"}, 0),
+    ("simt_bf16", torch.bfloat16, "bf16_tc", {"NM_TC_SP": "0"}, 5),   # alpha fused into the SIMT epilogue
     ("tf32", torch.float32, "tf32_tc", {}, 3),
 ]
 
