@@ -139,6 +139,11 @@ nm_status nm_validate(const uint8_t* idx, int64_t k, int64_t n, int N, int M, in
  *                                                        tensor-core kernel (tcgen05.mma.sp over the
  *                                                        offline slot packing) when L is 16/32/64/128,
  *                                                        k % 8 == 0, A 16-B and C 4-B aligned; else
+ *                                                        the fp32 SIMT kernel on exact fp32 copies of
+ *                                                        A and values (scratch from the library pool;
+ *                                                        C rounded to bf16 after the fp32 sum; needs
+ *                                                        the SIMT shape rules below and A / values
+ *                                                        16-B aligned, else NM_ERR_ALIGNMENT); else
  *                                                        the generic kernel (one thread per element)
  *                         NM_MATH_AUTO                -> selector (nm_plan_query)
  * bf16 / tf32 without a prepack re-pack the weight on every call (ms); use
