@@ -63,7 +63,8 @@ VARIANTS = ["cfg1:f32", "cfg2:bf16", "cfg3_62:f32", "cfg3_75:f32", "cfg4_13b:f32
             "cfg4_13b:bf16", "cfg4_13b_sq:bf16", "cfg4_65b_sq:bf16", "cfg4_65b:bf16", "cfg4_65b_m256:bf16",
             "cfg4_13b_m256:bf16", "cfg2:tf32", "cfg3_62:tf32", "cfg3_75:tf32",
             "cfg4_65b:tf32", "cfg2_shard8:f32", "cfg3_75_shard8:f32", "cfg4_65b_shard8:f32",
-            "cfg2_shard8:bf16", "cfg3_75_shard8:bf16", "cfg4_65b_shard8:bf16"]  # tf32 = fp32 operands on the tf32 sparse tensor cores (opt-in math)
+            "cfg2_shard8:bf16", "cfg3_75_shard8:bf16", "cfg4_65b_shard8:bf16", "cfg2:bf16at", "cfg2:f32at",
+            "cfg4_65b:bf16at"]  # ...at: feature-major activations (A^T given, no per-call transpose)  # tf32 = fp32 operands on the tf32 sparse tensor cores (opt-in math)
 
 
 def load_peaks():
@@ -146,12 +147,20 @@ def make_inputs(cfg, dtype, device, seed=0):
     return A, Bd, W
 
 
-def make_step(A, W, C, dtype, math=None):
+def make_step(A, W, C, dtype, math=None, at=False):
     '''One hot-path step.  fp32: nm_spmm (CUDA-core path).  bf16 and tf32 (fp32 operands,
     math="tf32_tc"): the weight is prepacked once, outside the timed region (the paper's
-    offline PreProcessing), and the step is nm_spmm_prepacked.'''
+    offline PreProcessing), and the step is nm_spmm_prepacked.  at=True (variants
+    "f32at" / "bf16at"): the activations arrive feature-major (A^T, nm_spmm_at /
+    nm_spmm_prepacked_at), so the step has no per-call transpose.'''
     import torch
     from paper_2503_01253_b200 import nmspmm
+    if at:
+        At = A.t().contiguous()  # the caller's layout (untimed)
+        if dtype == torch.float32:
+            return lambda: nmspmm.nm_spmm_at(At, W, out=C, math="f32_simt")
+        PWa = nmspmm.nm_prepack(W)
+        return lambda: nmspmm.nm_spmm_prepacked_at(At, PWa, out=C)
     if math == "tf32_tc":
         PWt = nmspmm.nm_prepack(W, math="tf32_tc")
         return lambda: nmspmm.nm_spmm_prepacked(A, PWt, out=C)
@@ -191,13 +200,13 @@ def alg_bytes(cfg, e):
     return e * m * k + e * w * n + w * q + e * m * n
 
 
-def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True, math=None):
+def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True, math=None, at=False):
     import torch
     from paper_2503_01253_b200 import nmspmm
     stream = torch.cuda.current_stream()
     A, Bd, W = make_inputs(cfg, dtype, "cuda")
     C = torch.empty(cfg[0], cfg[1], dtype=dtype, device="cuda")
-    step = make_step(A, W, C, dtype, math)
+    step = make_step(A, W, C, dtype, math, at)
     for _ in range(warmup):
         step()
     nmspmm.nm_profile_begin()
@@ -440,12 +449,14 @@ def run_ours(args):
         line["cpu_baseline"] = cpu_baseline(cfg, target_s=args.ref_seconds)
         variants = []
         for item in args.variants.split(",") if args.variants else []:
-            name, _, vdt = item.partition(":")
-            vdt = vdt or args.dtype
+            name, _, vdt_full = item.partition(":")
+            vdt_full = vdt_full or args.dtype
+            at = vdt_full.endswith("at")  # feature-major activations (A^T given): no per-call transpose
+            vdt = vdt_full[:-2] if at else vdt_full
             vcfg = CONFIGS[name]
             tdt = torch.bfloat16 if vdt == "bf16" else torch.float32
             r, _ = measure_config(vcfg, tdt, max(5, args.steps // 2), args.warmup, flush,
-                                  math="tf32_tc" if vdt == "tf32" else None)
+                                  math="tf32_tc" if vdt == "tf32" else None, at=at)
             # tf32 dense peak = the measured bf16 peak x the nominal tf32/bf16 ratio 1/2
             peak_v = (fp32_alu_peak_tflops(sm_mhz) if vdt == "f32" else
                       peaks.get("bf16_tflops", 1590.0) / (2.0 if vdt == "tf32" else 1.0))
@@ -456,6 +467,7 @@ def run_ours(args):
             t_m = alg_bytes(vcfg, e_v) / (peaks.get("hbm_gbs", 6650.0) * 1e9)
             t_k = r["kernel_ms"] * 1e-3
             variants.append({"config": name, "dtype": vdt, "m_n_k": vcfg[:3], "N:M": f"{vcfg[3]}:{vcfg[4]}",
+                             "a_layout": "A^T given (nm_spmm_at)" if at else "A row-major",
                              "L": vcfg[5], "tflops": round(r["tflops"], 3), "ms": round(r["ms"], 4),
                              "kernel_tflops": round(r["kernel_tflops"], 3), "kernel_ms": round(r["kernel_ms"], 5),
                              "roofline_frac": round(max(t_c, t_m) / t_k, 4),
@@ -470,7 +482,7 @@ def run_ours(args):
             torch.cuda.empty_cache()
         # kernel-only 8-GPU scaling of the column-sharded layer from one GPU: the full config's kernel
         # time over 8 x one shard's (the all-gather is not included; SURVEY 8(e) reporting (i))
-        kms = {(u["config"], u["dtype"]): u["kernel_ms"] for u in variants}
+        kms = {(u["config"], u["dtype"]): u["kernel_ms"] for u in variants if u["a_layout"] == "A row-major"}
         if roof.get("kernel_ms_per_launch"):
             kms.setdefault((args.config, args.dtype), roof["kernel_ms_per_launch"])
         for v in variants:

@@ -255,6 +255,21 @@ int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt)
 nm_status nm_prepack(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
                      void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
 nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt, void* stream);
+
+/* nm_spmm_at / nm_spmm_prepacked_at -- the same product with A supplied TRANSPOSED (feature-major
+ * activations): At is k x lda row-major, At[kk * lda + i] = A[i][kk], lda >= m (the columns
+ * m .. lda-1 are never used in C).  Both kernels consume A^T internally (the SIMT kernel stages
+ * A^T panels, the slot kernels gather rows of A^T), so this form skips the per-call transpose
+ * (Eq. 1 unchanged; results identical to nm_spmm / nm_spmm_prepacked bit for bit).
+ *   At : device, 16-B aligned, lda * element size a multiple of 16 B; C : m x n row-major.
+ *   Paths: fp32 -> the SIMT kernel (staged A^T mode); bf16 / tf32 -> the slot kernels (padding
+ *   slots are zero-filled by the gather, no zero row needed).  Other selections (the generic
+ *   kernel, bf16 on the SIMT kernel) return NM_ERR_UNSUPPORTED; misalignment NM_ERR_ALIGNMENT;
+ *   lda < m NM_ERR_SHAPE.  Asynchronous on `stream`. */
+nm_status nm_spmm_at(const void* At, int64_t lda, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
+                     int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math, void* stream);
+nm_status nm_spmm_prepacked_at(const void* At, int64_t lda, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt,
+                               void* stream);
 /* The same with the math the prepacked weight will run with: nm_prepack == nm_prepack_ex(...,
  * NM_MATH_AUTO, ...).  dt NM_F32 + NM_MATH_TF32_TC gives kind 3 (tf32 slot images, 1:2 slot
  * pairs, values rounded to tf32) when the tf32 path applies to the weight's shape, else kind 0;

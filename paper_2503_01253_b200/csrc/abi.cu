@@ -236,7 +236,8 @@ int simt_split_factor(int ntiles, int64_t w, int npanels);
 int simt_row_tile(int64_t m, int64_t n);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
-                          float alpha = 1.f, const uint32_t* Dw = nullptr);
+                          float alpha = 1.f, const uint32_t* Dw = nullptr, const float* At_in = nullptr,
+                          int64_t lda = 0);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 // tf: fp32 operands on the tf32 sparse tensor cores (1:2 slot pairs), else bf16 (2:4 slot quads)
 size_t tc_sp_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, bool tf);  // bound (no data)
@@ -246,9 +247,11 @@ void tc_sp_geometry(int64_t m, int64_t n, int64_t k, int N, int M, int L, int* h
 nm_status tc_sp_prepack(const void* Bv, const uint8_t* D, int64_t n, int64_t k, int N, int M, int L, bool tf, int H,
                         void* buf, int64_t buf_bytes, int64_t* exact, bool query_only, cudaStream_t s);
 nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
-                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po = nullptr, float alpha = 1.f);
+                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po = nullptr, float alpha = 1.f,
+                    const void* At_in = nullptr, int64_t lda = 0);
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha = 1.f);
+                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha = 1.f,
+                       const void* At_in = nullptr, int64_t lda = 0);
 
 // Sparse-tensor-core slot path (spmm_tc_sp.cu): bf16, L in {16, 32, 64, 128}, A 16-B aligned with
 // k % 8 == 0 (the per-call transpose reads 16-B chunks), C 4-B aligned.  NM_TC_SP=0 disables it.
@@ -913,6 +916,67 @@ nm_status nm_spmm_prepacked(const void* A, const nm_prepacked* w, void* C, int64
     }
     return nm_spmm(A, w->values, w->idx, C, m, w->n, w->k, w->N, w->M, w->L, static_cast<nm_dtype>(w->dtype), c_dt,
                    NM_MATH_AUTO, stream);
+}
+
+static nm_status at_check(const void* At, int64_t lda, int64_t m, int64_t e) {
+    if (lda < m) return fail(NM_ERR_SHAPE, "nm_spmm_at: lda < m");
+    if ((reinterpret_cast<uintptr_t>(At) & 15) || (lda * e) % 16)
+        return fail(NM_ERR_ALIGNMENT, "nm_spmm_at: At must be 16-B aligned with lda * element size % 16 == 0");
+    return NM_OK;
+}
+
+nm_status nm_spmm_at(const void* At, int64_t lda, const void* values, const uint8_t* idx, void* C, int64_t m, int64_t n,
+                     int64_t k, int N, int M, int L, nm_dtype ab_dt, nm_dtype c_dt, nm_math math, void* stream) {
+    nm_status st = check_common(m, n, k, N, M, L);
+    if (st) return st;
+    if (ab_dt > NM_BF16 || c_dt > NM_BF16 || math > NM_MATH_BF16_TC) return fail(NM_ERR_UNSUPPORTED, "dtype/math");
+    if (m == 0 || n == 0) return NM_OK;
+    if (!At || !C || (k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_spmm_at: NULL pointer");
+    if ((st = at_check(At, lda, m, ab_dt == NM_BF16 ? 2 : 4))) return st;
+    if ((st = require_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (k == 0) {
+        NM_CUDA_TRY(cudaMemsetAsync(C, 0, static_cast<size_t>(m * n) * (c_dt == NM_BF16 ? 2 : 4), s));
+        return NM_OK;
+    }
+    int kernel = K_GENERIC;
+    nm_math used = NM_MATH_AUTO;
+    if ((st = select(At, values, C, m, n, k, N, M, L, ab_dt, c_dt, math, &kernel, &used))) return st;
+    if (kernel == K_SIMT_F32)
+        return simt_f32_launch(nullptr, static_cast<const float*>(values), idx, static_cast<float*>(C), m, n, k, N, M, L,
+                               1, s, nullptr, 1.f, nullptr, static_cast<const float*>(At), lda);
+    if (kernel == K_TC_SP || kernel == K_TC_TF32)
+        return tc_sp_launch(nullptr, values, idx, C, c_dt == NM_BF16, m, n, k, N, M, L, kernel == K_TC_TF32, s, 1.f, At,
+                            lda);
+    return fail(NM_ERR_UNSUPPORTED, "nm_spmm_at: this shape selects a kernel without an A^T input (generic / bf16 SIMT)");
+}
+
+nm_status nm_spmm_prepacked_at(const void* At, int64_t lda, const nm_prepacked* w, void* C, int64_t m, nm_dtype c_dt,
+                               void* stream) {
+    if (!w || w->magic != kPrepackMagic) return fail(NM_ERR_NULL, "nm_spmm_prepacked_at: descriptor not filled by nm_prepack");
+    if (w->kind != 2 && w->kind != 3 && w->kind != 4)
+        return nm_spmm_at(At, lda, w->values, w->idx, C, m, w->n, w->k, w->N, w->M, w->L, static_cast<nm_dtype>(w->dtype),
+                          c_dt, NM_MATH_AUTO, stream);
+    nm_status st = check_common(m, w->n, w->k, w->N, w->M, w->L);
+    if (st) return st;
+    const bool tf = w->kind == 3, simt = w->kind == 4;
+    if ((tf || simt) && c_dt != NM_F32) return fail(NM_ERR_UNSUPPORTED, "fp32 operands need an fp32 C");
+    if (m == 0 || w->n == 0) return NM_OK;
+    if (!At || !C) return fail(NM_ERR_NULL, "nm_spmm_prepacked_at: NULL pointer");
+    if ((st = at_check(At, lda, m, w->kind == 2 ? 2 : 4))) return st;
+    if ((st = require_device())) return st;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (simt) {
+        if (!simt_f32_applicable(At, w->values, C, m, w->n, w->k, w->N, w->M, w->L))
+            return fail(NM_ERR_UNSUPPORTED, "nm_spmm_prepacked_at: the SIMT kernel's shape / alignment rules");
+        return simt_f32_launch(nullptr, static_cast<const float*>(w->values), w->idx, static_cast<float*>(C), m, w->n,
+                               w->k, w->N, w->M, w->L, 1, s, nullptr, 1.f, static_cast<const uint32_t*>(w->tbl),
+                               static_cast<const float*>(At), lda);
+    }
+    if (!tc_sp_ok(At, C, m, w->n, w->k, w->N, w->M, w->L))
+        return fail(NM_ERR_UNSUPPORTED, "nm_spmm_prepacked_at: slot kernel needs C 4-B aligned, k % 8 == 0");
+    return tc_sp_run(nullptr, w->bperm, w->bn / 128, C, c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, tf, s, nullptr,
+                     1.f, At, lda);
 }
 
 nm_status nm_profile_begin(void) {

@@ -12,12 +12,14 @@
 namespace nm {
 
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
-                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha, const uint32_t* Dw);
+                          int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha, const uint32_t* Dw,
+                          const float* At_in = nullptr, int64_t lda = 0);
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 nm_status require_device();
 nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
-                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha);
+                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha, const void* At_in,
+                    int64_t lda);
 bool tc_sp_applicable(int64_t m, int64_t n, int64_t k, int N, int M, int L);
 
 struct PeerFlags {
@@ -231,7 +233,7 @@ nm_status nm_spmm_prepacked_peers(const void* A, const nm_prepacked* w, void* co
     nm_status st = require_device();
     if (st) return st;
     return tc_sp_run(A, w->bperm, w->bn / 128, po.c[0], c_dt == NM_BF16, m, w->n, w->k, w->N, w->M, w->L, tf,
-                     static_cast<cudaStream_t>(stream), &po, 1.f);
+                     static_cast<cudaStream_t>(stream), &po, 1.f, nullptr, 0);
 }
 
 }  // extern "C"

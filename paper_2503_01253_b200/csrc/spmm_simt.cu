@@ -562,9 +562,11 @@ int simt_split_factor(int ntiles, int64_t w, int npanels) {
 
 // mode: 0 = A panels straight from A (swizzled [m][k] boxes), 1 = A^T staged (tile TMA),
 // 2 = A^T staged + packed col_info loads (high sparsity).  The selector decides.
+// At_in (nm_spmm_at): A arrives transposed from the caller (k x lda, lda >= m): staged mode
+// without the per-call transpose (the packed mode, which reads whole bm-row segments raw, is off).
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po, float alpha,
-                          const uint32_t* Dw) {
+                          const uint32_t* Dw, const float* At_in, int64_t lda) {
     using namespace simt;
     Params p{};
     p.D = D;
@@ -602,6 +604,7 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     if (mode == 2 && p.npanels > MAX_PANELS_PACKED) mode = 1;
     const int bm = simt_row_tile(m, n);
     if (bm == 64 && mode == 2) mode = 1;  // packed mode: 512-B A^T rows (BM = 128)
+    if (At_in) mode = 1;
     const bool use_at = mode >= 1;
     const bool packed = mode == 2;
     const int ntiles_n = static_cast<int>(ceil_div(n, BN));
@@ -612,7 +615,10 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     if (st) return st;
     float* AT = nullptr;
     uint64_t* masks = nullptr;
-    if (use_at) {
+    if (At_in) {
+        p.AT = At_in;
+        st = make_tma_2d_pitched(&tmA, At_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, k, m, lda, p.bk, bm, 0);
+    } else if (use_at) {
         st = scratch_alloc(reinterpret_cast<void**>(&AT), static_cast<size_t>(k) * p.at_ld * sizeof(float), s);
         if (st) return st;
         const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(p.at_ld, 64)));

@@ -279,7 +279,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int st = own + 4 * (v0 + u);  // local stage (global stage sa + st)
                 if (st >= nst) break;
                 const int s = st % STAGES;
-                const uint32_t off = static_cast<uint32_t>(kq[u]) * pitch;  // byte offset of this lane's row
+                // byte offset of this lane's row; padding slots (row k) are zero-filled by the copy
+                // (source size 0), so a caller's A^T needs no zero row (nm_spmm_at)
+                const uint32_t off = kq[u] < p.k ? static_cast<uint32_t>(kq[u]) * pitch : 0xFFFFFFFFu;
                 {
                     const int stn = st + 4 * PF;
                     if (stn < nst) kq[u] = ssrc[(sa + stn) * SLOTS];
@@ -305,8 +307,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int i = 0; i < NCOPY; ++i) {
                         const uint32_t o = __shfl_sync(0xffffffffu, off, i / CPR);
-                        cp_async16_pred(bstage + dl[i % 8] + (i / 8) * DSTEP, src_c[i % CPR] + o, srcsz_c[i % CPR],
-                                        on_c[i % CPR]);
+                        const bool pad = o == 0xFFFFFFFFu;
+                        cp_async16_pred(bstage + dl[i % 8] + (i / 8) * DSTEP, src_c[i % CPR] + (pad ? 0u : o),
+                                        pad ? 0u : srcsz_c[i % CPR], on_c[i % CPR]);
                     }
                 }
                 // arrives on full[s] once this thread's copies have landed (counts as one of the
@@ -1278,20 +1281,25 @@ static nm_status sp_dispatch(int H, int nt, const void* at, const tcs::Params& p
 
 // One SpMM on a prepacked weight (buf from tc_sp_prepack with H column halves per tile).
 nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16, int64_t m, int64_t n, int64_t k, int N,
-                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha) {
+                    int M, int L, bool tf, cudaStream_t s, const PeerOut* po, float alpha, const void* At_in,
+                    int64_t lda) {
     using namespace tcs;
     const SpGeom g = sp_geom(n, k, N, M, L, tf, H);
     const uint8_t* b = static_cast<const uint8_t*>(buf);
-    const int64_t mp = (m + 7) / 8 * 8;
+    const int64_t mp = At_in ? lda : (m + 7) / 8 * 8;  // A^T row pitch (elements)
     const int eb = tf ? 4 : 2;
     void* at = nullptr;
     if (static_cast<uint64_t>(k + 1) * static_cast<uint64_t>(mp) * static_cast<uint64_t>(eb) >= (1ull << 32))
         return fail(NM_ERR_UNSUPPORTED, "spmm_tc_sp: A^T larger than 4 GiB (32-bit row offsets)");
-    // k + 1 rows: row k is zero, the source of the padding slots (kappa = k)
-    nm_status st = scratch_alloc(&at, static_cast<size_t>((k + 1) * mp) * eb, s);
+    nm_status st = NM_OK;
+    cudaError_t e = cudaSuccess;
+    if (At_in) {  // nm_spmm_at: the caller's A^T (padding slots are zero-filled by the gather)
+        at = const_cast<void*>(At_in);
+    } else {
+    // k + 1 rows: row k is zero (padding slots also zero-fill in the gather; kept for the tf32 path)
+    st = scratch_alloc(&at, static_cast<size_t>((k + 1) * mp) * eb, s);
     if (st) return st;
     const dim3 tg(static_cast<unsigned>(ceil_div(k, 64)), static_cast<unsigned>(ceil_div(mp, 64)));
-    cudaError_t e = cudaSuccess;
     if (tf) {
         // fp32 A^T by the SIMT path's transpose (tokens >= m written as zeros), then the zero row k
         transpose_kernel<<<tg, 256, 0, s>>>(static_cast<const float*>(A), static_cast<float*>(at), static_cast<int>(m),
@@ -1307,6 +1315,7 @@ nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16,
         e = cudaGetLastError();
     }
     if (e != cudaSuccess) st = cuda_fail(e, "spmm_tc_sp transpose");
+    }
     if (!st) {
         Params p{};
         p.base = b;
@@ -1329,15 +1338,17 @@ nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16,
             p.n_valid = static_cast<int>(po->n_valid);
         }
         const int est = tcs::sp_est_stages(k, N, M, L, g.H, tf);
-        if (!po && tc_sp2_enabled(tf, g.H)) {
+        if (!po && !At_in && tc_sp2_enabled(tf, g.H)) {  // (the pair kernel reads the zero row k)
             st = tc_sp2_launch(at, p, m, n, est, s);  // CTA pairs (spmm_tc_sp2.cu)
         } else {
             const int nt = sp_tokens(g.H, m, n, est);
             st = tf ? sp_dispatch<true>(g.H, nt, at, p, m, n, est, s) : sp_dispatch<false>(g.H, nt, at, p, m, n, est, s);
         }
     }
-    e = cudaFreeAsync(at, s);
-    if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
+    if (!At_in) {
+        e = cudaFreeAsync(at, s);
+        if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
+    }
     return st;
 }
 
@@ -1354,14 +1365,15 @@ int tc_sp_halves_m(int N, int M, int L, int64_t m, int64_t n, int64_t k) { retur
 // nm_spmm without a prepacked weight: prepack into pooled scratch (the size bound, no sync), run,
 // release.
 nm_status tc_sp_launch(const void* A, const void* Bv, const uint8_t* D, void* C, bool c_bf16, int64_t m, int64_t n,
-                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha) {
+                       int64_t k, int N, int M, int L, bool tf, cudaStream_t s, float alpha, const void* At_in,
+                       int64_t lda) {
     void* buf = nullptr;
     const size_t bytes = tc_sp_prepack_bytes(n, k, N, M, L, tf);
     const int H = tcs::sp_halves_m(L, N, M, m, n, k);  // per-call prepack: the token count is known
     nm_status st = scratch_alloc(&buf, bytes, s);
     if (st) return st;
     st = tc_sp_prepack(Bv, D, n, k, N, M, L, tf, H, buf, static_cast<int64_t>(bytes), nullptr, false, s);
-    if (!st) st = tc_sp_run(A, buf, H, C, c_bf16, m, n, k, N, M, L, tf, s, nullptr, alpha);
+    if (!st) st = tc_sp_run(A, buf, H, C, c_bf16, m, n, k, N, M, L, tf, s, nullptr, alpha, At_in, lda);
     const cudaError_t e = cudaFreeAsync(buf, s);
     if (st == NM_OK && e != cudaSuccess) st = cuda_fail(e, "cudaFreeAsync");
     return st;

@@ -31,7 +31,8 @@ EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_
            "nm_prepack_bytes_ex", "nm_prepack_ex", "nm_ipc_get_handle", "nm_ipc_open_handle", "nm_ipc_close",
            "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled", "nm_prepack_size",
            "nm_index_packed_words", "nm_index_pack", "nm_index_unpack", "nm_mc_supported", "nm_mc_create",
-           "nm_mc_export", "nm_mc_import", "nm_mc_add_device", "nm_mc_bind_map", "nm_mc_free", "nm_spmm_mc"]
+           "nm_mc_export", "nm_mc_import", "nm_mc_add_device", "nm_mc_bind_map", "nm_mc_free", "nm_spmm_mc",
+           "nm_spmm_at", "nm_spmm_prepacked_at"]
 
 
 class NmError(RuntimeError):
@@ -91,6 +92,8 @@ def lib():
         L.nm_prepack_bytes.restype = I64
         L.nm_prepack.argtypes = [P, P, I64, I64, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
         L.nm_spmm_prepacked.argtypes = [P, ctypes.POINTER(Prepacked), P, I64, I, P]
+        L.nm_spmm_at.argtypes = [P, I64, P, P, P, I64, I64, I64, I, I, I, I, I, I, P]
+        L.nm_spmm_prepacked_at.argtypes = [P, I64, ctypes.POINTER(Prepacked), P, I64, I, P]
         L.nm_prepack_bytes_ex.argtypes = [I64, I64, I, I, I, I, I]
         L.nm_prepack_bytes_ex.restype = I64
         L.nm_prepack_ex.argtypes = [P, P, I64, I64, I, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
@@ -244,6 +247,39 @@ def nm_spmm(A: torch.Tensor, W: NmWeight, out: torch.Tensor | None = None, out_d
     return out
 
 
+def _at_args(At: torch.Tensor, k: int, m: int | None):
+    """A^T operand checks (nm_spmm_at): k x lda contiguous rows, lda >= m."""
+    _dev(At, "At")
+    if At.dim() != 2 or At.stride(1) != 1:
+        raise ValueError("At must be a 2-D tensor with unit column stride (k x lda)")
+    if At.shape[0] != k:
+        raise NmError(2, "nm_spmm_at", f"At has {At.shape[0]} rows, weight has k={k}")
+    lda = At.stride(0)
+    m = At.shape[1] if m is None else m
+    if m > At.shape[1]:
+        raise NmError(2, "nm_spmm_at", f"m={m} exceeds At's {At.shape[1]} columns")
+    return lda, m
+
+
+def nm_spmm_at(At: torch.Tensor, W: NmWeight, m: int | None = None, out: torch.Tensor | None = None, out_dtype=None,
+               math: str = "auto", stream=None) -> torch.Tensor:
+    """C = A . decompress(W) with A supplied transposed (At: k x lda, feature-major activations):
+    the per-call transpose of nm_spmm is skipped; same kernels, same results."""
+    _dev(W.values, "values")
+    _dev(W.idx, "idx")
+    lda, m = _at_args(At, W.k, m)
+    if At.dtype != W.values.dtype:
+        raise TypeError("At and values must share a dtype")
+    cdt = out_dtype or At.dtype
+    if out is None:
+        out = torch.empty((m, W.n), dtype=cdt, device=At.device)
+    else:
+        _check_out(out, At, m, W.n)
+    _check(lib().nm_spmm_at(At.data_ptr(), lda, W.values.data_ptr(), W.idx.data_ptr(), out.data_ptr(), m, W.n, W.k,
+                            W.N, W.M, W.L, _dt(At), _dt(out), MATH[math], _stream(At, stream)), "nm_spmm_at")
+    return out
+
+
 class PrepackedWeight:
     '''A weight after nm_prepack (the paper's offline PreProcessing, P:470-475): keeps the
     original NmWeight (referenced by the descriptor), the device buffer and the descriptor.'''
@@ -292,6 +328,22 @@ def nm_spmm_prepacked(A: torch.Tensor, PW: PrepackedWeight, out: torch.Tensor | 
         _check_out(out, A, m, PW.W.n)
     _check(lib().nm_spmm_prepacked(A.data_ptr(), ctypes.byref(PW.desc), out.data_ptr(), m, _dt(out),
                                    _stream(A, stream)), "nm_spmm_prepacked")
+    return out
+
+
+def nm_spmm_prepacked_at(At: torch.Tensor, PW: "PrepackedWeight", m: int | None = None, out: torch.Tensor | None = None,
+                         out_dtype=None, stream=None) -> torch.Tensor:
+    """nm_spmm_prepacked with A supplied transposed (At: k x lda); no per-call transpose."""
+    lda, m = _at_args(At, PW.W.k, m)
+    if At.dtype != PW.W.values.dtype:
+        raise TypeError(f"At is {At.dtype}, the prepacked weight is {PW.W.values.dtype}")
+    cdt = out_dtype or At.dtype
+    if out is None:
+        out = torch.empty((m, PW.W.n), dtype=cdt, device=At.device)
+    else:
+        _check_out(out, At, m, PW.W.n)
+    _check(lib().nm_spmm_prepacked_at(At.data_ptr(), lda, ctypes.byref(PW.desc), out.data_ptr(), m, _dt(out),
+                                      _stream(At, stream)), "nm_spmm_prepacked_at")
     return out
 
 

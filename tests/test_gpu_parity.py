@@ -853,3 +853,66 @@ def test_spmm_host_path_chunked_slot_kernels(nm, oracle, monkeypatch, dt, chunks
         torch.from_numpy(D).pin_memory(), C)
     ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A) if dt == "bf16" else A, vals, D, k, N, M, L)
     assert np.array_equal(C.numpy().astype(np.float64), ref)
+
+
+# --------------------------------------------------------------- A supplied transposed (nm_spmm_at)
+AT_CASES = [  # (dtype, math, m, n, k, N, M, L, lda padding)
+    (torch.float32, "auto", 300, 256, 512, 8, 32, 32, 4),      # SIMT staged-A^T mode, ragged m, lda > m
+    (torch.float32, "auto", 1024, 512, 1024, 16, 32, 32, 0),   # full tiles
+    (torch.bfloat16, "auto", 300, 384, 512, 16, 32, 32, 8),    # slot kernel, ragged m and n tile
+    (torch.bfloat16, "auto", 129, 256, 1024, 4, 32, 32, 0),    # 87.5 %: many zero-filled padding slots
+    (torch.bfloat16, "auto", 520, 256, 768, 3, 8, 64, 24),     # odd N, M = 8, L = 64
+    (torch.float32, "tf32_tc", 200, 256, 512, 8, 32, 32, 4),   # tf32 slot kernel
+]
+
+
+@pytest.mark.parametrize("dt,math,m,n,k,N,M,L,pad", AT_CASES)
+def test_spmm_at_matches_nm_spmm(nm, oracle, dt, math, m, n, k, N, M, L, pad):
+    """nm_spmm_at (A given as A^T, k x lda, columns m .. lda-1 filled with NaN) computes the same C
+    as nm_spmm bit for bit, and integer inputs match the oracle exactly; nm_spmm_prepacked_at the
+    same on the prepacked weight (kind 2 bf16, 3 tf32, 4 fp32 bit-packed indices)."""
+    tdt = dt
+    for kind_inputs in ("uniform", "integer"):
+        if kind_inputs == "uniform":
+            A = synth.bf16grid((m, k), 71, synth.TID_A) if dt == torch.bfloat16 else synth.uniform((m, k), 71, synth.TID_A)
+            B = synth.bf16grid((k, n), 72, synth.TID_B) if dt == torch.bfloat16 else synth.uniform((k, n), 72, synth.TID_B)
+        else:
+            A = synth.integer((m, k), 73, synth.TID_A)
+            B = synth.integer((k, n), 74, synth.TID_B)
+        bits = synth.to_bf16_bits(B) if dt == torch.bfloat16 else B
+        vals, D = oracle.compress(bits, N, M, L)
+        v = oracle.bf16_to_f32(vals) if dt == torch.bfloat16 else vals
+        W = nm.NmWeight(dev(v, tdt), dev(D, torch.uint8), k, N, M, L)
+        Ad = dev(A, tdt)
+        lda = (m + 7) // 8 * 8 + pad  # rows 16-B aligned (bf16: 8 elements)
+        At = torch.full((k, lda), float("nan"), dtype=tdt, device="cuda")
+        At[:, :m] = Ad.t()
+        C_ref = nm.nm_spmm(Ad, W, out_dtype=torch.float32, math=math)
+        C_at = nm.nm_spmm_at(At, W, m=m, out_dtype=torch.float32, math=math)
+        torch.cuda.synchronize()
+        assert torch.equal(C_at, C_ref)
+        PW = nm.nm_prepack(W, math=math)
+        C_pat = nm.nm_spmm_prepacked_at(At, PW, m=m, out_dtype=torch.float32)
+        C_pre = nm.nm_spmm_prepacked(Ad, PW, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert torch.equal(C_pat, C_pre)
+        src = synth.to_bf16_bits(A) if dt == torch.bfloat16 else A
+        ref = oracle.spmm_sparse_f64(src, vals, D, k, N, M, L)
+        if kind_inputs == "integer":
+            assert np.array_equal(C_at.cpu().numpy().astype(np.float64), ref)
+        else:
+            assert oracle.rel_frobenius(C_at.cpu().numpy(), ref) <= (TOL_F32 if math == "auto" and dt == torch.float32
+                                                                     else TOL_BF16)
+
+
+def test_spmm_at_rejects(nm):
+    """lda < m -> NM_ERR_SHAPE; a shape that selects a kernel without an A^T input -> unsupported."""
+    m, n, k, N, M, L = 64, 96, 96, 3, 8, 3   # L = 3: the generic kernel
+    W = nm.nm_compress(torch.ones(k, n, device="cuda"), N, M, L)
+    At = torch.zeros((k, m), device="cuda")
+    with pytest.raises(nm.NmError, match="UNSUPPORTED"):
+        nm.nm_spmm_at(At, W)
+    W2 = nm.nm_compress(torch.ones(128, 128, device="cuda"), 16, 32, 32)
+    At2 = torch.zeros((128, 64), device="cuda")
+    with pytest.raises(nm.NmError):
+        nm.nm_spmm_at(At2, W2, m=65)
