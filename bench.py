@@ -511,7 +511,11 @@ def run_sharded(args):
     dtype = torch.float32 if args.dtype == "f32" else torch.bfloat16
     m, n, k, N, M, L = cfg
     A, Bd, _ = make_inputs(cfg, dtype, "cuda")  # A replicated (column-parallel input), B generated identically
-    chunks = args.chunks if args.chunks > 0 else (4 if m >= 1024 else 1)
+    # row slices for the NCCL overlap: measured per-rank compute (profiles/r02m_shard_chunks.txt)
+    # grows with the slice count much faster than the all-gather it hides (cfg2 fp32 at G = 8:
+    # 226 us in one slice, 306 / 609 us in 2 / 4, against a 76 us all-gather floor), so one slice
+    # unless --chunks asks for more
+    chunks = args.chunks if args.chunks > 0 else 1
     layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD, exchange=args.exchange, chunks=chunks)
     del Bd
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -625,7 +629,7 @@ def main():
     ap.add_argument("--sharded", action="store_true", help="column-sharded path even at one rank (testing)")
     ap.add_argument("--ref-seconds", type=float, default=10.0)
     ap.add_argument("--chunks", type=int, default=0,
-                    help="sharded NCCL path: row slices whose all-gather overlaps the next slice (0 = auto)")
+                    help="sharded NCCL path: row slices whose all-gather overlaps the next slice (0 = 1 slice)")
     ap.add_argument("--launch-check", action="store_true",
                     help="start the ranks, all-reduce a count over gloo, rank 0 prints it (no GPU needed)")
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "p2p"],
