@@ -209,8 +209,9 @@ def measure_config(cfg, dtype, steps, warmup, flush, with_cublas=True, math=None
     step = make_step(A, W, C, dtype, math, at)
     for _ in range(warmup):
         step()
+    ms = time_steps(step, steps, 0, stream, flush)  # steps without the profiling events
     nmspmm.nm_profile_begin()
-    ms = time_steps(step, steps, 0, stream, flush)
+    time_steps(step, steps, 0, stream, flush)
     k_ms, k_cnt, launches = nmspmm.nm_profile_end()
     t = statistics.median(ms)
     kms = k_ms / max(1, k_cnt)
@@ -387,10 +388,13 @@ def run_ours(args):
         sampler = ClockSampler(local)
         with sampler:
             t0 = time.perf_counter()
-            nmspmm.nm_profile_begin()
             ms = time_steps(step, args.steps, 0, stream, flush)
-            k_ms, k_cnt, launches = nmspmm.nm_profile_end()
             wall = time.perf_counter() - t0
+        # the dominant kernel's time and the launch count from a second, profiled pass (the
+        # library's profiling events around the kernel are kept out of the timed steps above)
+        nmspmm.nm_profile_begin()
+        time_steps(step, args.steps, 0, stream, flush)
+        k_ms, k_cnt, launches = nmspmm.nm_profile_end()
         t_step = statistics.median(ms)
         value = flop_count(cfg) / (t_step * 1e-3) / 1e12
         kernel_ms = k_ms / max(1, k_cnt)  # dominant SpMM kernel, CUDA events on its stream
@@ -528,9 +532,11 @@ def run_sharded(args):
     dist.barrier()
     sampler = ClockSampler(local)
     with sampler:
-        nmspmm.nm_profile_begin()
         ms = time_steps(step, args.steps, 0, stream, flush)
-        k_ms, k_cnt, launches = nmspmm.nm_profile_end()
+    dist.barrier()
+    nmspmm.nm_profile_begin()  # kernel time and launches from a second, profiled pass
+    time_steps(step, args.steps, 0, stream, flush)
+    k_ms, k_cnt, launches = nmspmm.nm_profile_end()
     dist.barrier()
     t = torch.tensor([statistics.median(ms), k_ms / max(1, k_cnt)], device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)  # max over ranks (step, dominant kernel)
