@@ -95,7 +95,24 @@ def c_peers():  # fused exchange on one device: 2 "ranks" as two buffers, peer s
         check("peers (SIMT peer-store epilogue)", c[:, 256:], ref, True)
 
 
-CASES = {"format": c_format, "simt": c_simt, "generic": c_generic, "slot": c_slot, "pair": c_pair, "tf32": c_tf32,
+def c_at():  # A supplied transposed: slot kernel (zero-filled padding slots) and SIMT staged mode
+    for bf16, cfg in [(True, (300, 512, 1024, 4, 32, 32)), (False, (200, 384, 1024, 8, 32, 32))]:
+        A, vals, D, W, Ad = weights(*cfg, bf16, 61)
+        m, k = cfg[0], cfg[2]
+        At = torch.zeros((k, (m + 7) // 8 * 8 + 8), dtype=Ad.dtype, device="cuda")
+        At[:, :m] = Ad.t()
+        C = nm.nm_spmm_at(At, W, m=m, out_dtype=torch.float32)
+        check(f"nm_spmm_at {'bf16 slot' if bf16 else 'fp32 SIMT'}", C, oracle.spmm_sparse_f64(A, vals, D, k, *cfg[3:]), True)
+
+
+def c_bf16simt():  # bf16 with L = 4: widen -> fp32 SIMT kernel -> narrow
+    cfg = (300, 256, 512, 8, 32, 4)
+    A, vals, D, W, Ad = weights(*cfg, True, 71)
+    check("bf16 on the SIMT kernel", nm.nm_spmm(Ad, W, out_dtype=torch.float32),
+          oracle.spmm_sparse_f64(A, vals, D, 512, 8, 32, 4), True)
+
+
+CASES = {"at": c_at, "bf16simt": c_bf16simt, "format": c_format, "simt": c_simt, "generic": c_generic, "slot": c_slot, "pair": c_pair, "tf32": c_tf32,
          "unshard": c_unshard, "peers": c_peers}
 for name in sys.argv[1:] or list(CASES):
     CASES[name]()
