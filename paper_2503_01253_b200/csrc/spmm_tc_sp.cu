@@ -20,7 +20,7 @@
 // Roles: warps 0-7 gather (8 slot rows each per stage; warp 0 also bulk-copies the weight
 // image) and then the epilogue (TMEM -> registers -> smem -> TMA store); warp 8 issues the
 // tcgen05.cp + 2 H tcgen05.mma.sp per stage.  Optional: tail split of the last partial wave,
-// weight multicast over 2-CTA clusters (NM_SP_MC=1).
+// (the round-2 weight multicast over 2-CTA clusters measured slower and was removed).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -35,8 +35,6 @@ namespace nm {
 
 __global__ void transpose_kernel(const float* __restrict__ A, float* __restrict__ AT, int m, int k, int ld);
 
-bool tc_sp2_enabled(bool tf, int H);
-nm_status tc_sp2_launch(const void* at, tcs::Params p, int64_t m, int64_t n, int est_stages, cudaStream_t s);
 
 namespace tcs {
 
@@ -147,21 +145,17 @@ static int sp_halves_m(int L, int N, int M, int64_t m, int64_t n, int64_t k) {
             static_cast<long long*>(p.C)[(st) * 8 + (slot)] = clock64();                               \
     } while (0)
 
-// MCAST: launched as clusters of 2 CTAs (adjacent token tiles of one column tile, identical stage
-// ranges); each CTA bulk-copies half of every weight image with .multicast::cluster into both,
-// and every MMA commit releases the stage in both CTAs (empty count 2): the weight stream's L2
-// traffic per SM halves.
 // TF: fp32 operands on kind::tf32 (El<true>), else bf16 on kind::f16.  PEER: the fused exchange's
 // direct-store epilogue into every rank's C (a separate instantiation: the peer loop in the
 // common kernel cost 30 % on the tf32 NT = 208 variant through register allocation).
-template <int H, int NT_, bool MCAST, bool TF, bool PEER = false>
+template <int H, int NT_, bool TF, bool PEER = false>
 __global__ void __launch_bounds__(THREADS, 1)
     spmm_tc_sp_kernel(const void* __restrict__ At, const __grid_constant__ CUtensorMap tmC,
                       const __grid_constant__ CUtensorMap tmC16, const Params p) {
     using CF = Cfg<H, NT_, TF>;
     using EL = El<TF>;
     constexpr int NT = CF::NT, MC = CF::MC, B_BYTES = CF::B_BYTES, W_BYTES = CF::W_BYTES, STAGES = CF::ST;
-    constexpr int SLOTS = EL::SLOTS, RPW = SLOTS / GATHER_WARPS;  // slot rows per gather warp and stage
+    constexpr int SLOTS = EL::SLOTS;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sB = smem;                               // STAGES x B_BYTES (1024-aligned: 128-B swizzle atoms)
@@ -203,7 +197,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(&full[s], 1 + 2 * 32);  // two owner warps' copies + the weight copy
-                mbar_init(&empty[s], MCAST ? 2 : 1);
+                mbar_init(&empty[s], 1);
             }
             mbar_init(acc_full, 1);
             fence_mbar_init();
@@ -212,11 +206,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_alloc(tmem_slot, TMEM_COLS);
     }
     tc_fence_before();
-    if (MCAST) cluster_sync_all();  // the peer's multicast copies / commits target these barriers
-    else __syncthreads();
+    __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    const uint32_t crank = MCAST ? cluster_rank() : 0u;
 
     if (warp < GATHER_WARPS) {
         // ============ gather: stage-owning warp pairs ============
@@ -295,11 +287,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                         const uint32_t wb = ((sa + st) & 1) ? static_cast<uint32_t>(H * A_BYTES) : W_BYTES;
                         mbar_arrive_expect_tx(&full[s], wb);
                         const uint8_t* wst = wsrc + sp_stage_off(sa + st, H);
-                        if (MCAST)  // both halves land in both CTAs: copy (and multicast) ours
-                            bulk_load_mc(sW + s * W_BYTES + crank * (wb / 2), wst + crank * (wb / 2), wb / 2, &full[s],
-                                         0x3);
-                        else
-                            bulk_load(sW + s * W_BYTES, wst, wb, &full[s]);
+                        bulk_load(sW + s * W_BYTES, wst, wb, &full[s]);
                     }
                 }
                 if (!(p.dbg & 1)) {
@@ -353,7 +341,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                     }
                     if (p.dbg & 128) mbar_arrive(&empty[s]);       // timing study: plain arrive instead of commit
-                    else if (MCAST) tc_commit_mc(&empty[s], 0x3);  // the stage is free once both CTAs are done
                     else tc_commit(&empty[s]);
                 }
                 if (gs & 1) pi = pi + 1 == CF::NPAIR ? 0 : pi + 1;
@@ -562,8 +549,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_before();
         if (warp == 0) SP_TS(nst, 0);
     }
-    if (MCAST) cluster_sync_all();  // no multicast copy / commit may still target this CTA
-    else __syncthreads();
+    __syncthreads();
     if (warp == MMA_WARP) {
         tc_fence_after();
         tmem_dealloc(tmem, TMEM_COLS);
@@ -1160,11 +1146,9 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     using CF = Cfg<H, NT, TF>;
     static std::atomic<uint64_t> attr_mask{0};
     if (!attr_once(attr_mask)) {
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false, TF>,
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, TF>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, true, TF>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
-        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, false, TF, true>,
+        NM_CUDA_TRY(cudaFuncSetAttribute(spmm_tc_sp_kernel<H, NT, TF, true>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM_BYTES));
         attr_done(attr_mask);
     }
@@ -1187,12 +1171,7 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     }
     // tail split (NM_SP_TAIL=0 disables): the tiles of a partial last wave that at most half
     // fills the SMs run as two half-range CTAs each
-    // weight multicast (NM_SP_MC=1): clusters of two adjacent token tiles (n_tok padded to even;
-    // a padding tile gathers zeros and stores nothing); no tail split
-    const char* mce = std::getenv("NM_SP_MC");
-    const bool mc = mce && mce[0] == '1';
     p.n_tok = static_cast<int>(ceil_div(m, CF::NT));
-    if (mc) p.n_tok += p.n_tok & 1;
     const int64_t tiles = ceil_div(n, CF::MC) * p.n_tok;
     const int64_t sms = num_sms();
     // Split stage ranges (pair-aligned) over several CTAs per tile, partials added in a fixed order:
@@ -1203,7 +1182,7 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     // NM_SP_SPLIT=S forces S for those tiles; NM_SP_TAIL=0 disables splitting.
     const char* te2 = std::getenv("NM_SP_TAIL");
     const char* se = std::getenv("NM_SP_SPLIT");
-    const bool can_split = !mc && p.tma_c && !(te2 && te2[0] == '0');
+    const bool can_split = p.tma_c && !(te2 && te2[0] == '0');
     int64_t split_tiles = 0;
     int S = 1;
     // Every part must keep >= 24 stages: measured on B200 (profiles/r02f_sp_split_probe.txt) shorter
@@ -1233,25 +1212,10 @@ static nm_status sp_launch_h(const void* at, tcs::Params p, int64_t m, int64_t n
     }
     const unsigned grid = static_cast<unsigned>(p.full_ctas + split_tiles * S);
     prof_begin(s);
-    if (mc) {
-        cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(grid);
-        lc.blockDim = dim3(THREADS);
-        lc.dynamicSmemBytes = CF::SMEM_BYTES;
-        lc.stream = s;
-        cudaLaunchAttribute la[1];
-        la[0].id = cudaLaunchAttributeClusterDimension;
-        la[0].val.clusterDim.x = 2;
-        la[0].val.clusterDim.y = 1;
-        la[0].val.clusterDim.z = 1;
-        lc.attrs = la;
-        lc.numAttrs = 1;
-        cudaLaunchKernelEx(&lc, spmm_tc_sp_kernel<H, NT, true, TF>, at, tmC, tmC16, p);
-    } else if (p.npeer) {
-        spmm_tc_sp_kernel<H, NT, false, TF, true><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
-    } else {
-        spmm_tc_sp_kernel<H, NT, false, TF><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
-    }
+    if (p.npeer)
+        spmm_tc_sp_kernel<H, NT, TF, true><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
+    else
+        spmm_tc_sp_kernel<H, NT, TF><<<grid, THREADS, CF::SMEM_BYTES, s>>>(at, tmC, tmC16, p);
     prof_end(s);
     note_launch();
     const cudaError_t e = cudaGetLastError();
@@ -1338,12 +1302,8 @@ nm_status tc_sp_run(const void* A, const void* buf, int H, void* C, bool c_bf16,
             p.n_valid = static_cast<int>(po->n_valid);
         }
         const int est = tcs::sp_est_stages(k, N, M, L, g.H, tf);
-        if (!po && !At_in && tc_sp2_enabled(tf, g.H)) {  // (the pair kernel reads the zero row k)
-            st = tc_sp2_launch(at, p, m, n, est, s);  // CTA pairs (spmm_tc_sp2.cu)
-        } else {
-            const int nt = sp_tokens(g.H, m, n, est);
-            st = tf ? sp_dispatch<true>(g.H, nt, at, p, m, n, est, s) : sp_dispatch<false>(g.H, nt, at, p, m, n, est, s);
-        }
+        const int nt = sp_tokens(g.H, m, n, est);
+        st = tf ? sp_dispatch<true>(g.H, nt, at, p, m, n, est, s) : sp_dispatch<false>(g.H, nt, at, p, m, n, est, s);
     }
     if (!At_in) {
         e = cudaFreeAsync(at, s);

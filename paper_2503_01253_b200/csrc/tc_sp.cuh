@@ -1,5 +1,5 @@
-// tc_sp.cuh -- definitions shared by the slot-packed sparse tensor-core kernels (spmm_tc_sp.cu:
-// one CTA per tile; spmm_tc_sp2.cu: CTA pairs on tcgen05 cta_group::2): element types, the
+// tc_sp.cuh -- definitions of the slot-packed sparse tensor-core kernels (spmm_tc_sp.cu, one CTA
+// per tile; the round-2 CTA-pair variant was measured slower and removed): element types, the
 // prepacked weight-image geometry, launch parameters and inline-PTX helpers (written from the
 // PTX ISA).
 #pragma once
@@ -71,13 +71,8 @@ struct Params {
     int npeer, n_valid;
     int64_t ldc, col_off;
     float alpha;  // C = alpha . A B~ (nm_spmm_scaled); applied after the tail-split addition
-    int n_units;  // CTA-pair kernel (spmm_tc_sp2.cu): work units = full tiles + split tiles x split
 };
 
-// bulk L2 prefetch of global bytes (size a multiple of 16)
-__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
-}
 // mbarrier wait variants (timing studies of the stage hand-off, NM_SP_DBG 1024 / 2048 / 4096):
 // try_wait with an explicit suspend-time hint (ns), and a pure test_wait spin
 __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t ns) {
@@ -168,29 +163,6 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 }
 __device__ __forceinline__ void red_release_add(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void bulk_load_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            smem_u32(bar)),
-        "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 }  // namespace tcs

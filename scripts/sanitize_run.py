@@ -55,17 +55,11 @@ def c_generic():
     check("generic", nm.nm_spmm(Ad, W), oracle.spmm_sparse_f64(A, vals, D, 96, 3, 8, 3), True)
 
 
-def c_slot(pair=False):  # bf16 slot kernel, one-CTA (tail split on a small grid) or CTA pair
-    os.environ["NM_SP_PAIR"] = "1" if pair else "0"
+def c_slot():  # bf16 slot kernel (tail split on a small grid)
     cfg = (300, 512, 1024, 16, 32, 32)
     A, vals, D, W, Ad = weights(*cfg, True, 31)
     C = nm.nm_spmm_prepacked(Ad, nm.nm_prepack(W), out_dtype=torch.float32)
-    check(f"bf16 slot {'pair' if pair else 'one-CTA'}", C, oracle.spmm_sparse_f64(A, vals, D, 1024, 16, 32, 32), True)
-    os.environ.pop("NM_SP_PAIR")
-
-
-def c_pair():
-    c_slot(True)
+    check("bf16 slot", C, oracle.spmm_sparse_f64(A, vals, D, 1024, 16, 32, 32), True)
 
 
 def c_tf32():
@@ -112,7 +106,7 @@ def c_bf16simt():  # bf16 with L = 4: widen -> fp32 SIMT kernel -> narrow
           oracle.spmm_sparse_f64(A, vals, D, 512, 8, 32, 4), True)
 
 
-CASES = {"at": c_at, "bf16simt": c_bf16simt, "format": c_format, "simt": c_simt, "generic": c_generic, "slot": c_slot, "pair": c_pair, "tf32": c_tf32,
+CASES = {"at": c_at, "bf16simt": c_bf16simt, "format": c_format, "simt": c_simt, "generic": c_generic, "slot": c_slot, "tf32": c_tf32,
          "unshard": c_unshard, "peers": c_peers}
 for name in sys.argv[1:] or list(CASES):
     CASES[name]()

@@ -523,7 +523,6 @@ def test_spmm_tc_sp_token_tiles_all_rows(nm, oracle, monkeypatch, nt, cdt):
     checked: integer inputs make fp32 C exact and bf16 C its RNE (catches epilogue chunks that
     spill into the next tile's rows)."""
     use_tc_path(monkeypatch, "sp")
-    monkeypatch.setenv("NM_SP_PAIR", "0")  # the one-CTA kernel's token tiles (pairs: test_gpu_pair.py)
     monkeypatch.setenv("NM_SP_H", "2")     # the H = 2 token tiles (a small grid would otherwise take H = 1)
     monkeypatch.setenv("NM_SP_NT", nt)
     m, n, k, N, M, L = 650, 512, 256, 16, 32, 32
@@ -546,7 +545,6 @@ def test_spmm_tc_sp_tail_split_on_off(nm, oracle, monkeypatch, tail, m, n, k, N,
     """Small grids take the tail split (two half-range CTAs per tile, part 0 adds part 1's
     partial); NM_SP_TAIL=0 runs one CTA per tile.  Both bit-exact on integer inputs."""
     use_tc_path(monkeypatch, "sp")
-    monkeypatch.setenv("NM_SP_PAIR", "0")  # the one-CTA kernel's tail split (pairs: test_gpu_pair.py)
     monkeypatch.setenv("NM_SP_TAIL", tail)
     monkeypatch.setenv("NM_SP_SPLIT", "2")  # these tiles are too short for the selector to split them
     A = synth.integer((m, k), 131, synth.TID_A)
