@@ -175,7 +175,8 @@ nm_status nm_spmm_scaled(const void* A, const void* values, const uint8_t* idx, 
  * copies A, values, idx from host memory (pinned for async copies) into the
  * caller's device workspace, runs nm_spmm, copies C back to C_host.  On the fp32
  * SIMT path and the bf16 / tf32 slot kernels with m >= 1024 the rows of A / C go in
- * 4 chunks so that the copies of one chunk overlap the SpMM of another (two
+ * nch + 1 chunks sized 1 : 2 : .. : 2 : 1 (nch = 4; 8 on the fp32 SIMT path once m >= 2048;
+ * NM_HOST_CHUNKS=1..8 overrides) so that the copies of one chunk overlap the SpMM of another (two
  * library-created copy streams, destroyed before return; the slot kernels prepack the
  * weight once per call into pooled scratch first); other paths copy, compute and copy
  * back in sequence.
