@@ -233,7 +233,7 @@ bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
 int simt_split_factor(int ntiles, int64_t w, int npanels);
-int simt_row_tile(int64_t m, int64_t n);
+int simt_row_tile(int64_t m, int64_t n, int64_t w);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
                           float alpha = 1.f, const uint32_t* Dw = nullptr, const float* At_in = nullptr,
@@ -720,7 +720,7 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
     out->bytes = e * double(m) * double(k) + e * double(w) * double(n) + double(w) * double(q) + e * double(m) * double(n);
     int kernel = K_GENERIC;
     nm_math used = NM_MATH_AUTO;
-    static const float dummy[4] = {0, 0, 0, 0};  // 16-B aligned stand-in pointers for the alignment test
+    alignas(16) static const float dummy[4] = {0, 0, 0, 0};  // 16-B aligned stand-in pointers for the alignment test
     if ((st = select(dummy, dummy, dummy, m, n, k, N, M, L, ab_dt, ab_dt, math, &kernel, &used))) return st;
     out->math = used;
     out->kernel = kernel;
@@ -728,7 +728,7 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
     if (kernel == K_SIMT_F32 || kernel == K_SIMT_BF16) {
         int wp, bk, bkw;
         simt_f32_geometry(N, M, &wp, &bk, &bkw);
-        const int bm = simt_row_tile(m, n);
+        const int bm = simt_row_tile(m, n, w);
         out->bm = bm;
         out->bn = 128;
         out->bk = bk;

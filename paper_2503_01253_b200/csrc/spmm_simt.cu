@@ -512,18 +512,23 @@ static nm_status launch_simt(const CUtensorMap& tmA, const CUtensorMap& tmB, con
 }
 
 // Row tile of the SIMT kernel (the selector): 64 rows (4 warps, 3 resident CTAs per
-// SM) when the 64-row grid fits in one round of resident CTAs (tiles64 <= 3 x SMs: sub-wave grids
-// such as the column shards of a multi-GPU layer, m = 256 decode shapes, small problems), else 128
-// (8 warps, 2 per SM, with the wave-model split of its tail).  Measured on B200
-// (profiles/r02j_simt_row_tile.txt): 1024^3 47.1 -> 39.5 us, 256x13824x5120 141 -> 114, the
-// cfg3-75 % 8-GPU shard 183 -> 173, cfg1 27.2 -> 20.8; beyond one round the 128-row tile with its
-// split wins (m = 256 cfg4-65B 258 vs 280, 2048^3 188 vs 193); the one loss of the rule is the cfg2
-// shard (225 vs 220 us).  NM_SIMT_BM=64/128 overrides.
-int simt_row_tile(int64_t m, int64_t n) {
+// SM) or 128 (8 warps, 2 per SM, with the wave-model split of its tail / sub-wave grid).
+//  * tiles64 in (2, 3] x SMs (the 64-row grid fills 0.67-1 round of resident CTAs): 64.  Measured
+//    on B200 (profiles/r02j_simt_row_tile.txt, the 100-point dataset r02n vs r02e): 256x13824x5120
+//    141 -> 114 us, the cfg3-75 % 8-GPU shard 183 -> 173, 256x12288x4096 203 -> 162,
+//    512x6656x6656 322 -> 254.
+//  * tiles64 <= 2 x SMs: 128 with its k-split once the compressed k is long (w >= 1024: the split
+//    parts amortise their fixed cost; 256x4096x11008 167 vs 209 us, 256x8192x8192 219 vs 228, the
+//    cfg2 8-GPU shard 220 vs 225), 64 for short k (1024^3 39.5 vs 47.1, cfg1 20.8 vs 27.2).
+//  * larger grids: 128 (m = 256 cfg4-65B 258 vs 280, 2048^3 188 vs 193).
+// NM_SIMT_BM=64/128 overrides.
+int simt_row_tile(int64_t m, int64_t n, int64_t w) {
     const char* e = getenv("NM_SIMT_BM");
     if (e) return atoi(e) == 64 ? 64 : 128;
-    const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, simt::BN);
-    return tiles64 <= 3 * static_cast<int64_t>(num_sms()) ? 64 : 128;
+    const int64_t tiles64 = ceil_div(m, 64) * ceil_div(n, simt::BN), sms = num_sms();
+    if (tiles64 > 3 * sms) return 128;
+    if (tiles64 > 2 * sms) return 64;
+    return w >= 1024 ? 128 : 64;
 }
 
 // Split factor of the SIMT kernel's tile schedule (the selector's wave model): the
@@ -602,7 +607,7 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     p.nboxA = (p.bk + A_BOX_COLS - 1) / A_BOX_COLS;
     const int64_t w = k / M * N;
     if (mode == 2 && p.npanels > MAX_PANELS_PACKED) mode = 1;
-    const int bm = simt_row_tile(m, n);
+    const int bm = simt_row_tile(m, n, k / M * N);
     if (bm == 64 && mode == 2) mode = 1;  // packed mode: 512-B A^T rows (BM = 128)
     if (At_in) mode = 1;
     const bool use_at = mode >= 1;

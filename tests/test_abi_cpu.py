@@ -187,6 +187,13 @@ ROW_TILE_MEASURED = [
     ((2048, 2752, 8192, 4, 32, 32), 128),    # 303 vs 315 (cfg4-65B 8-GPU shard)
     ((2048, 2048, 2048, 16, 32, 32), 128),   # 188 vs 193
     ((4096, 4096, 4096, 16, 32, 32), 128),   # cfg2: 1208 vs 1200 (within 1 %)
+    # the 100-point dataset (profiles/r02n_llama_dataset.csv 64-row vs r02e 128-row, fp32 8:32)
+    ((256, 4096, 4096, 8, 32, 32), 128),     # 81.3 vs 86.4 (tiles64 128, w 1024: the split)
+    ((256, 4096, 11008, 8, 32, 32), 128),    # 167 vs 209
+    ((256, 8192, 8192, 8, 32, 32), 128),     # 219 vs 228
+    ((4096, 512, 4096, 16, 32, 32), 128),    # cfg2 8-GPU shard: 220 vs 225
+    ((256, 12288, 4096, 8, 32, 32), 64),     # 162 vs 203 (tiles64 384)
+    ((512, 6656, 6656, 8, 32, 32), 64),      # 254 vs 322 (tiles64 416)
 ]
 
 
