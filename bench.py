@@ -159,14 +159,14 @@ def make_step(A, W, C, dtype, math=None, at=False):
         At = A.t().contiguous()  # the caller's layout (untimed)
         if dtype == torch.float32:
             return lambda: nmspmm.nm_spmm_at(At, W, out=C, math="f32_simt")
-        PWa = nmspmm.nm_prepack(W)
+        PWa = nmspmm.nm_prepack(W, m_hint=A.shape[0])
         return lambda: nmspmm.nm_spmm_prepacked_at(At, PWa, out=C)
     if math == "tf32_tc":
-        PWt = nmspmm.nm_prepack(W, math="tf32_tc")
+        PWt = nmspmm.nm_prepack(W, math="tf32_tc", m_hint=A.shape[0])
         return lambda: nmspmm.nm_spmm_prepacked(A, PWt, out=C)
     if dtype == torch.float32:
         return lambda: nmspmm.nm_spmm(A, W, out=C, math="f32_simt")
-    PW = nmspmm.nm_prepack(W)
+    PW = nmspmm.nm_prepack(W, m_hint=A.shape[0])  # the serving batch is known when the layer is built
     return lambda: nmspmm.nm_spmm_prepacked(A, PW, out=C)
 
 
@@ -520,7 +520,8 @@ def run_sharded(args):
     # 226 us in one slice, 306 / 609 us in 2 / 4, against a 76 us all-gather floor), so one slice
     # unless --chunks asks for more
     chunks = args.chunks if args.chunks > 0 else 1
-    layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD, exchange=args.exchange, chunks=chunks)
+    layer = sharded.ShardedNmLinear.from_dense(Bd, N, M, L, dist.group.WORLD, exchange=args.exchange, chunks=chunks,
+                                               m_hint=m)
     del Bd
     flush_buf = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     flush = (lambda: flush_buf.fill_(1.0)) if not args.no_flush else None

@@ -281,6 +281,15 @@ nm_status nm_prepack_size(const void* values, const uint8_t* idx, int64_t n, int
                           nm_dtype dt, nm_math math, int64_t* bytes, void* stream);
 nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
                         nm_math math, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
+/* The same for an expected token count m_hint (> 0; 0 = unknown, the calls above): the slot
+ * prepacks (kinds 2 / 3) then choose their column halves H as nm_spmm does for that m -- H = 1 when
+ * H = 2 would leave the grid under two waves (small m, the column shards of a multi-GPU layer;
+ * DESIGN.md 6) -- so nm_spmm_prepacked on m tokens runs the tile nm_spmm would.  Any m may still be
+ * passed to nm_spmm_prepacked.  The size and the fill must use the same m_hint. */
+nm_status nm_prepack_size_m(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L,
+                            nm_dtype dt, nm_math math, int64_t m_hint, int64_t* bytes, void* stream);
+nm_status nm_prepack_m(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                       nm_math math, int64_t m_hint, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream);
 
 /*
  * Bit-packed indices (an index needs only ceil(log2 M) bits) in the tile-major layout of

@@ -821,8 +821,20 @@ int64_t nm_prepack_bytes(int64_t n, int64_t k, int N, int M, int L, nm_dtype dt)
     return nm_prepack_bytes_ex(n, k, N, M, L, dt, NM_MATH_AUTO);
 }
 
+// H of a slot prepack: without a token count the sparsity rule (tc_sp_halves); with the expected m
+// (nm_prepack_m) also the small-grid rule of the per-call path (tc_sp_halves_m: H = 1 when H = 2
+// would leave the grid under two waves; the A-F study)
+static int prepack_halves(int64_t m_hint, int64_t n, int64_t k, int N, int M, int L) {
+    return m_hint > 0 ? tc_sp_halves_m(N, M, L, m_hint, n, k) : tc_sp_halves(N, M, L);
+}
+
 nm_status nm_prepack_size(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
                           nm_math math, int64_t* bytes, void* stream) {
+    return nm_prepack_size_m(values, idx, n, k, N, M, L, dt, math, 0, bytes, stream);
+}
+
+nm_status nm_prepack_size_m(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L,
+                            nm_dtype dt, nm_math math, int64_t m_hint, int64_t* bytes, void* stream) {
     nm_status st = check_common(0, n, k, N, M, L);
     if (st) return st;
     if (!bytes || (n * k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_prepack_size: NULL pointer");
@@ -832,12 +844,17 @@ nm_status nm_prepack_size(const void* values, const uint8_t* idx, int64_t n, int
     if (kind == 4) *bytes = 4 * index_packed_words(k, n, N, M, L);
     if (kind == 0 || kind == 4) return NM_OK;
     if ((st = require_device())) return st;
-    return tc_sp_prepack(values, idx, n, k, N, M, L, kind == 3, tc_sp_halves(N, M, L), nullptr, 0, bytes, true,
-                         static_cast<cudaStream_t>(stream));
+    return tc_sp_prepack(values, idx, n, k, N, M, L, kind == 3, prepack_halves(m_hint, n, k, N, M, L), nullptr, 0, bytes,
+                         true, static_cast<cudaStream_t>(stream));
 }
 
 nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
                         nm_math math, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream) {
+    return nm_prepack_m(values, idx, n, k, N, M, L, dt, math, 0, buf, buf_bytes, out, stream);
+}
+
+nm_status nm_prepack_m(const void* values, const uint8_t* idx, int64_t n, int64_t k, int N, int M, int L, nm_dtype dt,
+                       nm_math math, int64_t m_hint, void* buf, int64_t buf_bytes, nm_prepacked* out, void* stream) {
     nm_status st = check_common(0, n, k, N, M, L);
     if (st) return st;
     if (!out || (n * k > 0 && (!values || !idx))) return fail(NM_ERR_NULL, "nm_prepack: NULL pointer");
@@ -864,7 +881,7 @@ nm_status nm_prepack_ex(const void* values, const uint8_t* idx, int64_t n, int64
     } else if (kind) {
         if (!buf) return fail(NM_ERR_NULL, "nm_prepack: buffer missing (size: nm_prepack_size)");
         if ((st = require_device())) return st;
-        const int H = tc_sp_halves(N, M, L);
+        const int H = prepack_halves(m_hint, n, k, N, M, L);
         // exact size check when the buffer is below the data-independent bound (synchronizes)
         const bool check = buf_bytes < static_cast<int64_t>(tc_sp_prepack_bytes(n, k, N, M, L, kind == 3));
         int64_t need = 0;

@@ -32,7 +32,7 @@ EXPORTS = ["nm_version", "nm_last_error", "nm_check_config", "nm_compress", "nm_
            "nm_spmm_peers", "nm_peer_barrier", "nm_spmm_prepacked_peers", "nm_spmm_scaled", "nm_prepack_size",
            "nm_index_packed_words", "nm_index_pack", "nm_index_unpack", "nm_mc_supported", "nm_mc_create",
            "nm_mc_export", "nm_mc_import", "nm_mc_add_device", "nm_mc_bind_map", "nm_mc_free", "nm_spmm_mc",
-           "nm_spmm_at", "nm_spmm_prepacked_at"]
+           "nm_spmm_at", "nm_spmm_prepacked_at", "nm_prepack_size_m", "nm_prepack_m"]
 
 
 class NmError(RuntimeError):
@@ -98,6 +98,8 @@ def lib():
         L.nm_prepack_bytes_ex.restype = I64
         L.nm_prepack_ex.argtypes = [P, P, I64, I64, I, I, I, I, I, P, I64, ctypes.POINTER(Prepacked), P]
         L.nm_prepack_size.argtypes = [P, P, I64, I64, I, I, I, I, I, ctypes.POINTER(I64), P]
+        L.nm_prepack_size_m.argtypes = [P, P, I64, I64, I, I, I, I, I, I64, ctypes.POINTER(I64), P]
+        L.nm_prepack_m.argtypes = [P, P, I64, I64, I, I, I, I, I, I64, P, I64, ctypes.POINTER(Prepacked), P]
         L.nm_index_packed_words.argtypes = [I64, I64, I, I, I]
         L.nm_index_packed_words.restype = I64
         L.nm_index_pack.argtypes = [P, I64, I64, I, I, I, P, P]
@@ -284,20 +286,21 @@ class PrepackedWeight:
     '''A weight after nm_prepack (the paper's offline PreProcessing): keeps the
     original NmWeight (referenced by the descriptor), the device buffer and the descriptor.'''
 
-    def __init__(self, W: NmWeight, stream=None, math: str = "auto"):
+    def __init__(self, W: NmWeight, stream=None, math: str = "auto", m_hint: int | None = None):
         self.W = W
+        mh = int(m_hint or 0)
         dt = _dt(W.values)
         if lib().nm_prepack_bytes_ex(W.n, W.k, W.N, W.M, W.L, dt, MATH[math]) < 0:
             raise NmError(2, "nm_prepack_bytes", "bad shape")
         # the exact size of the compact slot images (one packing pass; synchronizes the stream)
         nb = ctypes.c_int64(0)
-        _check(lib().nm_prepack_size(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt, MATH[math],
-                                     ctypes.byref(nb), _stream(W.values, stream)), "nm_prepack_size")
+        _check(lib().nm_prepack_size_m(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt, MATH[math],
+                                       mh, ctypes.byref(nb), _stream(W.values, stream)), "nm_prepack_size")
         nbytes = int(nb.value)
         self.buf = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=W.values.device)
         self.desc = Prepacked()
-        _check(lib().nm_prepack_ex(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt, MATH[math],
-                                   self.buf.data_ptr(), int(nbytes), ctypes.byref(self.desc), _stream(W.values, stream)),
+        _check(lib().nm_prepack_m(W.values.data_ptr(), W.idx.data_ptr(), W.n, W.k, W.N, W.M, W.L, dt, MATH[math], mh,
+                                  self.buf.data_ptr(), int(nbytes), ctypes.byref(self.desc), _stream(W.values, stream)),
                "nm_prepack")
 
     @property
@@ -308,9 +311,10 @@ class PrepackedWeight:
         return getattr(self.W, name)
 
 
-def nm_prepack(W: NmWeight, stream=None, math: str = "auto") -> PrepackedWeight:
-    """math="tf32_tc" on an fp32 weight prepares the tf32 sparse-tensor-core path (kind 3)."""
-    return PrepackedWeight(W, stream, math)
+def nm_prepack(W: NmWeight, stream=None, math: str = "auto", m_hint: int | None = None) -> PrepackedWeight:
+    """math="tf32_tc" on an fp32 weight prepares the tf32 sparse-tensor-core path (kind 3); m_hint =
+    the expected token count lets the slot prepack pick its tile for that m (nm_prepack_m)."""
+    return PrepackedWeight(W, stream, math, m_hint)
 
 
 def nm_spmm_prepacked(A: torch.Tensor, PW: PrepackedWeight, out: torch.Tensor | None = None, out_dtype=None,

@@ -97,14 +97,16 @@ class ShardedNmLinear:
     (all-gather + unshard kernel) or "p2p" (fused peer-store epilogue: fp32 SIMT kernel, or the bf16
     sparse-tensor-core kernel's direct-store epilogue)."""
 
-    def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl", all_gather=None, chunks: int = 1):
+    def __init__(self, local_weight, n: int, group=None, exchange: str = "nccl", all_gather=None, chunks: int = 1,
+                 m_hint: int | None = None):
         from . import nmspmm
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' or 'p2p'")
         self.W = local_weight  # nmspmm.NmWeight of this rank's padded shard
         # the offline weight prepack (P:470-475) once per layer: the bf16 sparse-tensor-core
         # kernel's slot packing and images; plain values/idx for the fp32 path
-        self.PW = nmspmm.nm_prepack(local_weight) if local_weight.values.is_cuda else None
+        # m_hint: the expected token count, so the slot prepack picks the tile nm_spmm would (nm_prepack_m)
+        self.PW = nmspmm.nm_prepack(local_weight, m_hint=m_hint) if local_weight.values.is_cuda else None
         self.group = group
         self.G = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
@@ -132,7 +134,7 @@ class ShardedNmLinear:
 
     @classmethod
     def from_dense(cls, B: torch.Tensor, N: int, M: int, L: int, group=None, exchange: str = "nccl", all_gather=None,
-                   chunks: int = 1):
+                   chunks: int = 1, m_hint: int | None = None):
         """Compress only this rank's columns (compression is per column group, so
         the shard of compress(B) equals compress of the shard)."""
         from . import nmspmm
@@ -145,7 +147,7 @@ class ShardedNmLinear:
         Bs[:, :(g1 - g0) * L] = B[:, g0 * L:g1 * L]
         # padding groups are all-zero: compress gives zero values and the pattern 0..N-1
         W = nmspmm.nm_compress(Bs.contiguous(), N, M, L)
-        return cls(W, n, group, exchange, all_gather, chunks)
+        return cls(W, n, group, exchange, all_gather, chunks, m_hint)
 
     def local(self, A: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         from . import nmspmm

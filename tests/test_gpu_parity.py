@@ -914,3 +914,22 @@ def test_spmm_at_rejects(nm):
     At2 = torch.zeros((128, 64), device="cuda")
     with pytest.raises(nm.NmError):
         nm.nm_spmm_at(At2, W2, m=65)
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L,bn_hint", [(512, 1024, 1024, 16, 32, 32, 128),   # small grid: H = 1
+                                                 (4096, 4096, 1024, 16, 32, 32, 256)])  # large grid: H = 2 stays
+def test_prepack_m_hint(nm, oracle, m, n, k, N, M, L, bn_hint):
+    """nm_prepack_m: with the token count known the slot prepack takes the tile nm_spmm would (H = 1
+    when H = 2 leaves the grid under two waves); results are exact on integer inputs either way."""
+    A = synth.integer((m, k), 81, synth.TID_A)
+    B = synth.integer((k, n), 82, synth.TID_B)
+    vals, D = oracle.compress(synth.to_bf16_bits(B), N, M, L)
+    W = nm.NmWeight(dev(oracle.bf16_to_f32(vals), torch.bfloat16), dev(D, torch.uint8), k, N, M, L)
+    ref = oracle.spmm_sparse_f64(synth.to_bf16_bits(A), vals, D, k, N, M, L)
+    Ad = dev(A, torch.bfloat16)
+    PW0, PWm = nm.nm_prepack(W), nm.nm_prepack(W, m_hint=m)
+    assert PW0.kind == PWm.kind == 2 and PW0.desc.bn == 256 and PWm.desc.bn == bn_hint
+    for PW in (PW0, PWm):
+        C = nm.nm_spmm_prepacked(Ad, PW, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert np.array_equal(C.cpu().numpy().astype(np.float64), ref)
