@@ -1,5 +1,5 @@
-"""A/B of the bf16 slot kernel: weights in TMEM (NM_SP_TW=1, Cfg TW) vs shared memory (NM_SP_TW=0),
-per token tile NT, on the BASELINE shapes.  Kernel time from nm_profile (CUDA events around the
+"""A/B of the bf16 slot kernel by an environment switch (SP_ENV, default NM_SP_TW: weights in TMEM,
+the round-2 study; NM_SP_PERSIST: the persistent form), per token tile NT, on the BASELINE shapes.  Kernel time from nm_profile (CUDA events around the
 SpMM launch, 20 launches after 3 warm-ups); C of every variant is compared with the TW=0 default
 (bit-identical expected: same slots, same MMA K order) and with cuBLAS on the decompressed weight.
 Usage: sp_tw_ab.py [m n k N M L ...] (groups of six), SP_NTS="0 192 176 160" (0 = selector)."""
@@ -58,7 +58,7 @@ for (m, n, k, N, M, L) in shapes:
     flops = 2.0 * m * n * (k // M * N)
     base = None
     for tw in (0, 1):
-        os.environ["NM_SP_TW"] = str(tw)
+        os.environ[os.environ.get("SP_ENV", "NM_SP_TW")] = str(tw)
         for nt in nts:
             if nt:
                 os.environ["NM_SP_NT"] = str(nt)
@@ -80,4 +80,4 @@ for (m, n, k, N, M, L) in shapes:
             print(f"{m}x{n}x{k} {N}:{M} L{L} tw={tw} nt={nt or 'sel'}: kernel {t:7.1f} us  {flops / t / 1e6:7.1f} TFLOP/s  "
                   f"{t_cub / t:5.2f}x cuBLAS ({t_cub:.1f} us)  rel_err {err:.2e}{same}", flush=True)
     os.environ.pop("NM_SP_NT", None)
-    os.environ.pop("NM_SP_TW", None)
+    os.environ.pop(os.environ.get("SP_ENV", "NM_SP_TW"), None)
