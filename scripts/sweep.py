@@ -22,8 +22,8 @@ for name in os.environ.get("SWEEP_DT", "f32,bf16").split(","):
         cub = None
         for N in (16, 12, 8, 4):
             for L in (4, 32, 64):
-                if (dt == torch.bfloat16 or math) and L == 4:
-                    continue  # no tensor-core kernel for L < 16 (the generic CUDA kernel runs); not swept
+                if math and L == 4:
+                    continue  # the tf32 tensor-core path needs L >= 16 (bf16 L = 4 runs the SIMT kernel, id 5)
                 cfg = (s, s, s, N, 32, L)
                 steps = 3 if s >= 8192 else 5
                 try:
