@@ -663,43 +663,57 @@ nm_status nm_spmm_host(const void* A_host, const void* values_host, const uint8_
             return st;
         }
     }
-    cudaStream_t hs = nullptr, ds = nullptr;
-    cudaEvent_t ev[2 * 9 + 1] = {};
+    // Two compute streams (the caller's s and cs2) alternate over the chunks: a chunk's SpMM may
+    // start while the previous one still runs, so the sub-wave grids of consecutive chunks share
+    // the SMs instead of each leaving some idle (CUPTI timeline: the chunked SpMMs, not the copies,
+    // are the critical path once the weights are up, profiles/r02l_host_timeline.txt).
+    cudaStream_t hs = nullptr, ds = nullptr, cs2 = nullptr;
+    cudaEvent_t ev[2 * 9 + 3] = {};
     auto cleanup = [&]() {
         for (cudaEvent_t x : ev)
             if (x) cudaEventDestroy(x);
         if (hs) cudaStreamDestroy(hs);
         if (ds) cudaStreamDestroy(ds);
+        if (cs2) cudaStreamDestroy(cs2);
         if (pbuf) cudaFreeAsync(pbuf, s);
     };
     cudaError_t ce = cudaStreamCreateWithFlags(&hs, cudaStreamNonBlocking);
     if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&ds, cudaStreamNonBlocking);
-    for (int i = 0; ce == cudaSuccess && i < 2 * nck + 1; ++i) ce = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    if (ce == cudaSuccess) ce = cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking);
+    for (int i = 0; ce == cudaSuccess && i < 2 * nck + 3; ++i) ce = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    cudaEvent_t ev_w = ev[2 * nck + 1], ev_c2 = ev[2 * nck + 2];
+    if (ce == cudaSuccess) ce = cudaEventRecord(ev_w, s);  // the weights (and the slot prepack) are ready
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(cs2, ev_w, 0);
     for (int i = 0; ce == cudaSuccess && i < nck; ++i) {
         const int64_t r0 = rb[i], r1 = rb[i + 1];
         if (r0 >= r1) continue;
+        cudaStream_t cs = (i & 1) ? cs2 : s;
         ce = cudaMemcpyAsync(dA + r0 * k * e, static_cast<const uint8_t*>(A_host) + r0 * k * e,
                              static_cast<size_t>((r1 - r0) * k * e), cudaMemcpyHostToDevice, hs);
         if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * i], hs);
-        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * i], 0);
+        if (ce == cudaSuccess) ce = cudaStreamWaitEvent(cs, ev[2 * i], 0);
         if (ce != cudaSuccess) break;
-        st = slot ? tc_sp_run(dA + r0 * k * e, pbuf, hsp, dC + r0 * n * ec, c_dt == NM_BF16, r1 - r0, n, k, N, M, L, tf, s)
-                  : nm_spmm(dA + r0 * k * e, dV, dD, dC + r0 * n * ec, r1 - r0, n, k, N, M, L, ab_dt, c_dt, math, stream);
+        st = slot ? tc_sp_run(dA + r0 * k * e, pbuf, hsp, dC + r0 * n * ec, c_dt == NM_BF16, r1 - r0, n, k, N, M, L, tf, cs)
+                  : nm_spmm(dA + r0 * k * e, dV, dD, dC + r0 * n * ec, r1 - r0, n, k, N, M, L, ab_dt, c_dt, math, cs);
         if (st) {
             cudaStreamSynchronize(s);
+            cudaStreamSynchronize(cs2);
             cudaStreamSynchronize(hs);
             cleanup();
             return st;
         }
-        ce = cudaEventRecord(ev[2 * i + 1], s);
+        ce = cudaEventRecord(ev[2 * i + 1], cs);
         if (ce == cudaSuccess) ce = cudaStreamWaitEvent(ds, ev[2 * i + 1], 0);
         if (ce == cudaSuccess)
             ce = cudaMemcpyAsync(static_cast<uint8_t*>(C_host) + r0 * n * ec, dC + r0 * n * ec,
                                  static_cast<size_t>((r1 - r0) * n * ec), cudaMemcpyDeviceToHost, ds);
     }
+    if (ce == cudaSuccess) ce = cudaEventRecord(ev_c2, cs2);
+    if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev_c2, 0);  // before pbuf is released on s
     if (ce == cudaSuccess) ce = cudaEventRecord(ev[2 * nck], ds);
     if (ce == cudaSuccess) ce = cudaStreamWaitEvent(s, ev[2 * nck], 0);  // the caller's stream sees C_host
     const cudaError_t se = cudaStreamSynchronize(s);
+    cudaStreamSynchronize(cs2);
     cudaStreamSynchronize(hs);
     cudaStreamSynchronize(ds);
     cleanup();
