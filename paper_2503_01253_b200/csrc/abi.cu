@@ -232,7 +232,7 @@ nm_status index_pack_launch(const uint8_t* D, uint32_t* P, int64_t k, int64_t n,
 bool simt_f32_applicable(const void* A, const void* Bv, const void* C, int64_t m, int64_t n, int64_t k, int N, int M,
                          int L);
 void simt_f32_geometry(int N, int M, int* wp, int* bk, int* bkw);
-int simt_split_factor(int ntiles, int64_t w, int npanels);
+int simt_split_factor(int ntiles, int64_t w, int npanels, int bm);
 int simt_row_tile(int64_t m, int64_t n, int64_t w);
 nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, float* C, int64_t m, int64_t n, int64_t k,
                           int N, int M, int L, int mode, cudaStream_t s, const PeerOut* po = nullptr,
@@ -751,7 +751,7 @@ nm_status nm_plan_query(int64_t m, int64_t n, int64_t k, int N, int M, int L, nm
         out->threads = 2 * bm;
         const int64_t tiles = ceil_div(m, bm) * ceil_div(n, 128);
         const int npanels = static_cast<int>(ceil_div(k / M, wp));
-        const int sp = bm == 128 || getenv("NM_SIMT_SPLIT") ? simt_split_factor(static_cast<int>(tiles), w, npanels) : 1;
+        const int sp = simt_split_factor(static_cast<int>(tiles), w, npanels, bm);
         const int64_t resident = (bm == 128 ? 2 : 3) * static_cast<int64_t>(sms);
         out->split = sp;
         out->split_tiles = sp > 1 ? static_cast<int32_t>(tiles % resident) : 0;

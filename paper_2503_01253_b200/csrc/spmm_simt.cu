@@ -545,12 +545,24 @@ int simt_row_tile(int64_t m, int64_t n, int64_t w) {
 // Measured on B200 (pipelined kernel, profiles/r02c_simt_streamk.txt table 1) this picks the
 // fastest S of {1, 2, 3, 4} at all 11 shapes timed (BASELINE tails, m = 256, the 8-GPU shards of
 // cfg2 / cfg3 / cfg4, 1024^3 and 2048^3).  NM_SIMT_SPLIT overrides (never for whole waves).
-int simt_split_factor(int ntiles, int64_t w, int npanels) {
+int simt_split_factor(int ntiles, int64_t w, int npanels, int bm) {
     const int sms = num_sms(), resident = 2 * sms;
     if (ntiles <= 0 || npanels < 2 || (ntiles >= resident && ntiles % resident == 0)) return 1;
     const char* e = getenv("NM_SIMT_SPLIT");  // timing studies / tests
     if (e) return std::max(1, std::min(atoi(e), std::min(4, npanels / 2)));
     int S = 1;
+    if (bm == 64) {
+        // the 64-row tile splits only grids whose split CTAs all run alone on their SMs, with >= 128
+        // compressed rows per part: measured (profiles/r02v_simt_small_split.txt) 512x1024x1024
+        // 16:32 39.0 -> 31.1 us, 512^3 27.5 -> 25.2; 1024^3 (128 x 2 CTAs > SMs) and cfg1 (w = 128)
+        // lose with any split
+        for (int c = 4; c >= 2; --c)
+            if (static_cast<int64_t>(ntiles) * c <= sms && w / c >= 128) {
+                S = c;
+                break;
+            }
+        return std::min(S, std::max(1, npanels / 2));
+    }
     if (ntiles >= resident) {
         const int rem = ntiles % resident;
         if (rem > 0 && 2 * rem <= sms) S = std::min(3, sms / rem);
@@ -658,9 +670,8 @@ nm_status simt_f32_launch(const float* A, const float* Bv, const uint8_t* D, flo
     const int ntiles = ntiles_n * static_cast<int>(ceil_div(m, bm));
     const int resident = 2 * num_sms();  // 2 CTAs per SM (launch bounds, ~105 KB smem)
     const int rem = ntiles % resident;
-    // the wave-model split is tuned for the 128-row tile; the 64-row tile is itself the sub-wave
-    // answer (NM_SIMT_SPLIT still forces a split for tests / studies)
-    const int split = bm == 128 || getenv("NM_SIMT_SPLIT") ? simt_split_factor(ntiles, w, p.npanels) : 1;
+    // the wave-model split of the 128-row tile, or the 64-row tile's split of very small grids
+    const int split = simt_split_factor(ntiles, w, p.npanels, bm);
     p.split = split;
     p.full_tiles = split > 1 ? ntiles - rem : ntiles;
     float* ws = nullptr;

@@ -137,6 +137,26 @@ def test_plan_simt_split_matches_measured_best(L, monkeypatch, cfg, best):
     assert abs(p["waves"] - p["grid"] / 296) < 1e-9
 
 
+# The 64-row tile's split (small grids whose split CTAs all run alone) pinned to the fastest
+# measured S (profiles/r02v_simt_small_split.txt, NM_SIMT_BM=64 with NM_SIMT_SPLIT 1..4).
+SPLIT64_MEASURED = [
+    ((512, 1024, 1024, 16, 32, 32), 2),    # 64 tiles: 31.1 vs 39.0 us
+    ((512, 512, 512, 16, 32, 32), 2),      # 32 tiles, w = 256: 25.2 vs 27.5
+    ((1024, 1024, 1024, 16, 32, 32), 1),   # 128 tiles: 2 x 128 > 148 SMs (46.0 vs 39.6)
+    ((1024, 1024, 1024, 4, 32, 32), 1),    # 23.4 vs 30.4
+    ((256, 256, 256, 2, 4, 4), 1),         # cfg1: w = 128 too short (21.2 vs 22.3)
+]
+
+
+@pytest.mark.parametrize("cfg,best", SPLIT64_MEASURED)
+def test_plan_simt_split64(L, cfg, best):
+    from paper_2503_01253_b200 import nmspmm
+    import torch
+    p = nmspmm.nm_plan_query(*cfg, torch.float32)
+    assert p["kernel"] == 1 and p["bm"] == 64, p
+    assert p["split"] == best, p
+
+
 # The bf16 slot kernel's geometry for nm_spmm (per-call prepack: m known) pinned to the choices the
 # A-F study and the BASELINE timings support (profiles/r02e_protocol_summary.txt,
 # profiles/r02g_protocol_af_after_retune.csv, profiles/r02g_sp_tmem_weights_ab.txt): bn = 128 H output
