@@ -131,7 +131,9 @@ static int sp_est_stages(int64_t k, int N, int M, int L, int H, bool tf) {
 
 static int sp_halves_m(int L, int N, int M, int64_t m, int64_t n, int64_t k) {
     const int H = sp_halves(L, N, M);
-    if (H != 2 || N == M || std::getenv("NM_SP_H")) return H;
+    // (N = M included: the A-F study at 0 % also prefers H = 1 on grids under two waves, A-E 9-23 %
+    // faster, profiles/r02w_protocol_summary.txt)
+    if (H != 2 || std::getenv("NM_SP_H")) return H;
     const int nt = sp_tokens(2, m, n, sp_est_stages(k, N, M, L, 2, false));
     const int64_t tiles = ((n + 255) / 256) * ((m + nt - 1) / nt);
     return tiles >= 2 * static_cast<int64_t>(num_sms()) ? 2 : 1;

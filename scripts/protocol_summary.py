@@ -1,13 +1,24 @@
 """Summarise scripts/paper_protocol.py's CSVs (v123 and af studies): the step-wise table at 4096^3
 and, per (matrix, dtype, sparsity), the selector's kernel rate, the best variant and the selector's
 loss to it.  Usage: protocol_summary.py v123.csv af.csv"""
-import csv
 import sys
 from collections import defaultdict
 
 
 def rows(path):
-    return [r for r in csv.DictReader(open(path)) if r.get("kernel_tflops")]
+    """paper_protocol.py writes variant names with commas unquoted: the last six fields are fixed."""
+    out = []
+    lines = open(path).read().splitlines()
+    hdr = lines[0].split(",")
+    for line in lines[1:]:
+        f = line.split(",")
+        if len(f) < len(hdr):
+            continue
+        fixed = f[:8] + [",".join(f[8:len(f) - 6])] + f[len(f) - 6:]
+        r = dict(zip(hdr, fixed))
+        if r.get("kernel_tflops"):
+            out.append(r)
+    return out
 
 
 v123, af = rows(sys.argv[1]), rows(sys.argv[2])

@@ -169,7 +169,8 @@ SLOT_GEOMETRY = [
     ((2048, 22016, 8192, 4, 32, 32), 128, 256),    # cfg4 87.5 %: H = 1
     ((2048, 4096, 4096, 12, 32, 32), 128, 256),    # A-F "E" 62.5 %: H = 2 would be < 2 waves -> H = 1
     ((1024, 2048, 2048, 16, 32, 32), 128, 128),    # A-F "D" 50 %: small grid -> H = 1, NT = 128
-    ((512, 512, 512, 32, 32, 32), 256, 128),       # N = M: H = 2 always; 8 tiles -> the smallest NT
+    ((512, 512, 512, 32, 32, 32), 128, 128),       # N = M, small grid: H = 1 (A-F 'A' at 0 %: 19.5 vs 15.9 TF)
+    ((4096, 4096, 4096, 32, 32, 32), 256, 192),    # N = M, 4096^3: H = 2 (352 tiles)
 ]
 
 
