@@ -933,3 +933,32 @@ def test_prepack_m_hint(nm, oracle, m, n, k, N, M, L, bn_hint):
         C = nm.nm_spmm_prepacked(Ad, PW, out_dtype=torch.float32)
         torch.cuda.synchronize()
         assert np.array_equal(C.cpu().numpy().astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("m,n,k,N,M,L,split", [(512, 1024, 1024, 16, 32, 32, 2),   # 64-row tile, split 2
+                                               (512, 512, 512, 16, 32, 32, 2),
+                                               (200, 384, 768, 8, 32, 32, 0)])     # whatever the selector picks
+def test_simt_small_grid_split_exact(nm, oracle, m, n, k, N, M, L, split):
+    """The 64-row tile's k-split of small grids (fixed-order partial sums) on integer inputs: fp32 C
+    equals the oracle exactly; the selector's split is the pinned one."""
+    p = nm.nm_plan_query(m, n, k, N, M, L, torch.float32)
+    if split:
+        assert p["bm"] == 64 and p["split"] == split, p
+    A = synth.integer((m, k), 91, synth.TID_A)
+    vals, D = oracle.compress(synth.integer((k, n), 92, synth.TID_B), N, M, L)
+    W = nm.NmWeight(dev(vals), dev(D, torch.uint8), k, N, M, L)
+    C = nm.nm_spmm(dev(A), W, math="f32_simt")
+    torch.cuda.synchronize()
+    assert np.array_equal(C.cpu().numpy().astype(np.float64), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L))
+
+
+def test_host_path_bf16_simt_fallback(nm, oracle):
+    """nm_spmm_host with bf16 operands at L = 4 (the SIMT fallback, kernel 5): integer inputs exact."""
+    m, n, k, N, M, L = 300, 256, 512, 8, 32, 4
+    A = synth.integer((m, k), 93, synth.TID_A)
+    vals, D = oracle.compress(synth.integer((k, n), 94, synth.TID_B), N, M, L)
+    run = nm.HostSpmm(m, n, k, N, M, L, ab_dtype=torch.bfloat16, c_dtype=torch.float32)
+    C = torch.full((m, n), float("nan")).pin_memory()
+    run(torch.from_numpy(A).to(torch.bfloat16).pin_memory(), torch.from_numpy(vals).to(torch.bfloat16).pin_memory(),
+        torch.from_numpy(D).pin_memory(), C)
+    assert np.array_equal(C.numpy().astype(np.float64), oracle.spmm_sparse_f64(A, vals, D, k, N, M, L))
